@@ -1,0 +1,309 @@
+#!/usr/bin/env python
+"""PGD-TO optimizer-step benchmark (BASELINE.json metric: design vars/s and
+achieved HBM GB/s).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step = one PGD-TO optimizer step (BB step + PR+ direction + rho_tilde +
+linearization + projection + x_{t+1}) over one synthetic batch with the
+BASELINE config's shapes (seeded; the FE solve / filter are outside the hot
+path and replaced by synthetic sensitivities).  `value` is device-timed with
+inputs resident in HBM; `e2e` is the same metric through the host-buffer
+C-ABI call (pinned H2D of every input and D2H of x_{t+1} and d inside the
+timed region).  L2 is flushed (256 MiB write) between timed steps.
+
+--impl reference times the reference's own CPU projection (oracle/_ref: the
+reference projection.cpp compiled in place) plus the spec step restatement,
+single-threaded, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_VAR = {"C1": 64, "C2": 64, "C3": 64, "C4": 112, "C4p": 112, "C5": 112}
+METRIC = "PGD-TO step throughput (design vars/s)"
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def make_problem(config, seed, rank=0):
+    from paper_2511_13905_b200 import synth
+    return synth.CONFIGS[config](seed + 1000 * rank)
+
+
+def cpu_reference_sample(p, budget_s=12.0, max_reps=50):
+    """The reference's CPU path on this host: spec step (oracle.c) + the
+    reference's own build+project (oracle/_ref), 1 thread, a bounded sample."""
+    import oracle as O
+    kind = "reference" if O.ref_available() else "port"
+    reps, t0 = 0, time.perf_counter()
+    while reps < max_reps:
+        d, gd, rt, info = O.step_direction(p.x, p.x_prev, p.g, p.g_prev, p.d_prev, p.t,
+                                           p.violation)
+        if kind == "reference":
+            O.ref_project(rt, p.grad, p.g_values, p.bounds_g, gd, p.is_eq, p.partition,
+                          p.lower, p.upper)
+        else:
+            O.project(rt, p.grad, p.g_values, p.bounds_g, gd, p.is_eq, p.partition, p.lower,
+                      p.upper)
+        reps += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": p.n * reps / dt, "unit": "design vars/s", "cores": 1, "kind": kind,
+            "sample": f"{reps} full steps of {p.name} (n={p.n}), single-threaded, "
+                      f"{dt:.1f} s", "ms_per_step": 1e3 * dt / reps}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    p = make_problem(args.config, args.seed)
+    # each "step" is the bounded sample of one full reference step
+    for _ in range(args.warmup):
+        cpu_reference_sample(p, budget_s=0.0, max_reps=1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_reference_sample(p, budget_s=0.0, max_reps=1)
+    dt = (time.perf_counter() - t0) / args.steps
+    import oracle as O
+    kind = "reference" if O.ref_available() else "port"
+    val = p.n / dt
+    line = {"metric": METRIC, "value": val, "unit": "design vars/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE.json config distributions)",
+            "config": {"workload": p.name, "n": p.n, "m": p.m, "seed": args.seed},
+            "impl": "reference",
+            "cpu_baseline": {"value": val, "unit": "design vars/s", "cores": 1, "kind": kind,
+                             "sample": f"{args.steps} full steps of {p.name}, 1 thread "
+                                       "(the reference is single-threaded)"},
+            "e2e": {"value": val, "unit": "design vars/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world):
+    import numpy as np
+    import torch
+    from paper_2511_13905_b200 import _lib, api
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    p = make_problem(args.config, args.seed, rank)
+    n, m = p.n, p.m
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{dev}")  # noqa: E731
+    X = {k: cu(getattr(p, k)) for k in ("x", "x_prev", "g", "g_prev", "d_prev")}
+    A = cu(p.grad.reshape(-1))
+    outs = {k: torch.empty(n, dtype=torch.float64, device=f"cuda:{dev}")
+            for k in ("x_new", "d", "rho_tilde")}
+    ctx = _lib.context(dev)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+
+    def step():
+        return api.pgd_step(X["x"], X["x_prev"], X["g"], X["g_prev"], X["d_prev"], A,
+                            p.g_values, p.bounds_g, p.is_eq, p.partition, t=p.t,
+                            violation=p.violation, lower=p.lower, upper=p.upper, device=dev,
+                            out=outs)
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(dev)
+    clocks.start()
+    launches0 = ctx.launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    kern_ms = []
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.fill_(k & 0xff)                        # evict L2 between timed steps
+        ev[k][0].record(stream)
+        res = step()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    launches = ctx.launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = sum(step_ms) / len(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    clk = clocks.stop()
+
+    # ---- e2e: host-buffer C-ABI call, pinned H2D inputs + D2H x_new, d --------
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    H = {k: pin(getattr(p, k)) for k in ("x", "x_prev", "g", "g_prev", "d_prev")}
+    HA = pin(p.grad)
+    e2e_steps = max(3, min(args.steps, 10))
+    api.pgd_step(H["x"], H["x_prev"], H["g"], H["g_prev"], H["d_prev"], HA, p.g_values,
+                 p.bounds_g, p.is_eq, p.partition, t=p.t, device=dev, host_outputs=("x_new", "d"))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        api.pgd_step(H["x"], H["x_prev"], H["g"], H["g_prev"], H["d_prev"], HA, p.g_values,
+                     p.bounds_g, p.is_eq, p.partition, t=p.t, device=dev,
+                     host_outputs=("x_new", "d"))
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    h2d = 8 * n * (5 + m)
+    d2h = 8 * n * 2
+
+    if rank != 0:
+        return
+    peak, peak_kind = measured_peak()
+    b_alg = BYTES_PER_VAR.get(args.config, 64) * n
+    total_n = n * world
+    value = total_n / (ms * 1e-3)
+    # dominant kernel: k_pass (every pass of the step is one launch of it)
+    kern = kernel_pass_stats(ctx, step, min(args.steps, 10), flush)
+    per_launch_bytes = b_alg / max(1.0, kern["launches"] / max(1, min(args.steps, 10)))
+    avg_launch_ms = kern.get("avg_ms")
+    achieved = (per_launch_bytes / (avg_launch_ms * 1e-3) / 1e9) if avg_launch_ms else \
+        (b_alg / (ms * 1e-3) / 1e9)
+    cpu = cpu_reference_sample(make_problem(args.config, args.seed), budget_s=args.cpu_budget)
+    line = {
+        "metric": METRIC, "value": value, "unit": "design vars/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json config distributions)",
+        "config": {"workload": p.name, "n": n, "m": m, "seed": args.seed,
+                   "l2": "flushed (256 MiB write) between timed steps",
+                   "path": res.projection.path.name,
+                   "passes_per_step": res.projection.passes,
+                   "sweeps_per_step": res.projection.sweeps,
+                   "near_ties": res.projection.near_ties},
+        "achieved_hbm_gbs_step": b_alg / (ms * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
+                     "kernel": "k_pass", "alg_bytes_per_var": BYTES_PER_VAR.get(args.config, 64),
+                     "avg_launch_ms": avg_launch_ms, "max_launch_ms": kern.get("max_ms"),
+                     "kernel_ms_per_step": kern.get("total_ms_per_step")},
+        "cpu_baseline": cpu,
+        "e2e": {"value": total_n / (e2e_ms * 1e-3), "unit": "design vars/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def ctx_kernel_stats(ctx):
+    return {}
+
+
+def kernel_pass_stats(ctx, step, steps, flush):
+    """Average device duration of one k_pass launch (CUDA events on the
+    launching stream, inside the library), over `steps` extra steps."""
+    ctx.set_profiling(True)
+    ctx.kernel_time()
+    for k in range(steps):
+        flush.fill_(k & 0xff)
+        step()
+    total, nl, mx = ctx.kernel_time()
+    ctx.set_profiling(False)
+    return {"avg_ms": total / max(nl, 1), "launches": nl, "max_ms": mx,
+            "total_ms_per_step": total / max(steps, 1)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--seed", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch
+        backend = "gloo" if args.impl == "reference" else "nccl"
+        if backend == "nccl":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        torch.distributed.init_process_group(backend)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world)
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,184 @@
+"""ctypes binding of libtopt_b200.so (include/topt_b200.h).
+
+The shared library is built in-tree by ``paper_2511_13905_b200.build.build()``
+(``nvcc -gencode arch=compute_100a,code=sm_100a``).  There is no fallback:
+if the library or a CUDA device is missing every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtopt_b200.so")
+
+MAX_M = 16
+
+OK = 0
+ERR_PARAMETER, ERR_DOMAIN, ERR_SINGULAR, ERR_INFEASIBLE, ERR_NUMERICAL, ERR_UNSUPPORTED, \
+    ERR_CUDA, ERR_INTERNAL = range(1, 9)
+
+PROJECT_AUTO, PROJECT_SINGLE, PROJECT_INDEPENDENT, PROJECT_NEWTON = range(4)
+
+_dp = C.POINTER(C.c_double)
+
+
+class ProjOptions(C.Structure):
+    _fields_ = [("c", C.c_double), ("tol_b", C.c_double), ("tol_n", C.c_double),
+                ("newton_maxiter", C.c_int32), ("binary_maxiter", C.c_int32)]
+
+
+class PgdSettingsC(C.Structure):
+    _fields_ = [("alpha_max", C.c_double), ("alpha_fallback", C.c_double),
+                ("omega", C.c_double), ("eps_alpha", C.c_double), ("tol_n", C.c_double),
+                ("t_warmup", C.c_int32)]
+
+
+class ProjMeta(C.Structure):
+    _fields_ = [("path", C.c_int32), ("newton_iters", C.c_int32), ("converged", C.c_int32),
+                ("curvature_violations", C.c_int32), ("residual", C.c_double),
+                ("passes", C.c_int32), ("sweeps", C.c_int32), ("stage1_row", C.c_int32),
+                ("near_ties", C.c_int32), ("min_margin", C.c_double),
+                ("bisect_iters", C.c_int32 * MAX_M), ("alpha", C.c_double),
+                ("beta", C.c_double), ("fallback", C.c_int32), ("reserved", C.c_int32)]
+
+
+class Linearization(C.Structure):
+    _fields_ = [("num_constraints", C.c_size_t), ("num_vars", C.c_size_t),
+                ("grad", C.c_void_p), ("g_values", C.c_void_p), ("bounds_g", C.c_void_p),
+                ("gd_step", C.c_void_p), ("g_hat", C.c_void_p), ("g_hat_err", C.c_void_p),
+                ("is_equality", C.c_void_p), ("part_offsets", C.c_void_p),
+                ("part_indices", C.c_void_p), ("owner", C.c_void_p)]
+
+
+class StepProblem(C.Structure):
+    _fields_ = [("n", C.c_int64), ("m", C.c_int32), ("t", C.c_int32),
+                ("violation", C.c_double), ("lower", C.c_double), ("upper", C.c_double),
+                ("x", C.c_void_p), ("x_prev", C.c_void_p), ("g", C.c_void_p),
+                ("g_prev", C.c_void_p), ("d_prev", C.c_void_p), ("grad", C.c_void_p),
+                ("g_values", C.c_void_p), ("bounds_g", C.c_void_p),
+                ("is_equality", C.c_void_p), ("part_offsets", C.c_void_p),
+                ("part_indices", C.c_void_p), ("owner", C.c_void_p)]
+
+
+class StepOutputs(C.Structure):
+    _fields_ = [("x_new", C.c_void_p), ("d", C.c_void_p), ("rho_tilde", C.c_void_p),
+                ("delta", C.c_void_p), ("y", C.c_void_p), ("slacks", C.c_void_p),
+                ("g_hat", C.c_void_p), ("mask", C.c_void_p)]
+
+
+EXPORTS = [
+    "topt_b200_version", "topt_b200_ctx_create", "topt_b200_ctx_destroy",
+    "topt_b200_last_error", "topt_b200_kernel_launches", "topt_b200_get_stream",
+    "topt_b200_set_stream", "topt_b200_default_options", "topt_b200_default_settings",
+    "topt_b200_build", "topt_b200_delta_of_y", "topt_b200_constraint_residual_h",
+    "topt_b200_project", "topt_b200_project_dev", "topt_b200_owner_map",
+    "topt_b200_pgd_step", "topt_b200_pgd_step_dev", "topt_b200_step_direction",
+    "topt_b200_set_profiling", "topt_b200_kernel_time",
+]
+
+_lib = None
+
+
+def load():
+    """Load libtopt_b200.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with paper_2511_13905_b200.build.build() "
+            "(no CPU fallback exists)")
+    lib = C.CDLL(LIB_PATH)
+    lib.topt_b200_version.restype = C.c_char_p
+    lib.topt_b200_last_error.restype = C.c_char_p
+    lib.topt_b200_last_error.argtypes = [C.c_void_p]
+    lib.topt_b200_kernel_launches.restype = C.c_int64
+    lib.topt_b200_kernel_launches.argtypes = [C.c_void_p]
+    lib.topt_b200_get_stream.restype = C.c_void_p
+    lib.topt_b200_get_stream.argtypes = [C.c_void_p]
+    lib.topt_b200_ctx_destroy.argtypes = [C.c_void_p]
+    lib.topt_b200_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+    vp, d, i32, i64 = C.c_void_p, C.c_double, C.c_int32, C.c_int64
+    sig = {
+        "topt_b200_build": [vp, vp, vp, vp],
+        "topt_b200_delta_of_y": [vp, vp, vp, vp, d, d, vp],
+        "topt_b200_constraint_residual_h": [vp, vp, vp, vp, d, d, d, vp],
+        "topt_b200_project": [vp, C.c_int, vp, vp, d, d, vp, vp, vp, vp, vp],
+        "topt_b200_project_dev": [vp, C.c_int, vp, vp, d, d, vp, vp, vp, vp, vp, vp],
+        "topt_b200_owner_map": [vp, i64, i32, vp, vp, vp],
+        "topt_b200_pgd_step": [vp, vp, vp, vp, vp, vp],
+        "topt_b200_pgd_step_dev": [vp, vp, vp, vp, vp, vp],
+        "topt_b200_set_stream": [vp, vp],
+        "topt_b200_step_direction": [vp, i64, vp, vp, vp, vp, vp, i32, d, vp, vp, vp, vp, vp,
+                                     vp],
+        "topt_b200_set_profiling": [vp, C.c_int],
+        "topt_b200_kernel_time": [vp, vp, vp, vp],
+        "topt_b200_default_options": [vp],
+        "topt_b200_default_settings": [vp],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = None if name.startswith("topt_b200_default") else C.c_int
+    _lib = lib
+    return lib
+
+
+class Context:
+    """One CUDA device context of the library (stream, plan, workspaces)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load()
+        h = C.c_void_p()
+        rc = self.lib.topt_b200_ctx_create(int(device), C.byref(h))
+        if rc != OK:
+            raise RuntimeError(f"topt_b200_ctx_create(device={device}) failed with status {rc} "
+                               "(no CUDA device?)")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            self.lib.topt_b200_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def last_error(self) -> str:
+        return self.lib.topt_b200_last_error(self.h).decode()
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.topt_b200_kernel_launches(self.h))
+
+    @property
+    def stream(self) -> int:
+        return int(self.lib.topt_b200_get_stream(self.h) or 0)
+
+    def set_stream(self, stream_ptr: int):
+        self.lib.topt_b200_set_stream(self.h, C.c_void_p(stream_ptr))
+
+    def set_profiling(self, on: bool):
+        self.lib.topt_b200_set_profiling(self.h, 1 if on else 0)
+
+    def kernel_time(self):
+        """(total_ms, launches, max_ms) of profiled pass launches since the last call."""
+        t = C.c_double(0); n = C.c_int64(0); mx = C.c_double(0)
+        self.lib.topt_b200_kernel_time(self.h, C.byref(t), C.byref(n), C.byref(mx))
+        return t.value, n.value, mx.value
+
+
+_ctx = {}
+
+
+def context(device: int = 0) -> Context:
+    c = _ctx.get(device)
+    if c is None:
+        c = Context(device)
+        _ctx[device] = c
+    return c

@@ -1,0 +1,469 @@
+"""Python mirror of the reference's projection / optimizer-step interface.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/topt/projection.hpp:17-109 and errors.hpp:9-42
+(and SPEC.md:272-313 for the optimizer step, which has no reference code), so
+parity tests read like the reference's own tests.  Every function runs on the
+GPU through the C-ABI (include/topt_b200.h); there is no CPU path.
+
+Host numpy arrays use the host-buffer entry points (H2D/D2H inside the
+call); torch CUDA tensors use the *_dev entry points (no copies).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import enum
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+
+# ---- errors.hpp:9-42 ---------------------------------------------------------
+class ParameterError(ValueError):
+    """topt::ParameterError (std::invalid_argument)."""
+
+
+class DomainError(ValueError):
+    """topt::DomainError (std::domain_error)."""
+
+
+class SingularSystemError(RuntimeError):
+    """topt::SingularSystemError."""
+
+
+class InfeasibleLinearization(RuntimeError):
+    """topt::InfeasibleLinearization."""
+
+
+class NumericalError(RuntimeError):
+    """topt::NumericalError."""
+
+
+class UnsupportedProblem(RuntimeError):
+    """topt::UnsupportedProblem."""
+
+
+class CudaError(RuntimeError):
+    """CUDA runtime failure inside the library."""
+
+
+_ERRMAP = {L.ERR_PARAMETER: ParameterError, L.ERR_DOMAIN: DomainError,
+           L.ERR_SINGULAR: SingularSystemError, L.ERR_INFEASIBLE: InfeasibleLinearization,
+           L.ERR_NUMERICAL: NumericalError, L.ERR_UNSUPPORTED: UnsupportedProblem,
+           L.ERR_CUDA: CudaError, L.ERR_INTERNAL: RuntimeError}
+
+
+def _check(ctx: L.Context, rc: int):
+    if rc != L.OK:
+        raise _ERRMAP.get(rc, RuntimeError)(ctx.last_error())
+
+
+# ---- projection.hpp:43-64 ----------------------------------------------------
+class ProjectionPath(enum.IntEnum):
+    single_binary = 0
+    independent_binary = 1
+    newton = 2
+
+
+def to_string(path) -> str:
+    try:
+        return ProjectionPath(int(path)).name
+    except ValueError:
+        return "unknown"
+
+
+@dataclasses.dataclass
+class ProjectionOptions:
+    c: float = 1e12
+    tol_b: float = 1e-8
+    tol_n: float = 1e-6
+    newton_maxiter: int = 50
+    binary_maxiter: int = 200
+
+    def _c(self):
+        return L.ProjOptions(self.c, self.tol_b, self.tol_n, self.newton_maxiter,
+                             self.binary_maxiter)
+
+
+@dataclasses.dataclass
+class ProjectionResult:
+    delta: object
+    y: np.ndarray
+    slacks: np.ndarray
+    path: ProjectionPath = ProjectionPath.single_binary
+    newton_iters: int = 0
+    residual: float = 0.0
+    converged: bool = True
+    curvature_violations: int = 0
+    # diagnostics (not in the reference)
+    passes: int = 0
+    sweeps: int = 0
+    stage1_row: int = -1
+    near_ties: int = 0
+    min_margin: float = float("inf")
+    bisect_iters: Optional[list] = None
+    mask: object = None
+
+
+def _meta_to_result(meta: L.ProjMeta, delta, y, slacks, m, mask=None) -> ProjectionResult:
+    return ProjectionResult(
+        delta=delta, y=y, slacks=slacks, path=ProjectionPath(meta.path),
+        newton_iters=meta.newton_iters, residual=meta.residual,
+        converged=bool(meta.converged), curvature_violations=meta.curvature_violations,
+        passes=meta.passes, sweeps=meta.sweeps, stage1_row=meta.stage1_row,
+        near_ties=meta.near_ties, min_margin=meta.min_margin,
+        bisect_iters=list(meta.bisect_iters[:m]), mask=mask)
+
+
+def _is_torch_cuda(a) -> bool:
+    return hasattr(a, "is_cuda") and bool(a.is_cuda)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if _is_torch_cuda(a):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+def _f64(a):
+    if a is None or _is_torch_cuda(a):
+        return a
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _part_csr(partition, m):
+    if partition is None:
+        return None, None
+    if len(partition) != m:
+        raise DomainError("ConstraintLinearization: partition size != m")
+    off = np.zeros(m + 1, np.int64)
+    for j, p in enumerate(partition):
+        off[j + 1] = off[j] + len(p)
+    idx = (np.concatenate([np.asarray(p, dtype=np.int32).ravel() for p in partition])
+           if m else np.zeros(0, np.int32))
+    return off, np.ascontiguousarray(idx, dtype=np.int32)
+
+
+# ---- ConstraintLinearization (projection.hpp:17-41) --------------------------
+class ConstraintLinearization:
+    """Per-iteration linearization; g_hat is computed on the GPU by build()."""
+
+    def __init__(self):
+        self.num_constraints = 0
+        self.num_vars = 0
+        self.grad = None
+        self.g_values = None
+        self.bounds_g = None
+        self.gd_step = None
+        self.g_hat = None
+        self.g_hat_err = None
+        self.is_equality = None
+        self.partition = None
+        self._device = 0
+        self._owner = None
+
+    @staticmethod
+    def build(m, n, grad, g_values, bounds_g, gd_step, is_equality=None, partition=None,
+              device: int = 0) -> "ConstraintLinearization":
+        lin = ConstraintLinearization()
+        lin.num_constraints = int(m)
+        lin.num_vars = int(n)
+        lin._device = device
+        if _is_torch_cuda(grad):
+            lin.grad = grad.reshape(m, n) if m * n else grad
+        else:
+            lin.grad = np.ascontiguousarray(np.asarray(grad, np.float64).reshape(-1))
+        lin.g_values = np.ascontiguousarray(g_values, np.float64).reshape(-1)
+        lin.bounds_g = np.ascontiguousarray(bounds_g, np.float64).reshape(-1)
+        lin.gd_step = _f64(gd_step)
+        lin.is_equality = (np.zeros(m, np.uint8) if is_equality is None or len(is_equality) == 0
+                           else np.ascontiguousarray(is_equality, np.uint8))
+        lin.partition = partition
+        gsz = lin.grad.numel() if _is_torch_cuda(lin.grad) else lin.grad.size
+        gdsz = lin.gd_step.numel() if _is_torch_cuda(lin.gd_step) else np.asarray(lin.gd_step).size
+        if (gsz != m * n or lin.g_values.size != m or lin.bounds_g.size != m or gdsz != n
+                or lin.is_equality.size != m):
+            raise DomainError("ConstraintLinearization: inconsistent dimensions")
+        if not _is_torch_cuda(lin.grad):
+            lin.grad = lin.grad.reshape(m, n)
+        ctx = L.context(device)
+        g_hat = np.zeros(m)
+        g_err = np.zeros(m)
+        with _LinC(lin, need_gd=True) as lc:
+            if lc.device_mode:
+                raise DomainError("build() takes host arrays; use pgd_step_device for device data")
+            _check(ctx, ctx.lib.topt_b200_build(ctx.h, C.byref(lc.s), _ptr(g_hat), _ptr(g_err)))
+        lin.g_hat = g_hat
+        lin.g_hat_err = g_err
+        return lin
+
+    def row(self, j):
+        return self.grad[j]
+
+    def validate(self):
+        """Recheck g_hat (1e-14) and partition validity (projection.cpp:150-181)."""
+        m = self.num_constraints
+        if self.partition is not None and len(self.partition) != m:
+            raise DomainError("ConstraintLinearization: partition size != m")
+        fresh = ConstraintLinearization.build(m, self.num_vars, self.grad, self.g_values,
+                                              self.bounds_g, self.gd_step, self.is_equality,
+                                              self.partition, self._device)
+        for j in range(m):
+            expect = fresh.g_hat[j]
+            scale = max(1.0, abs(expect), abs(self.g_hat[j]))
+            if abs(self.g_hat[j] - expect) > 1e-14 * scale + self.g_hat_err[j]:
+                raise DomainError("ConstraintLinearization: g_hat inconsistent with fields")
+
+
+class _LinC:
+    """Builds the C topt_linearization view (keeps buffers alive)."""
+
+    def __init__(self, lin: ConstraintLinearization, need_gd=False, ghat=True):
+        self.lin = lin
+        self.need_gd = need_gd
+        self.ghat = ghat
+
+    def __enter__(self):
+        lin = self.lin
+        m = lin.num_constraints
+        self.device_mode = _is_torch_cuda(lin.grad)
+        self.off, self.idx = _part_csr(lin.partition, m)
+        s = L.Linearization()
+        s.num_constraints = m
+        s.num_vars = lin.num_vars
+        s.grad = _ptr(lin.grad)
+        s.g_values = _ptr(lin.g_values)
+        s.bounds_g = _ptr(lin.bounds_g)
+        s.gd_step = _ptr(lin.gd_step) if (self.need_gd and lin.gd_step is not None) else None
+        self._gh = None if lin.g_hat is None else np.ascontiguousarray(lin.g_hat, np.float64)
+        self._ge = None if lin.g_hat_err is None else np.ascontiguousarray(lin.g_hat_err,
+                                                                          np.float64)
+        s.g_hat = _ptr(self._gh)
+        s.g_hat_err = _ptr(self._ge)
+        s.is_equality = _ptr(lin.is_equality)
+        s.part_offsets = _ptr(self.off)
+        s.part_indices = _ptr(self.idx)
+        s.owner = None
+        self.s = s
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def _check_rho(lin, rho):
+    n = rho.numel() if _is_torch_cuda(rho) else np.asarray(rho).size
+    if n != lin.num_vars:
+        raise DomainError("projection: rho_tilde size does not match linearization")
+
+
+# ---- projection.hpp:66-109 ---------------------------------------------------
+def delta_of_y(y, lin: ConstraintLinearization, rho_tilde, lower, upper):
+    rho = _f64(rho_tilde)
+    _check_rho(lin, rho)
+    y = np.ascontiguousarray(y, np.float64)
+    if y.size != lin.num_constraints:
+        raise DomainError("delta_of_y: dual size does not match linearization")
+    ctx = L.context(lin._device)
+    out = np.empty(lin.num_vars)
+    with _LinC(lin) as lc:
+        _check(ctx, ctx.lib.topt_b200_delta_of_y(ctx.h, _ptr(y), C.byref(lc.s), _ptr(rho),
+                                                 C.c_double(lower), C.c_double(upper),
+                                                 _ptr(out)))
+    return out
+
+
+def constraint_residual_h(y, lin: ConstraintLinearization, rho_tilde, lower, upper, c):
+    rho = _f64(rho_tilde)
+    y = np.ascontiguousarray(y, np.float64)
+    if not (c > 0.0):
+        raise ParameterError("constraint_residual_h: c must be > 0")
+    _check_rho(lin, rho)
+    if y.size != lin.num_constraints:
+        raise DomainError("delta_of_y: dual size does not match linearization")
+    ctx = L.context(lin._device)
+    out = np.empty(lin.num_constraints)
+    with _LinC(lin) as lc:
+        _check(ctx, ctx.lib.topt_b200_constraint_residual_h(
+            ctx.h, _ptr(y), C.byref(lc.s), _ptr(rho), C.c_double(lower), C.c_double(upper),
+            C.c_double(c), _ptr(out)))
+    return out
+
+
+def _project(which, rho_tilde, lin, lower, upper, options: ProjectionOptions,
+             want_mask=False):
+    rho = _f64(rho_tilde)
+    _check_rho(lin, rho)
+    ctx = L.context(lin._device)
+    m, n = lin.num_constraints, lin.num_vars
+    y = np.zeros(m)
+    sl = np.zeros(m)
+    meta = L.ProjMeta()
+    opts = options._c()
+    with _LinC(lin, need_gd=lin.partition is not None) as lc:
+        if lc.device_mode:
+            import torch
+            delta = torch.empty(n, dtype=torch.float64, device=rho.device)
+            mask = torch.empty(n, dtype=torch.uint8, device=rho.device) if want_mask else None
+            if lin._owner is None and lin.partition is not None and m > 1:
+                lin._owner = torch.empty(n, dtype=torch.int8, device=rho.device)
+                _check(ctx, ctx.lib.topt_b200_owner_map(ctx.h, C.c_int64(n), C.c_int32(m),
+                                                        _ptr(lc.off), _ptr(lc.idx),
+                                                        C.c_void_p(lin._owner.data_ptr())))
+            lc.s.owner = None if lin._owner is None else lin._owner.data_ptr()
+            _check(ctx, ctx.lib.topt_b200_project_dev(
+                ctx.h, which, rho.data_ptr(), C.byref(lc.s), lower, upper, C.byref(opts),
+                delta.data_ptr(), mask.data_ptr() if mask is not None else None, _ptr(y),
+                _ptr(sl), C.byref(meta)))
+            return _meta_to_result(meta, delta, y, sl, m, mask)
+        delta = np.empty(n)
+        _check(ctx, ctx.lib.topt_b200_project(ctx.h, which, _ptr(rho), C.byref(lc.s),
+                                              C.c_double(lower), C.c_double(upper),
+                                              C.byref(opts), _ptr(delta), _ptr(y), _ptr(sl),
+                                              C.byref(meta)))
+    return _meta_to_result(meta, delta, y, sl, m)
+
+
+def project_single_binary_search(rho_tilde, lin, lower, upper, tol_b, binary_maxiter=200):
+    o = ProjectionOptions(tol_b=tol_b, binary_maxiter=binary_maxiter)
+    return _project(L.PROJECT_SINGLE, rho_tilde, lin, lower, upper, o)
+
+
+def project_independent(rho_tilde, lin, lower, upper, tol_b, binary_maxiter=200):
+    o = ProjectionOptions(tol_b=tol_b, binary_maxiter=binary_maxiter)
+    return _project(L.PROJECT_INDEPENDENT, rho_tilde, lin, lower, upper, o)
+
+
+def project_general_newton(rho_tilde, lin, lower, upper, options: ProjectionOptions = None):
+    return _project(L.PROJECT_NEWTON, rho_tilde, lin, lower, upper,
+                    options or ProjectionOptions())
+
+
+def project(rho_tilde, lin, lower, upper, options: ProjectionOptions = None, want_mask=False):
+    return _project(L.PROJECT_AUTO, rho_tilde, lin, lower, upper,
+                    options or ProjectionOptions(), want_mask)
+
+
+# ---- optimizer step ----------------------------------------
+@dataclasses.dataclass
+class PgdSettings:
+    alpha_max: float = 1e2
+    alpha_fallback: float = 0.2
+    t_warmup: int = 50
+    omega: float = 1.0
+    eps_alpha: float = 1e-6
+    tol: float = 0.0
+    K_max: int = 300
+    C: float = 1e12
+    tol_B: float = 1e-8
+    tol_N: float = 1e-6
+
+    def _c(self):
+        return L.PgdSettingsC(self.alpha_max, self.alpha_fallback, self.omega, self.eps_alpha,
+                              self.tol_N, self.t_warmup)
+
+    def options(self) -> ProjectionOptions:
+        return ProjectionOptions(c=self.C, tol_b=self.tol_B, tol_n=self.tol_N)
+
+
+@dataclasses.dataclass
+class StepResult:
+    x_new: object
+    d: object
+    rho_tilde: object
+    delta: object
+    y: np.ndarray
+    slacks: np.ndarray
+    g_hat: np.ndarray
+    alpha: float
+    beta: float
+    fallback: bool
+    projection: ProjectionResult
+    mask: object = None
+
+
+def pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_equality=None,
+             partition=None, t=1, violation=0.0, lower=0.0, upper=1.0,
+             settings: PgdSettings = None, device: int = 0, want_delta=False,
+             want_mask=False, out=None,
+             host_outputs=("x_new", "d", "rho_tilde")) -> StepResult:
+    """One PGD-TO step (Alg. 3 lines 2-15): BB step, PR+ direction, rho_tilde,
+    linearization, projection, rho_{t+1} = rho_tilde + delta.
+
+    numpy inputs -> host-buffer C-ABI (copies inside the call);
+    torch CUDA tensors -> device C-ABI (no copies; `out` may supply buffers).
+    """
+    settings = settings or PgdSettings()
+    ctx = L.context(device)
+    dev = _is_torch_cuda(x)
+    n = int(x.numel() if dev else np.asarray(x).size)
+    m = int(len(g_values))
+    gv = np.ascontiguousarray(g_values, np.float64)
+    bg = np.ascontiguousarray(bounds_g, np.float64)
+    ie = None if is_equality is None else np.ascontiguousarray(is_equality, np.uint8)
+    off, idx = _part_csr(partition, m)
+    pr = L.StepProblem()
+    pr.n, pr.m, pr.t, pr.violation, pr.lower, pr.upper = n, m, int(t), float(violation), \
+        float(lower), float(upper)
+    y = np.zeros(m)
+    sl = np.zeros(m)
+    gh = np.zeros(m)
+    meta = L.ProjMeta()
+    opts = settings.options()._c()
+    sc = settings._c()
+    o = L.StepOutputs()
+    o.y, o.slacks, o.g_hat = _ptr(y), _ptr(sl), _ptr(gh)
+    if dev:
+        import torch
+        bufs = out or {}
+        x_new = bufs.get("x_new") if bufs.get("x_new") is not None else torch.empty_like(x)
+        d = bufs.get("d") if bufs.get("d") is not None else torch.empty_like(x)
+        rt = bufs.get("rho_tilde") if bufs.get("rho_tilde") is not None else torch.empty_like(x)
+        delta = (bufs.get("delta") if bufs.get("delta") is not None else torch.empty_like(x)) \
+            if want_delta else None
+        mask = torch.empty(n, dtype=torch.uint8, device=x.device) if want_mask else None
+        owner = bufs.get("owner")
+        if owner is None and partition is not None and m > 1:
+            owner = torch.empty(n, dtype=torch.int8, device=x.device)
+            _check(ctx, ctx.lib.topt_b200_owner_map(ctx.h, C.c_int64(n), C.c_int32(m), _ptr(off),
+                                                    _ptr(idx), C.c_void_p(owner.data_ptr())))
+        for f, a in (("x", x), ("x_prev", x_prev), ("g", g), ("g_prev", g_prev),
+                     ("d_prev", d_prev), ("grad", grad)):
+            setattr(pr, f, a.data_ptr())
+        pr.g_values, pr.bounds_g = _ptr(gv), _ptr(bg)
+        pr.is_equality = _ptr(ie)
+        pr.part_offsets, pr.part_indices = _ptr(off), _ptr(idx)
+        pr.owner = owner.data_ptr() if owner is not None else None
+        o.x_new, o.d, o.rho_tilde = x_new.data_ptr(), d.data_ptr(), rt.data_ptr()
+        o.delta = delta.data_ptr() if delta is not None else None
+        o.mask = mask.data_ptr() if mask is not None else None
+        _check(ctx, ctx.lib.topt_b200_pgd_step_dev(ctx.h, C.byref(pr), C.byref(sc), C.byref(opts),
+                                                   C.byref(o), C.byref(meta)))
+    else:
+        arrs = {k: np.ascontiguousarray(v, np.float64) for k, v in
+                (("x", x), ("x_prev", x_prev), ("g", g), ("g_prev", g_prev), ("d_prev", d_prev),
+                 ("grad", grad))}
+        for f, a in arrs.items():
+            setattr(pr, f, a.ctypes.data)
+        pr.g_values, pr.bounds_g = _ptr(gv), _ptr(bg)
+        pr.is_equality = _ptr(ie)
+        pr.part_offsets, pr.part_indices = _ptr(off), _ptr(idx)
+        x_new = np.empty(n) if "x_new" in host_outputs else None
+        d = np.empty(n) if "d" in host_outputs else None
+        rt = np.empty(n) if "rho_tilde" in host_outputs else None
+        delta = np.empty(n) if want_delta else None
+        mask = np.empty(n, np.uint8) if want_mask else None
+        o.x_new, o.d, o.rho_tilde = _ptr(x_new), _ptr(d), _ptr(rt)
+        o.delta = _ptr(delta)
+        o.mask = _ptr(mask)
+        _check(ctx, ctx.lib.topt_b200_pgd_step(ctx.h, C.byref(pr), C.byref(sc), C.byref(opts),
+                                               C.byref(o), C.byref(meta)))
+    proj = _meta_to_result(meta, delta, y, sl, m, mask)
+    return StepResult(x_new=x_new, d=d, rho_tilde=rt, delta=delta, y=y, slacks=sl, g_hat=gh,
+                      alpha=meta.alpha, beta=meta.beta, fallback=bool(meta.fallback),
+                      projection=proj, mask=mask)

@@ -1,0 +1,744 @@
+// capi.cu — kernels that drive the passes + the extern "C" boundary.
+//
+// Launch model (single GPU).  One kernel launch per pass: every CTA sweeps
+// its grid-stride share of the slab and writes its partial slots; the CTA
+// that finishes last (atomic ticket) combines all CTAs' partials in a fixed
+// order and runs the controller (controller.h) on the device, which writes
+// the next pass's command into the device-resident Plan.  The host only
+// relaunches and polls one int (the next phase); no partial sum or decision
+// ever crosses PCIe.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/topt_b200.h"
+#include "controller.h"
+#include "passes.cuh"
+#include "topt_core.h"
+
+using namespace topt_b200;
+
+namespace {
+
+constexpr int RED_SCRATCH = NWARP * 160;   // doubles (max NS = 16 + 136)
+
+__device__ void finish_reduce(const double* partials, int nb, int ns, int phase,
+                              double* totals, double* smem) {
+  // Group g sums CTAs g, g+G, g+2G, ... sequentially; groups combine in
+  // order.  The order depends only on (nb, ns): deterministic.
+  for (int s0 = 0; s0 < ns; s0 += BLOCK) {
+    const int per = min(ns - s0, BLOCK);
+    int G = 1;
+    while (G * 2 * per <= BLOCK && G * 2 <= nb && G < 64) G *= 2;
+    const int t = threadIdx.x;
+    const int s = t % per, g = t / per;
+    if (g < G) {
+      const int op = slot_op(phase, s0 + s);
+      double r = __ldcg(partials + (size_t)g * PMAX + s0 + s);
+      for (int b = g + G; b < nb; b += G) r = apply_op(op, r, __ldcg(partials + (size_t)b * PMAX + s0 + s));
+      smem[g * per + s] = r;
+    }
+    __syncthreads();
+    if (t < per) {
+      const int op = slot_op(phase, s0 + t);
+      double r = smem[t];
+      for (int gg = 1; gg < G; ++gg) r = apply_op(op, r, smem[gg * per + t]);
+      totals[s0 + t] = r;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(BLOCK) k_pass(Plan* plan, double* partials,
+                                                unsigned* counter, double* totals) {
+  __shared__ Cmd s_cmd;
+  __shared__ double s_red[RED_SCRATCH];
+  __shared__ int s_last;
+  {
+    const int* src = reinterpret_cast<const int*>(&plan->cmd);
+    int* dst = reinterpret_cast<int*>(&s_cmd);
+    for (int k = threadIdx.x; k < (int)(sizeof(Cmd) / sizeof(int)); k += BLOCK) dst[k] = src[k];
+  }
+  __syncthreads();
+  if (s_cmd.phase == PH_DONE) return;
+  PassCtx c;
+  c.plan = plan;
+  c.cmd = &s_cmd;
+  c.out = partials + (size_t)blockIdx.x * PMAX;
+  c.smem = s_red;
+  c.i0 = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
+  c.stride = (int64_t)gridDim.x * BLOCK;
+  run_pass(c);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  finish_reduce(partials, gridDim.x, s_cmd.nslots, s_cmd.phase, totals, s_red);
+  if (threadIdx.x == 0) {
+    plan_consume(*plan, totals);
+    *counter = 0u;
+    __threadfence();
+  }
+}
+
+__global__ void k_owner_init(int32_t* o32, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    o32[i] = -1;
+}
+
+// validate(): range and overlap (projection.cpp:163-171)
+__global__ void k_owner_scatter(int32_t* o32, int64_t n, const int32_t* idx, const int64_t* off,
+                                int m, int* err) {
+  const int64_t total = off[m];
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int j = 0;
+    while (j + 1 < m && off[j + 1] <= k) ++j;   // m <= 16
+    const int32_t i = idx[k];
+    if (i < 0 || (int64_t)i >= n) { atomicOr(err, 1); continue; }
+    if (atomicCAS(o32 + i, -1, j) != -1) atomicOr(err, 2);
+  }
+}
+
+__global__ void k_owner_pack(const int32_t* o32, int8_t* o8, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    o8[i] = (int8_t)o32[i];
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct topt_b200_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int nsm = 0;
+  int grid = 0;
+  Plan* d_plan = nullptr;
+  double* d_part = nullptr;
+  unsigned* d_counter = nullptr;
+  double* d_totals = nullptr;
+  int* h_phase = nullptr;   // pinned
+  int* d_err = nullptr;
+  Plan h_plan;
+  std::string err;
+  int64_t launches = 0;
+  DevBuf bufs[16];
+  int profile = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double prof_ms = 0.0, prof_max = 0.0;
+  int64_t prof_n = 0;
+};
+
+namespace {
+
+int fail(topt_b200_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+#define CUDA_TRY(ctx, expr)                                                         \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(ctx, TOPT_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+void* buf(topt_b200_ctx* ctx, int slot, size_t bytes) {
+  DevBuf& b = ctx->bufs[slot];
+  if (b.bytes < bytes) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    if (cudaMalloc(&b.p, bytes) != cudaSuccess) return nullptr;
+    b.bytes = bytes;
+  }
+  return b.p;
+}
+
+enum BufSlot {
+  B_RHO = 0, B_GRAD, B_GD, B_DELTA, B_OWNER, B_OWNER32, B_X, B_XP, B_G, B_GP, B_DP, B_D,
+  B_XNEW, B_PIDX, B_POFF, B_MASK
+};
+
+const char* status_msg(int st) {
+  switch (st) {
+    case ST_OK: return "ok";
+    case ST_PARAMETER: return "ParameterError";
+    case ST_DOMAIN: return "DomainError";
+    case ST_SINGULAR: return "SingularSystemError";
+    case ST_INFEASIBLE: return "InfeasibleLinearization: linearized feasible set is empty";
+    case ST_NUMERICAL: return "NumericalError: singular or non-finite Newton system";
+    case ST_UNSUPPORTED: return "UnsupportedProblem";
+    default: return "internal error";
+  }
+}
+
+// Run a plan to completion on the device.  hp.P must be filled.
+int run_plan(topt_b200_ctx* ctx, Plan& hp) {
+  const int64_t per_thread = (hp.P.n + (int64_t)ctx->grid * BLOCK - 1) / ((int64_t)ctx->grid * BLOCK);
+  hp.P.ours_len = (double)per_thread + (double)ctx->grid + 64.0;
+  plan_start(hp);
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_plan, &hp, sizeof(Plan), cudaMemcpyHostToDevice, ctx->stream));
+  int phase = hp.cmd.phase;
+  for (int it = 0; phase != PH_DONE && it < 4096; ++it) {
+    if (ctx->profile) cudaEventRecord(ctx->ev0, ctx->stream);
+    k_pass<<<ctx->grid, BLOCK, 0, ctx->stream>>>(ctx->d_plan, ctx->d_part, ctx->d_counter,
+                                                 ctx->d_totals);
+    ctx->launches++;
+    CUDA_TRY(ctx, cudaGetLastError());
+    if (ctx->profile) cudaEventRecord(ctx->ev1, ctx->stream);
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_phase, &ctx->d_plan->cmd.phase, sizeof(int),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->profile) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+      ctx->prof_ms += ms;
+      ctx->prof_max = std::max(ctx->prof_max, (double)ms);
+      ctx->prof_n++;
+    }
+    phase = *ctx->h_phase;
+  }
+  CUDA_TRY(ctx, cudaMemcpyAsync(&hp, ctx->d_plan, sizeof(Plan), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (phase != PH_DONE) return fail(ctx, TOPT_ERR_INTERNAL, "plan did not terminate");
+  if (hp.res.status != ST_OK) return fail(ctx, hp.res.status, status_msg(hp.res.status));
+  return TOPT_OK;
+}
+
+void fill_meta(const Plan& hp, topt_proj_meta* meta) {
+  if (!meta) return;
+  const Result& r = hp.res;
+  std::memset(meta, 0, sizeof(*meta));
+  meta->path = r.path;
+  meta->newton_iters = r.newton_iters;
+  meta->converged = r.converged;
+  meta->curvature_violations = r.curvature_violations;
+  meta->residual = r.residual;
+  meta->passes = r.passes;
+  meta->sweeps = r.sweeps;
+  meta->stage1_row = r.stage1_row;
+  meta->near_ties = r.near_ties;
+  meta->min_margin = r.min_margin;
+  for (int j = 0; j < MAX_M; ++j) meta->bisect_iters[j] = r.bisect_iters[j];
+  meta->alpha = r.alpha;
+  meta->beta = r.beta;
+  meta->fallback = r.fallback;
+}
+
+void default_opts(ProjOptions& o) {
+  o.c = 1e12; o.tol_b = 1e-8; o.tol_n = 1e-6; o.newton_maxiter = 50; o.binary_maxiter = 200;
+}
+
+int init_problem(topt_b200_ctx* ctx, Plan& hp, int64_t n, int m, const topt_proj_options* opts) {
+  std::memset(&hp, 0, sizeof(Plan));
+  if (m > MAX_M)
+    return fail(ctx, TOPT_ERR_UNSUPPORTED, "topt_b200: at most 16 constraint rows supported");
+  if (m < 0 || n < 0) return fail(ctx, TOPT_ERR_DOMAIN, "topt_b200: negative sizes");
+  Problem& P = hp.P;
+  P.n = n;
+  P.n_global = n;
+  P.m = m;
+  P.ld = n;
+  if (opts) {
+    P.opt.c = opts->c; P.opt.tol_b = opts->tol_b; P.opt.tol_n = opts->tol_n;
+    P.opt.newton_maxiter = opts->newton_maxiter; P.opt.binary_maxiter = opts->binary_maxiter;
+  } else {
+    default_opts(P.opt);
+  }
+  for (int j = 0; j < m; ++j) P.row_count[j] = (double)n;
+  return TOPT_OK;
+}
+
+void set_lin_scalars(Plan& hp, const topt_linearization* lin) {
+  Problem& P = hp.P;
+  const int m = P.m;
+  for (int j = 0; j < m; ++j) {
+    if (lin->bounds_g && lin->g_values) P.G_minus_g[j] = lin->bounds_g[j] - lin->g_values[j];
+    if (lin->g_hat) P.ghat_in[j] = lin->g_hat[j];
+    P.ghat_err_in[j] = lin->g_hat_err ? lin->g_hat_err[j] : 0.0;
+    P.is_eq[j] = lin->is_equality ? (lin->is_equality[j] ? 1 : 0) : 0;
+  }
+  if (lin->part_offsets) {
+    for (int j = 0; j < m; ++j)
+      P.row_count[j] = (double)(lin->part_offsets[j + 1] - lin->part_offsets[j]);
+  }
+}
+
+int upload(topt_b200_ctx* ctx, int slot, const void* src, size_t bytes, void** dst) {
+  *dst = nullptr;
+  if (!src || bytes == 0) return TOPT_OK;
+  void* d = buf(ctx, slot, bytes);
+  if (!d) return fail(ctx, TOPT_ERR_CUDA, "cudaMalloc failed");
+  CUDA_TRY(ctx, cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  *dst = d;
+  return TOPT_OK;
+}
+
+int owner_map_impl(topt_b200_ctx* ctx, int64_t n, int32_t m, const int64_t* off,
+                   const int32_t* idx, int8_t* owner_dev) {
+  int32_t* o32 = (int32_t*)buf(ctx, B_OWNER32, sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1));
+  if (!o32) return fail(ctx, TOPT_ERR_CUDA, "cudaMalloc failed");
+  const int64_t total = off[m];
+  void* didx = nullptr;
+  void* doff = nullptr;
+  int rc = upload(ctx, B_PIDX, idx, sizeof(int32_t) * (size_t)total, &didx);
+  if (rc) return rc;
+  rc = upload(ctx, B_POFF, off, sizeof(int64_t) * (size_t)(m + 1), &doff);
+  if (rc) return rc;
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
+  const int g = ctx->nsm * 4;
+  if (n > 0) k_owner_init<<<g, 256, 0, ctx->stream>>>(o32, n);
+  if (total > 0)
+    k_owner_scatter<<<g, 256, 0, ctx->stream>>>(o32, n, (const int32_t*)didx,
+                                                (const int64_t*)doff, m, ctx->d_err);
+  if (n > 0) k_owner_pack<<<g, 256, 0, ctx->stream>>>(o32, owner_dev, n);
+  ctx->launches += 3;
+  CUDA_TRY(ctx, cudaGetLastError());
+  int herr = 0;
+  CUDA_TRY(ctx, cudaMemcpyAsync(&herr, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (herr & 1) return fail(ctx, TOPT_ERR_DOMAIN, "ConstraintLinearization: partition index out of range");
+  if (herr & 2) return fail(ctx, TOPT_ERR_DOMAIN, "ConstraintLinearization: partition sets overlap");
+  return TOPT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* topt_b200_version(void) { return "topt_b200 0.1 (sm_100a)"; }
+
+void topt_b200_default_options(topt_proj_options* o) {
+  o->c = 1e12; o->tol_b = 1e-8; o->tol_n = 1e-6; o->newton_maxiter = 50; o->binary_maxiter = 200;
+}
+
+void topt_b200_default_settings(topt_pgd_settings* s) {
+  s->alpha_max = 1e2; s->alpha_fallback = 0.2; s->omega = 1.0; s->eps_alpha = 1e-6;
+  s->tol_n = 1e-6; s->t_warmup = 50;
+}
+
+int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device) return TOPT_ERR_CUDA;
+  topt_b200_ctx* ctx = new topt_b200_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) { delete ctx; return TOPT_ERR_CUDA; }
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  ctx->nsm = prop.multiProcessorCount;
+  ctx->grid = ctx->nsm * 4;
+  bool ok = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) == cudaSuccess;
+  ctx->own_stream = ok;
+  ok = ok && cudaMalloc(&ctx->d_plan, sizeof(Plan)) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_part, sizeof(double) * PMAX * ctx->grid) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_counter, sizeof(unsigned)) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_totals, sizeof(double) * PMAX) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_err, sizeof(int)) == cudaSuccess;
+  ok = ok && cudaMallocHost(&ctx->h_phase, sizeof(int)) == cudaSuccess;
+  ok = ok && cudaMemset(ctx->d_counter, 0, sizeof(unsigned)) == cudaSuccess;
+  ok = ok && cudaEventCreate(&ctx->ev0) == cudaSuccess;
+  ok = ok && cudaEventCreate(&ctx->ev1) == cudaSuccess;
+  if (!ok) { topt_b200_ctx_destroy(ctx); return TOPT_ERR_CUDA; }
+  *out = ctx;
+  return TOPT_OK;
+}
+
+void topt_b200_ctx_destroy(topt_b200_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto& b : ctx->bufs)
+    if (b.p) cudaFree(b.p);
+  cudaFree(ctx->d_plan);
+  cudaFree(ctx->d_part);
+  cudaFree(ctx->d_counter);
+  cudaFree(ctx->d_totals);
+  cudaFree(ctx->d_err);
+  if (ctx->h_phase) cudaFreeHost(ctx->h_phase);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* topt_b200_last_error(const topt_b200_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+int64_t topt_b200_kernel_launches(const topt_b200_ctx* ctx) { return ctx ? ctx->launches : 0; }
+void* topt_b200_get_stream(const topt_b200_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+int topt_b200_set_stream(topt_b200_ctx* ctx, void* stream) {
+  if (!ctx) return TOPT_ERR_INTERNAL;
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  ctx->stream = (cudaStream_t)stream;
+  ctx->own_stream = false;
+  return TOPT_OK;
+}
+
+int topt_b200_set_profiling(topt_b200_ctx* ctx, int enabled) {
+  if (!ctx) return TOPT_ERR_INTERNAL;
+  ctx->profile = enabled ? 1 : 0;
+  return TOPT_OK;
+}
+
+int topt_b200_kernel_time(topt_b200_ctx* ctx, double* total_ms, int64_t* launches,
+                          double* max_ms) {
+  if (!ctx) return TOPT_ERR_INTERNAL;
+  if (total_ms) *total_ms = ctx->prof_ms;
+  if (launches) *launches = ctx->prof_n;
+  if (max_ms) *max_ms = ctx->prof_max;
+  ctx->prof_ms = 0.0;
+  ctx->prof_max = 0.0;
+  ctx->prof_n = 0;
+  return TOPT_OK;
+}
+
+int topt_b200_owner_map(topt_b200_ctx* ctx, int64_t n, int32_t m, const int64_t* part_offsets,
+                        const int32_t* part_indices, int8_t* owner_dev) {
+  cudaSetDevice(ctx->device);
+  return owner_map_impl(ctx, n, m, part_offsets, part_indices, owner_dev);
+}
+
+// ----- host-buffer linearization helpers ----------------------------------
+static int stage_lin(topt_b200_ctx* ctx, Plan& hp, const topt_linearization* lin, bool need_gd,
+                     bool with_part) {
+  const int64_t n = (int64_t)lin->num_vars;
+  const int m = (int)lin->num_constraints;
+  void* dgrad = nullptr;
+  void* dgd = nullptr;
+  int rc = upload(ctx, B_GRAD, lin->grad, sizeof(double) * (size_t)m * (size_t)n, &dgrad);
+  if (rc) return rc;
+  if (need_gd && lin->gd_step) {
+    rc = upload(ctx, B_GD, lin->gd_step, sizeof(double) * (size_t)n, &dgd);
+    if (rc) return rc;
+  }
+  hp.P.grad = (const double*)dgrad;
+  hp.P.gd_step = (const double*)dgd;
+  if (with_part && lin->part_offsets) {
+    int8_t* own = (int8_t*)buf(ctx, B_OWNER, (size_t)std::max<int64_t>(n, 1));
+    if (!own) return fail(ctx, TOPT_ERR_CUDA, "cudaMalloc failed");
+    rc = owner_map_impl(ctx, n, m, lin->part_offsets, lin->part_indices, own);
+    if (rc) return rc;
+    hp.P.owner = own;
+    hp.P.has_part = 1;
+  }
+  return TOPT_OK;
+}
+
+int topt_b200_build(topt_b200_ctx* ctx, const topt_linearization* lin, double* g_hat_out,
+                    double* g_hat_err_out) {
+  cudaSetDevice(ctx->device);
+  Plan& hp = ctx->h_plan;
+  const int64_t n = (int64_t)lin->num_vars;
+  const int m = (int)lin->num_constraints;
+  int rc = init_problem(ctx, hp, n, m, nullptr);
+  if (rc) return rc;
+  if (m == 0) return TOPT_OK;
+  if (!lin->gd_step || !lin->grad || !lin->g_values || !lin->bounds_g)
+    return fail(ctx, TOPT_ERR_DOMAIN, "ConstraintLinearization: inconsistent dimensions");
+  hp.P.job = JOB_BUILD;
+  set_lin_scalars(hp, lin);
+  rc = stage_lin(ctx, hp, lin, true, true);
+  if (rc) return rc;
+  void* drho = buf(ctx, B_RHO, sizeof(double) * (size_t)std::max<int64_t>(n, 1));
+  if (!drho) return fail(ctx, TOPT_ERR_CUDA, "cudaMalloc failed");
+  CUDA_TRY(ctx, cudaMemsetAsync(drho, 0, sizeof(double) * (size_t)n, ctx->stream));
+  hp.P.rho = (double*)drho;
+  rc = run_plan(ctx, hp);
+  if (rc == TOPT_ERR_DOMAIN)
+    ctx->err = "ConstraintLinearization: gradient nonzero outside partition set";
+  if (rc) return rc;
+  for (int j = 0; j < m; ++j) {
+    if (g_hat_out) g_hat_out[j] = hp.res.ghat[j];
+    if (g_hat_err_out) g_hat_err_out[j] = hp.res.ghat_err[j];
+  }
+  return TOPT_OK;
+}
+
+static int small_job(topt_b200_ctx* ctx, int job, const double* y, const topt_linearization* lin,
+                     const double* rho, double lower, double upper, double c, double* out) {
+  cudaSetDevice(ctx->device);
+  Plan& hp = ctx->h_plan;
+  const int64_t n = (int64_t)lin->num_vars;
+  const int m = (int)lin->num_constraints;
+  int rc = init_problem(ctx, hp, n, m, nullptr);
+  if (rc) return rc;
+  if (job == JOB_RESIDUAL_H && !(c > 0.0))
+    return fail(ctx, TOPT_ERR_PARAMETER, "constraint_residual_h: c must be > 0");
+  hp.P.job = job;
+  hp.P.lower = lower;
+  hp.P.upper = upper;
+  hp.P.opt.c = c;
+  set_lin_scalars(hp, lin);
+  for (int j = 0; j < m; ++j) hp.P.y_in[j] = y[j];
+  rc = stage_lin(ctx, hp, lin, false, false);
+  if (rc) return rc;
+  void* drho = nullptr;
+  rc = upload(ctx, B_RHO, rho, sizeof(double) * (size_t)n, &drho);
+  if (rc) return rc;
+  hp.P.rho = (double*)drho;
+  double* ddelta = nullptr;
+  if (job == JOB_DELTA && n > 0) {
+    ddelta = (double*)buf(ctx, B_DELTA, sizeof(double) * (size_t)n);
+    if (!ddelta) return fail(ctx, TOPT_ERR_CUDA, "cudaMalloc failed");
+    hp.P.delta_out = ddelta;
+  }
+  rc = run_plan(ctx, hp);
+  if (rc) return rc;
+  if (job == JOB_DELTA) {
+    if (n > 0)
+      CUDA_TRY(ctx, cudaMemcpyAsync(out, ddelta, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  } else {
+    for (int j = 0; j < m; ++j) out[j] = hp.res.h[j];
+  }
+  return TOPT_OK;
+}
+
+int topt_b200_delta_of_y(topt_b200_ctx* ctx, const double* y, const topt_linearization* lin,
+                         const double* rho_tilde, double lower, double upper,
+                         double* delta_out) {
+  return small_job(ctx, JOB_DELTA, y, lin, rho_tilde, lower, upper, 1e12, delta_out);
+}
+
+int topt_b200_constraint_residual_h(topt_b200_ctx* ctx, const double* y,
+                                    const topt_linearization* lin, const double* rho_tilde,
+                                    double lower, double upper, double c, double* h_out) {
+  return small_job(ctx, JOB_RESIDUAL_H, y, lin, rho_tilde, lower, upper, c, h_out);
+}
+
+static int project_common(topt_b200_ctx* ctx, Plan& hp, int which, double lower, double upper,
+                          double* y_out, double* slacks_out, topt_proj_meta* meta) {
+  hp.P.job = JOB_PROJECT;
+  hp.P.which = which;
+  hp.P.lower = lower;
+  hp.P.upper = upper;
+  const int m = hp.P.m;
+  if (which == W_SINGLE && m != 1)
+    return fail(ctx, TOPT_ERR_DOMAIN, "project_single_binary_search: exactly one constraint required");
+  if (which == W_INDEPENDENT && !hp.P.has_part)
+    return fail(ctx, TOPT_ERR_DOMAIN, "project_independent: linearization has no partition");
+  if ((which == W_NEWTON || (which == W_AUTO && m != 1 && !hp.P.has_part)) && m < 1)
+    return fail(ctx, TOPT_ERR_DOMAIN, "project_general_newton: no constraints");
+  int rc = run_plan(ctx, hp);
+  if (rc == TOPT_ERR_DOMAIN && hp.res.status == ST_DOMAIN)
+    ctx->err = "ConstraintLinearization: partition/g_hat validation failed";
+  if (rc) return rc;
+  for (int j = 0; j < m; ++j) {
+    if (y_out) y_out[j] = hp.res.y[j];
+    if (slacks_out) slacks_out[j] = hp.res.slacks[j];
+  }
+  fill_meta(hp, meta);
+  return TOPT_OK;
+}
+
+int topt_b200_project(topt_b200_ctx* ctx, int which, const double* rho_tilde,
+                      const topt_linearization* lin, double lower, double upper,
+                      const topt_proj_options* opts, double* delta_out, double* y_out,
+                      double* slacks_out, topt_proj_meta* meta) {
+  cudaSetDevice(ctx->device);
+  Plan& hp = ctx->h_plan;
+  const int64_t n = (int64_t)lin->num_vars;
+  const int m = (int)lin->num_constraints;
+  int rc = init_problem(ctx, hp, n, m, opts);
+  if (rc) return rc;
+  set_lin_scalars(hp, lin);
+  const bool use_part = lin->part_offsets && which != W_SINGLE && which != W_NEWTON && m > 1;
+  rc = stage_lin(ctx, hp, lin, use_part, use_part || (which == W_INDEPENDENT && lin->part_offsets));
+  if (rc) return rc;
+  void* drho = nullptr;
+  rc = upload(ctx, B_RHO, rho_tilde, sizeof(double) * (size_t)n, &drho);
+  if (rc) return rc;
+  hp.P.rho = (double*)drho;
+  double* dd = nullptr;
+  if (delta_out && n > 0) {
+    dd = (double*)buf(ctx, B_DELTA, sizeof(double) * (size_t)n);
+    if (!dd) return fail(ctx, TOPT_ERR_CUDA, "cudaMalloc failed");
+  }
+  hp.P.delta_out = dd;
+  if (which == W_INDEPENDENT && !lin->part_offsets) hp.P.has_part = 0;
+  rc = project_common(ctx, hp, which, lower, upper, y_out, slacks_out, meta);
+  if (rc) return rc;
+  if (dd)
+    CUDA_TRY(ctx, cudaMemcpyAsync(delta_out, dd, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return TOPT_OK;
+}
+
+int topt_b200_project_dev(topt_b200_ctx* ctx, int which, const double* rho_tilde,
+                          const topt_linearization* lin, double lower, double upper,
+                          const topt_proj_options* opts, double* delta_out, uint8_t* mask_out,
+                          double* y_out, double* slacks_out, topt_proj_meta* meta) {
+  cudaSetDevice(ctx->device);
+  Plan& hp = ctx->h_plan;
+  const int64_t n = (int64_t)lin->num_vars;
+  const int m = (int)lin->num_constraints;
+  int rc = init_problem(ctx, hp, n, m, opts);
+  if (rc) return rc;
+  set_lin_scalars(hp, lin);
+  hp.P.grad = lin->grad;
+  hp.P.gd_step = lin->gd_step;
+  const bool use_part = lin->owner && which != W_SINGLE && which != W_NEWTON && m > 1;
+  hp.P.owner = use_part ? lin->owner : nullptr;
+  hp.P.has_part = use_part ? 1 : 0;
+  hp.P.rho = const_cast<double*>(rho_tilde);
+  hp.P.delta_out = delta_out;
+  hp.P.mask_out = mask_out;
+  return project_common(ctx, hp, which, lower, upper, y_out, slacks_out, meta);
+}
+
+static int pgd_step_impl(topt_b200_ctx* ctx, Plan& hp, const topt_step_problem* prob,
+                         const topt_pgd_settings* s, const topt_proj_options* opts,
+                         topt_proj_meta* meta, double* y, double* slacks, double* ghat,
+                         int job = JOB_PGD_STEP) {
+  Problem& P = hp.P;
+  P.job = job;
+  P.which = W_AUTO;
+  P.t = prob->t;
+  P.violation = prob->violation;
+  P.lower = prob->lower;
+  P.upper = prob->upper;
+  if (s) {
+    P.set.alpha_max = s->alpha_max; P.set.alpha_fallback = s->alpha_fallback;
+    P.set.omega = s->omega; P.set.eps_alpha = s->eps_alpha; P.set.tol_n = s->tol_n;
+    P.set.t_warmup = s->t_warmup;
+  } else {
+    P.set.alpha_max = 1e2; P.set.alpha_fallback = 0.2; P.set.omega = 1.0;
+    P.set.eps_alpha = 1e-6; P.set.tol_n = 1e-6; P.set.t_warmup = 50;
+  }
+  for (int j = 0; j < P.m; ++j) {
+    P.G_minus_g[j] = prob->bounds_g[j] - prob->g_values[j];
+    P.is_eq[j] = prob->is_equality ? (prob->is_equality[j] ? 1 : 0) : 0;
+    if (prob->part_offsets)
+      P.row_count[j] = (double)(prob->part_offsets[j + 1] - prob->part_offsets[j]);
+  }
+  int rc = run_plan(ctx, hp);
+  if (rc) return rc;
+  for (int j = 0; j < P.m; ++j) {
+    if (y) y[j] = hp.res.y[j];
+    if (slacks) slacks[j] = hp.res.slacks[j];
+    if (ghat) ghat[j] = hp.res.ghat[j];
+  }
+  fill_meta(hp, meta);
+  return TOPT_OK;
+}
+
+int topt_b200_pgd_step_dev(topt_b200_ctx* ctx, const topt_step_problem* prob,
+                           const topt_pgd_settings* settings, const topt_proj_options* opts,
+                           const topt_step_outputs* out, topt_proj_meta* meta) {
+  cudaSetDevice(ctx->device);
+  Plan& hp = ctx->h_plan;
+  int rc = init_problem(ctx, hp, prob->n, prob->m, opts);
+  if (rc) return rc;
+  if (!out->rho_tilde || !out->d)
+    return fail(ctx, TOPT_ERR_DOMAIN, "pgd_step_dev: rho_tilde and d outputs are required");
+  Problem& P = hp.P;
+  P.x = prob->x; P.x_prev = prob->x_prev; P.g = prob->g; P.g_prev = prob->g_prev;
+  P.d_prev = prob->d_prev; P.grad = prob->grad;
+  P.owner = (prob->owner && prob->m > 1) ? prob->owner : nullptr;
+  P.has_part = P.owner ? 1 : 0;
+  P.rho = out->rho_tilde; P.d_out = out->d; P.x_out = out->x_new; P.delta_out = out->delta;
+  P.mask_out = out->mask;
+  return pgd_step_impl(ctx, hp, prob, settings, opts, meta, out->y, out->slacks, out->g_hat);
+}
+
+int topt_b200_pgd_step(topt_b200_ctx* ctx, const topt_step_problem* prob,
+                       const topt_pgd_settings* settings, const topt_proj_options* opts,
+                       const topt_step_outputs* out, topt_proj_meta* meta) {
+  cudaSetDevice(ctx->device);
+  Plan& hp = ctx->h_plan;
+  const int64_t n = prob->n;
+  const int m = prob->m;
+  int rc = init_problem(ctx, hp, n, m, opts);
+  if (rc) return rc;
+  const size_t nb = sizeof(double) * (size_t)std::max<int64_t>(n, 1);
+  void *dx, *dxp, *dg, *dgp, *ddp, *dgrad;
+  if ((rc = upload(ctx, B_X, prob->x, nb, &dx))) return rc;
+  if ((rc = upload(ctx, B_XP, prob->x_prev, nb, &dxp))) return rc;
+  if ((rc = upload(ctx, B_G, prob->g, nb, &dg))) return rc;
+  if ((rc = upload(ctx, B_GP, prob->g_prev, nb, &dgp))) return rc;
+  if ((rc = upload(ctx, B_DP, prob->d_prev, nb, &ddp))) return rc;
+  if ((rc = upload(ctx, B_GRAD, prob->grad, nb * (size_t)m, &dgrad))) return rc;
+  Problem& P = hp.P;
+  P.x = (const double*)dx; P.x_prev = (const double*)dxp; P.g = (const double*)dg;
+  P.g_prev = (const double*)dgp; P.d_prev = (const double*)ddp; P.grad = (const double*)dgrad;
+  if (prob->part_offsets && m > 1) {
+    int8_t* own = (int8_t*)buf(ctx, B_OWNER, (size_t)std::max<int64_t>(n, 1));
+    if (!own) return fail(ctx, TOPT_ERR_CUDA, "cudaMalloc failed");
+    if ((rc = owner_map_impl(ctx, n, m, prob->part_offsets, prob->part_indices, own))) return rc;
+    P.owner = own;
+    P.has_part = 1;
+  }
+  P.rho = (double*)buf(ctx, B_RHO, nb);
+  P.d_out = (double*)buf(ctx, B_D, nb);
+  P.x_out = (double*)buf(ctx, B_XNEW, nb);
+  P.delta_out = out->delta ? (double*)buf(ctx, B_DELTA, nb) : nullptr;
+  P.mask_out = out->mask ? (uint8_t*)buf(ctx, B_MASK, (size_t)std::max<int64_t>(n, 1)) : nullptr;
+  if (!P.rho || !P.d_out || !P.x_out) return fail(ctx, TOPT_ERR_CUDA, "cudaMalloc failed");
+  rc = pgd_step_impl(ctx, hp, prob, settings, opts, meta, out->y, out->slacks, out->g_hat);
+  if (rc) return rc;
+  const size_t nbytes = sizeof(double) * (size_t)n;
+  if (n > 0) {
+    if (out->x_new) CUDA_TRY(ctx, cudaMemcpyAsync(out->x_new, P.x_out, nbytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (out->d) CUDA_TRY(ctx, cudaMemcpyAsync(out->d, P.d_out, nbytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (out->rho_tilde) CUDA_TRY(ctx, cudaMemcpyAsync(out->rho_tilde, P.rho, nbytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (out->delta) CUDA_TRY(ctx, cudaMemcpyAsync(out->delta, P.delta_out, nbytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (out->mask) CUDA_TRY(ctx, cudaMemcpyAsync(out->mask, P.mask_out, (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return TOPT_OK;
+}
+
+int topt_b200_step_direction(topt_b200_ctx* ctx, int64_t n, const double* x,
+                             const double* x_prev, const double* g, const double* g_prev,
+                             const double* d_prev, int32_t t, double violation,
+                             const topt_pgd_settings* settings, double* d_out,
+                             double* rho_tilde_out, double* alpha_out, double* beta_out,
+                             int32_t* fallback_out) {
+  cudaSetDevice(ctx->device);
+  Plan& hp = ctx->h_plan;
+  int rc = init_problem(ctx, hp, n, 0, nullptr);
+  if (rc) return rc;
+  const size_t nb = sizeof(double) * (size_t)std::max<int64_t>(n, 1);
+  void *dx, *dxp, *dg, *dgp, *ddp;
+  if ((rc = upload(ctx, B_X, x, nb, &dx))) return rc;
+  if ((rc = upload(ctx, B_XP, x_prev, nb, &dxp))) return rc;
+  if ((rc = upload(ctx, B_G, g, nb, &dg))) return rc;
+  if ((rc = upload(ctx, B_GP, g_prev, nb, &dgp))) return rc;
+  if ((rc = upload(ctx, B_DP, d_prev, nb, &ddp))) return rc;
+  Problem& P = hp.P;
+  P.x = (const double*)dx; P.x_prev = (const double*)dxp; P.g = (const double*)dg;
+  P.g_prev = (const double*)dgp; P.d_prev = (const double*)ddp;
+  P.rho = (double*)buf(ctx, B_RHO, nb);
+  P.d_out = (double*)buf(ctx, B_D, nb);
+  if (!P.rho || !P.d_out) return fail(ctx, TOPT_ERR_CUDA, "cudaMalloc failed");
+  topt_step_problem pr;
+  std::memset(&pr, 0, sizeof(pr));
+  pr.n = n; pr.t = t; pr.violation = violation; pr.lower = 0.0; pr.upper = 1.0;
+  rc = pgd_step_impl(ctx, hp, &pr, settings, nullptr, nullptr, nullptr, nullptr, nullptr,
+                     JOB_DIRECTION);
+  if (rc) return rc;
+  if (n > 0) {
+    if (d_out) CUDA_TRY(ctx, cudaMemcpyAsync(d_out, P.d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (rho_tilde_out) CUDA_TRY(ctx, cudaMemcpyAsync(rho_tilde_out, P.rho, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (alpha_out) *alpha_out = hp.res.alpha;
+  if (beta_out) *beta_out = hp.res.beta;
+  if (fallback_out) *fallback_out = hp.res.fallback;
+  return TOPT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,189 @@
+// topt_core.h — plan/controller state shared by the CUDA passes and the host.
+//
+// The PGD-TO step is a sequence of full-array PASSES (HBM/L2 sweeps that
+// produce a handful of partial sums) separated by tiny scalar CONTROL steps
+// (BB/PR+ scalars, the bisection walks, Stage-1 selection, the Newton m x m
+// solve).  The controller below is plain C++ compiled for both the device
+// (it runs inside the pass kernels, in the block that finishes last, so no
+// host round trip sits between passes) and the host (C-ABI controller entry
+// points used by the multi-rank tests).  Nothing here allocates.
+//
+// Reference map (file:line in /root/reference/proj):
+//   Walk            <- binary_search_row            src/projection.cpp:48-110
+//   stage-1 select  <- project_general_newton       src/projection.cpp:312-343
+//   Newton          <- project_general_newton       src/projection.cpp:345-437
+//   dispatch        <- project                      src/projection.cpp:440-460
+//   step scalars    <- SPEC.md:287-313 (no reference code exists)
+#pragma once
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define TOPT_HD __host__ __device__ __forceinline__
+#define TOPT_HDN __host__ __device__
+#else
+#define TOPT_HD inline
+#define TOPT_HDN
+#endif
+
+namespace topt_b200 {
+
+constexpr int MAX_M = 16;      // constraint rows
+constexpr int MAX_K = 16;      // bisection candidates per row per sweep
+constexpr int MAX_CAND = 64;   // candidates per sweep over all rows
+constexpr int MAX_FEAS = MAX_M + 1;
+constexpr int PMAX = 512;      // partial-sum slots per pass
+
+enum Phase : int32_t {
+  PH_STEP_REDUCE = 0,  // K1: BB / PR+ dot products
+  PH_PREP = 1,         // K2: direction + rho_tilde + linearization + r(0) + breakpoints
+  PH_SWEEP = 2,        // K3: r_j(y) at up to MAX_CAND candidate duals
+  PH_FEAS = 3,         // K4: stage-1 feasibility dots
+  PH_NEWTON = 4,       // K5: delta(y), h-dots and A D A^T at one trial dual
+  PH_FINAL = 5,        // K7: delta / x_new writes + residual dots
+  PH_DONE = 6
+};
+
+enum Status : int32_t {
+  ST_OK = 0,
+  ST_PARAMETER = 1,     // topt::ParameterError
+  ST_DOMAIN = 2,        // topt::DomainError
+  ST_SINGULAR = 3,      // topt::SingularSystemError
+  ST_INFEASIBLE = 4,    // topt::InfeasibleLinearization
+  ST_NUMERICAL = 5,     // topt::NumericalError
+  ST_UNSUPPORTED = 6,   // topt::UnsupportedProblem
+  ST_CUDA = 7,
+  ST_INTERNAL = 8
+};
+
+enum Path : int32_t { PATH_SINGLE = 0, PATH_INDEPENDENT = 1, PATH_NEWTON = 2 };
+enum Which : int32_t { W_AUTO = 0, W_SINGLE = 1, W_INDEPENDENT = 2, W_NEWTON = 3 };
+enum Job : int32_t {
+  JOB_PROJECT = 0,    // project / project_* (rho_tilde + linearization given)
+  JOB_PGD_STEP = 1,   // full optimizer step from (x, x_prev, g, g_prev, d_prev, A)
+  JOB_BUILD = 2,      // ConstraintLinearization::build: g_hat (+ partition validation)
+  JOB_DELTA = 3,      // delta_of_y
+  JOB_RESIDUAL_H = 4, // constraint_residual_h
+  JOB_DIRECTION = 5   // spectral_step_size + cg_direction + rho_tilde only
+};
+enum Stage : int32_t {
+  SG_INIT = 0, SG_SINGLE, SG_INDEP, SG_STAGE1, SG_FEAS, SG_NEWTON, SG_FINAL, SG_DONE
+};
+enum WalkStatus : int32_t { WK_IDLE = 0, WK_NEED = 1, WK_DONE = 2, WK_INFEASIBLE = 3 };
+
+struct ProjOptions {
+  double c, tol_b, tol_n;
+  int32_t newton_maxiter, binary_maxiter;
+};
+
+struct PgdSettings {
+  double alpha_max, alpha_fallback, omega, eps_alpha, tol_n;
+  int32_t t_warmup;
+};
+
+// One reference bisection (binary_search_row) replayed from evaluations.
+struct Walk {
+  int32_t status, eq, up, feas_done;
+  int32_t iters, nc, near_ties, n_direct;
+  double ghat, E, r0, S0, bp_lo, bp_hi, count;
+  double lo, hi, ym, y, residual, min_margin;
+  int32_t hasL, hasH, hasA, hasB;
+  double yL, yH;                    // certified: R(yL) < -E, R(yH) > E
+  double ya, Ra, Sa, yb, Rb, Sb;    // nearest evaluated points with R<=0 / R>0
+  double cy[MAX_K], cR[MAX_K], cS[MAX_K];   // this sweep's evaluations
+};
+
+struct Newton {
+  double y[MAX_M], step[MAX_M], h[MAX_M], phi[MAX_M];
+  double gram[MAX_M * (MAX_M + 1) / 2];   // A D A^T at the accepted y (upper, packed)
+  double ty[MAX_M];                        // trial dual
+  double merit, merit0, phi_sq, prev_phi_sq, gamma;
+  int32_t iters, curv_viol, have_prev, in_linesearch;
+};
+
+// The command the next pass executes (read by every CTA).
+struct Cmd {
+  int32_t phase;
+  int32_t nslots;
+  // PH_PREP
+  int32_t compute_dir, use_dprev, compute_dot, validate_part;
+  double beta, wa;
+  // PH_SWEEP: candidates grouped by row
+  int32_t ncand;
+  int32_t row_start[MAX_M + 1];
+  double cand_y[MAX_CAND];
+  // PH_FEAS: distinct stage-1 candidate duals (row < 0 -> all-zero dual)
+  int32_t nfeas;
+  int32_t feas_row[MAX_FEAS];
+  double feas_y[MAX_FEAS];
+  // PH_NEWTON / PH_FINAL: dual vector
+  double y[MAX_M];
+  int32_t want_gram;
+  int32_t resid_rows;            // PH_FINAL: accumulate a_j . delta for all rows
+  int32_t write_delta, write_x, write_mask;
+};
+
+// Problem description (device pointers are filled by the host).
+struct Problem {
+  int64_t n;          // local element count (this rank's slab)
+  int64_t n_global;   // global element count (error bounds)
+  int32_t m;
+  int32_t job, which, has_part, t;
+  double lower, upper, violation;
+  ProjOptions opt;
+  PgdSettings set;
+  // device arrays
+  const double* x;
+  const double* x_prev;
+  const double* g;
+  const double* g_prev;
+  const double* d_prev;
+  const double* grad;      // m x ld row-major
+  int64_t ld;              // row stride of grad
+  const double* gd_step;   // JOB_PROJECT / JOB_BUILD
+  const int8_t* owner;     // partition owner map (-1 = none) or null
+  double* rho;             // rho_tilde (read in PROJECT, written in PGD_STEP)
+  double* d_out;           // new direction (PGD_STEP)
+  double* delta_out;       // optional
+  double* x_out;           // optional x_{t+1}
+  uint8_t* mask_out;       // optional 0 free, 1 lower, 2 upper
+  // host-provided scalars
+  double G_minus_g[MAX_M];      // bounds_g - g_values (rounded as the reference does)
+  double ghat_in[MAX_M];        // JOB_PROJECT: lin.g_hat
+  double ghat_err_in[MAX_M];    // bound on |ghat_in - reference ghat| (0 if exact)
+  double y_in[MAX_M];           // JOB_DELTA / JOB_RESIDUAL_H
+  int32_t is_eq[MAX_M];
+  double row_count[MAX_M];      // terms summed by the reference per row
+  double ours_len;              // bound on our summation depth (error bound)
+};
+
+// Controller-visible result.
+struct Result {
+  int32_t status, path, newton_iters, converged, curvature_violations;
+  int32_t passes, sweeps, stage1_row, near_ties, fallback;
+  int32_t bisect_iters[MAX_M];
+  double residual, alpha, beta, min_margin;
+  double y[MAX_M], slacks[MAX_M], ghat[MAX_M], ghat_err[MAX_M], h[MAX_M];
+  double step_sums[6];
+};
+
+// Controller scratch (kept in the Plan so device threads carry no big stack).
+constexpr int CAND_CAP = 96;
+struct Scratch {
+  double np[CAND_CAP], nlo[CAND_CAP], nhi[CAND_CAP], nym[CAND_CAP];
+  int32_t nit[CAND_CAP];
+  double jh[MAX_M * MAX_M], jp[MAX_M * MAX_M];
+};
+
+struct Plan {
+  Problem P;
+  Cmd cmd;
+  int32_t stage;
+  int32_t dot_mode;    // 1: ghat computed in-pass (errors include dot bound)
+  Walk w[MAX_M];
+  Newton nt;
+  Result res;
+  int32_t feas_map[MAX_M];
+  Scratch sc;
+};
+
+}  // namespace topt_b200
