@@ -119,9 +119,13 @@ TOPT_HDN inline bool fullpiv_solve(int m, double* a, const double* b, double* x)
 
 // Exact evaluation lookup among this sweep's candidates.
 TOPT_HD bool walk_lookup(const Walk& w, double y, double* R) {
-  for (int k = 0; k < w.nc; ++k)
-    if (w.cy[k] == y) { *R = w.cR[k]; return true; }
-  return false;
+  int hit = -1;
+#pragma unroll
+  for (int k = 0; k < MAX_K; ++k)
+    if (k < w.nc && w.cy[k] == y) hit = k;
+  if (hit < 0) return false;
+  *R = w.cR[hit];
+  return true;
 }
 
 // +1: reference sees r(y) > 0 ; -1: reference sees r(y) <= 0 ; 0: unknown.
@@ -176,9 +180,15 @@ TOPT_HDN inline void walk_advance(Walk& w, const ProjOptions& o) {
   w.y = w.ym;
 }
 
-// Probability that the root of r lies above y (used only to choose which
-// midpoints to evaluate speculatively; never affects a decision).
-TOPT_HDN inline double walk_p_above(const Walk& w, double y) {
+// Root estimate used to choose speculative midpoints (never a decision).
+struct RootEst {
+  int kind;        // 0: gaussian(ye, sig) ; 1: log-uniform prior below 0 ; 2: above 0
+  double ye, sig, L;
+};
+
+TOPT_HDN inline RootEst walk_estimate(const Walk& w) {
+  RootEst e;
+  e.kind = 0; e.ye = 0.0; e.sig = 1.0; e.L = 0.0;
   if (w.hasA && w.hasB && w.ya < w.yb) {
     const double ya = w.ya, yb = w.yb;
     double sec = ya - w.Ra * (yb - ya) / (w.Rb - w.Ra);
@@ -186,95 +196,102 @@ TOPT_HDN inline double walk_p_above(const Walk& w, double y) {
     if (!(sec <= yb)) sec = yb;
     double spread = 0.0;
     if (w.Sa > 0.0) {
-      double e = ya - w.Ra / w.Sa;
-      e = dmin_(dmax_(e, ya), yb);
-      spread = dmax_(spread, fabs(e - sec));
+      const double t = dmin_(dmax_(ya - w.Ra / w.Sa, ya), yb);
+      spread = dmax_(spread, fabs(t - sec));
     }
     if (w.Sb > 0.0) {
-      double e = yb - w.Rb / w.Sb;
-      e = dmin_(dmax_(e, ya), yb);
-      spread = dmax_(spread, fabs(e - sec));
+      const double t = dmin_(dmax_(yb - w.Rb / w.Sb, ya), yb);
+      spread = dmax_(spread, fabs(t - sec));
     }
     double sig = dmax_(spread, (yb - ya) * 1e-6);
     sig = dmax_(sig, fabs(sec) * 1e-15);
-    sig = dmax_(sig, 1e-300);
-    return 0.5 * erfc((y - sec) / (sig * 1.4142135623730951));
+    e.ye = sec;
+    e.sig = dmax_(sig, 1e-300);
+    return e;
   }
-  // One-sided knowledge: Newton from the evaluated side, else a log-uniform
-  // prior on |root| across the bracket's magnitude range.
   if (!w.up) {  // root in [bp_lo, 0], r(0) > 0 known
     if (w.hasB && w.Sb > 0.0) {
-      double e = w.yb - w.Rb / w.Sb;
-      e = dmax_(e, w.lo);
-      const double sig = dmax_(0.5 * fabs(e), 1e-300);
-      return 0.5 * erfc((y - e) / (sig * 1.4142135623730951));
+      e.ye = dmax_(w.yb - w.Rb / w.Sb, w.lo);
+      e.sig = dmax_(0.5 * fabs(e.ye), 1e-300);
+      return e;
     }
-    const double ay = fabs(y), L = log(fabs(w.lo) + 1e-300);
-    if (!(ay > 0.0)) return 0.0;
-    double p = (log(ay) - (L - 46.0)) / 46.0;  // P(|root| < |y|)
-    return dmin_(dmax_(p, 0.0), 1.0);
-  } else {      // root in [0, bp_hi], r(0) < 0 known
-    if (w.hasA && w.Sa > 0.0) {
-      double e = w.ya - w.Ra / w.Sa;
-      e = dmin_(e, w.hi);
-      const double sig = dmax_(0.5 * fabs(e), 1e-300);
-      return 0.5 * erfc((y - e) / (sig * 1.4142135623730951));
-    }
-    const double ay = fabs(y), L = log(fabs(w.hi) + 1e-300);
-    if (!(ay > 0.0)) return 1.0;
-    double p = (log(ay) - (L - 46.0)) / 46.0;  // P(|root| < |y|)
-    return 1.0 - dmin_(dmax_(p, 0.0), 1.0);
+    e.kind = 1;
+    e.L = log(fabs(w.lo) + 1e-300);
+    return e;
   }
+  if (w.hasA && w.Sa > 0.0) {  // root in [0, bp_hi], r(0) < 0 known
+    e.ye = dmin_(w.ya - w.Ra / w.Sa, w.hi);
+    e.sig = dmax_(0.5 * fabs(e.ye), 1e-300);
+    return e;
+  }
+  e.kind = 2;
+  e.L = log(fabs(w.hi) + 1e-300);
+  return e;
 }
 
-// Choose up to K midpoints of the walk's decision tree to evaluate next, most
-// probable first (best-first expansion of the remaining tree).
+// Probability that the root lies above y.
+TOPT_HDN inline double est_p_above(const RootEst& e, double y) {
+  if (e.kind == 0) return 0.5 * erfc((y - e.ye) / (e.sig * 1.4142135623730951));
+  const double ay = fabs(y);
+  if (!(ay > 0.0)) return e.kind == 1 ? 0.0 : 1.0;
+  double p = (log(ay) - (e.L - 46.0)) / 46.0;  // P(|root| < |y|), log-uniform prior
+  p = dmin_(dmax_(p, 0.0), 1.0);
+  return e.kind == 1 ? p : 1.0 - p;
+}
+
+// Choose up to K midpoints of the walk's remaining decision tree to evaluate
+// next: the predicted path (most probable branch at every uncertain level),
+// plus first-level alternatives ("hedges") of its least certain levels,
+// ranked by the probability of being visited.  O(K + certain levels).
 TOPT_HDN inline int walk_candidates(const Walk& w, const ProjOptions& o, int K, double* out,
                                     Scratch& scr) {
   int n = 0;
   if (w.status != WK_NEED || K <= 0) return 0;
   if (!w.feas_done) out[n++] = w.up ? w.bp_hi : w.bp_lo;
-  constexpr int CAP = CAND_CAP;
-  double* np = scr.np;
-  double* nlo = scr.nlo;
-  double* nhi = scr.nhi;
-  double* nym = scr.nym;
-  int32_t* nit = scr.nit;
-  int sz = 0;
-  np[0] = 1.0; nlo[0] = w.lo; nhi[0] = w.hi; nym[0] = w.ym; nit[0] = w.iters;
-  sz = 1;
-  int guard = 0;
-  while (sz > 0 && n < K && guard < 4 * CAP) {
-    ++guard;
-    int best = 0;
-    for (int i = 1; i < sz; ++i)
-      if (np[i] > np[best]) best = i;
-    const double p = np[best], lo = nlo[best], hi = nhi[best], ym = nym[best];
-    const int it = nit[best];
-    --sz;
-    np[best] = np[sz]; nlo[best] = nlo[sz]; nhi[best] = nhi[sz]; nym[best] = nym[sz];
-    nit[best] = nit[sz];
-    if (!((hi - lo) > o.tol_b && it < o.binary_maxiter)) continue;
+  const RootEst e = walk_estimate(w);
+  double* pp = scr.np;    // path node probability
+  double* py = scr.nlo;   // path node y
+  double* hp = scr.nhi;   // hedge probability
+  double* hy = scr.nym;   // hedge y
+  int np = 0, nh = 0;
+  double lo = w.lo, hi = w.hi, ym = w.ym, p = 1.0;
+  int it = w.iters;
+  while (np < K && (hi - lo) > o.tol_b && it < o.binary_maxiter) {
     int d = 0;
     if (w.hasH && w.yH <= ym) d = 1;
     else if (w.hasL && w.yL >= ym) d = -1;
     if (d == 0) {
-      bool dup = false;
-      for (int k = 0; k < n; ++k) dup |= (out[k] == ym);
-      if (!dup) out[n++] = ym;
-      const double pa = walk_p_above(w, ym);  // root above ym -> r(ym) < 0 -> lo = ym
-      if (sz + 2 > CAP) continue;
-      const double pr = p * pa, pl = p * (1.0 - pa);
-      if (pr > 1e-14) {
-        np[sz] = pr; nlo[sz] = ym; nhi[sz] = hi; nym[sz] = 0.5 * (ym + hi); nit[sz] = it + 1; ++sz;
+      const double pa = est_p_above(e, ym);   // root above ym -> r(ym) <= 0 -> lo = ym
+      const bool right = pa >= 0.5;
+      py[np] = ym; pp[np] = p; ++np;
+      const double palt = right ? 1.0 - pa : pa;
+      if (palt > 1e-12 && nh < CAND_CAP) {
+        hy[nh] = right ? 0.5 * (lo + ym) : 0.5 * (ym + hi);
+        hp[nh] = p * palt;
+        ++nh;
       }
-      if (pl > 1e-14) {
-        np[sz] = pl; nlo[sz] = lo; nhi[sz] = ym; nym[sz] = 0.5 * (lo + ym); nit[sz] = it + 1; ++sz;
-      }
+      p = p * (right ? pa : 1.0 - pa);
+      if (right) lo = ym; else hi = ym;
     } else {
-      if (sz + 1 > CAP) continue;
-      const double nl = d > 0 ? lo : ym, nh = d > 0 ? ym : hi;
-      np[sz] = p; nlo[sz] = nl; nhi[sz] = nh; nym[sz] = 0.5 * (nl + nh); nit[sz] = it + 1; ++sz;
+      if (d > 0) hi = ym; else lo = ym;
+    }
+    ym = 0.5 * (lo + hi);
+    ++it;
+  }
+  // merge: path nodes are a prefix ordered by decreasing probability; take
+  // hedges greedily when more probable than the next path node.
+  int ip = 0;
+  while (n < K && (ip < np || nh > 0)) {
+    int bh = -1;
+    for (int k = 0; k < nh; ++k)
+      if (bh < 0 || hp[k] > hp[bh]) bh = k;
+    if (ip < np && (bh < 0 || pp[ip] >= hp[bh])) {
+      out[n++] = py[ip++];
+    } else {
+      // a hedge is useless if its parent path node will not be evaluated; its
+      // parent was evaluated iff it was taken (parents precede in pp order).
+      out[n++] = hy[bh];
+      hy[bh] = hy[nh - 1]; hp[bh] = hp[nh - 1]; --nh;
     }
   }
   return n;

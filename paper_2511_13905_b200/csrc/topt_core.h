@@ -167,10 +167,9 @@ struct Result {
 };
 
 // Controller scratch (kept in the Plan so device threads carry no big stack).
-constexpr int CAND_CAP = 96;
+constexpr int CAND_CAP = 64;
 struct Scratch {
   double np[CAND_CAP], nlo[CAND_CAP], nhi[CAND_CAP], nym[CAND_CAP];
-  int32_t nit[CAND_CAP];
   double jh[MAX_M * MAX_M], jp[MAX_M * MAX_M];
 };
 
