@@ -97,7 +97,10 @@ typedef struct {
   double alpha;
   double beta;
   int32_t fallback;
+  int32_t local_sweeps;          /* CTA-local sweeps on gathered active elements */
+  int32_t gathered;              /* 1 if the active sets were gathered */
   int32_t reserved;
+  double active;                 /* active elements after the last compacted sweep */
 } topt_proj_meta;
 
 /* topt::ConstraintLinearization, projection.hpp:17-41.  grad/gd_step are
@@ -169,6 +172,9 @@ int topt_b200_set_stream(topt_b200_ctx* ctx, void* stream);
 int topt_b200_set_profiling(topt_b200_ctx* ctx, int enabled);
 int topt_b200_kernel_time(topt_b200_ctx* ctx, double* total_ms, int64_t* launches,
                           double* max_ms);
+
+/* Debug: per-pass device timestamps of the next persistent launch. */
+int topt_b200_debug_trace(topt_b200_ctx* ctx, int enable, unsigned long long* out);
 
 void topt_b200_default_options(topt_proj_options* o);
 void topt_b200_default_settings(topt_pgd_settings* s);

@@ -40,7 +40,8 @@ class ProjMeta(C.Structure):
                 ("passes", C.c_int32), ("sweeps", C.c_int32), ("stage1_row", C.c_int32),
                 ("near_ties", C.c_int32), ("min_margin", C.c_double),
                 ("bisect_iters", C.c_int32 * MAX_M), ("alpha", C.c_double),
-                ("beta", C.c_double), ("fallback", C.c_int32), ("reserved", C.c_int32)]
+                ("beta", C.c_double), ("fallback", C.c_int32), ("local_sweeps", C.c_int32),
+                ("gathered", C.c_int32), ("reserved", C.c_int32), ("active", C.c_double)]
 
 
 class Linearization(C.Structure):
@@ -74,7 +75,7 @@ EXPORTS = [
     "topt_b200_build", "topt_b200_delta_of_y", "topt_b200_constraint_residual_h",
     "topt_b200_project", "topt_b200_project_dev", "topt_b200_owner_map",
     "topt_b200_pgd_step", "topt_b200_pgd_step_dev", "topt_b200_step_direction",
-    "topt_b200_set_profiling", "topt_b200_kernel_time",
+    "topt_b200_set_profiling", "topt_b200_kernel_time", "topt_b200_debug_trace",
 ]
 
 _lib = None
@@ -113,6 +114,7 @@ def load():
         "topt_b200_step_direction": [vp, i64, vp, vp, vp, vp, vp, i32, d, vp, vp, vp, vp, vp,
                                      vp],
         "topt_b200_set_profiling": [vp, C.c_int],
+        "topt_b200_debug_trace": [vp, C.c_int, vp],
         "topt_b200_kernel_time": [vp, vp, vp, vp],
         "topt_b200_default_options": [vp],
         "topt_b200_default_settings": [vp],

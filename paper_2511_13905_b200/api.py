@@ -106,6 +106,8 @@ class ProjectionResult:
     min_margin: float = float("inf")
     bisect_iters: Optional[list] = None
     mask: object = None
+    local_sweeps: int = 0
+    gathered: bool = False
 
 
 def _meta_to_result(meta: L.ProjMeta, delta, y, slacks, m, mask=None) -> ProjectionResult:
@@ -115,7 +117,8 @@ def _meta_to_result(meta: L.ProjMeta, delta, y, slacks, m, mask=None) -> Project
         converged=bool(meta.converged), curvature_violations=meta.curvature_violations,
         passes=meta.passes, sweeps=meta.sweeps, stage1_row=meta.stage1_row,
         near_ties=meta.near_ties, min_margin=meta.min_margin,
-        bisect_iters=list(meta.bisect_iters[:m]), mask=mask)
+        bisect_iters=list(meta.bisect_iters[:m]), mask=mask, local_sweeps=meta.local_sweeps,
+        gathered=bool(meta.gathered))
 
 
 def _is_torch_cuda(a) -> bool:

@@ -7,9 +7,11 @@
 // the next pass's command into the device-resident Plan.  The host only
 // relaunches and polls one int (the next phase); no partial sum or decision
 // ever crosses PCIe.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -21,25 +23,43 @@
 #include "topt_core.h"
 
 using namespace topt_b200;
+namespace cg = cooperative_groups;
 
 namespace {
 
 constexpr int RED_SCRATCH = NWARP * 160;   // doubles (max NS = 16 + 136)
 
+// Combine all CTAs' partial slots in a fixed order into totals[].  Group g
+// sums CTAs g, g+G, g+2G, ... sequentially (loads batched 8 deep, the
+// addition order unchanged); groups combine in order.  The order depends only
+// on (nb, ns): deterministic.
 __device__ void finish_reduce(const double* partials, int nb, int ns, int phase,
-                              double* totals, double* smem) {
-  // Group g sums CTAs g, g+G, g+2G, ... sequentially; groups combine in
-  // order.  The order depends only on (nb, ns): deterministic.
+                              double* totals, double* smem, int stride = PMAX) {
   for (int s0 = 0; s0 < ns; s0 += BLOCK) {
     const int per = min(ns - s0, BLOCK);
-    int G = 1;
-    while (G * 2 * per <= BLOCK && G * 2 <= nb && G < 64) G *= 2;
+    int G = BLOCK / per;
+    if (G > nb) G = nb;
+    if (G > 64) G = 64;
+    if (G < 1) G = 1;
     const int t = threadIdx.x;
     const int s = t % per, g = t / per;
     if (g < G) {
       const int op = slot_op(phase, s0 + s);
-      double r = __ldcg(partials + (size_t)g * PMAX + s0 + s);
-      for (int b = g + G; b < nb; b += G) r = apply_op(op, r, __ldcg(partials + (size_t)b * PMAX + s0 + s));
+      const double* src = partials + s0 + s;
+      // issue every load of this thread's chain before combining (MLP)
+      constexpr int CH = 16;
+      double r = __ldcg(src + (size_t)g * stride);
+      for (int b0 = g + G; b0 < nb; b0 += CH * G) {
+        double v[CH];
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          const int b = b0 + k * G;
+          v[k] = (b < nb) ? __ldcg(src + (size_t)b * stride) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < CH; ++k)
+          if (b0 + k * G < nb) r = apply_op(op, r, v[k]);
+      }
       smem[g * per + s] = r;
     }
     __syncthreads();
@@ -53,17 +73,53 @@ __device__ void finish_reduce(const double* partials, int nb, int ns, int phase,
   }
 }
 
-__global__ void __launch_bounds__(BLOCK) k_pass(Plan* plan, double* partials,
+// Copy the device-resident Plan into this CTA's shared memory, run the
+// controller on it (thread 0), and write it back.  The controller's many
+// small dependent accesses then see shared-memory latency, not L2.
+__device__ __forceinline__ void copy_words(int* dst, const int* src, int nwords, bool cg_store) {
+  for (int k = threadIdx.x; k < nwords; k += BLOCK) {
+    const int v = __ldcg(src + k);
+    if (cg_store) __stcg(dst + k, v); else dst[k] = v;
+  }
+}
+
+__device__ void control_step(Plan* plan, Plan* s_plan, const double* totals) {
+  // live controller state: [0, walks of the m rows) and [nt, sc); the
+  // Problem is read-only and Scratch is scratch.
+  const int m = plan->P.m;
+  const int endA = (int)(offsetof(Plan, w) + sizeof(Walk) * (size_t)m) / 4;
+  const int begB = (int)offsetof(Plan, nt) / 4, endB = (int)offsetof(Plan, sc) / 4;
+  const int begCmd = (int)offsetof(Plan, cmd) / 4;
+  int* gp = reinterpret_cast<int*>(plan);
+  int* sp = reinterpret_cast<int*>(s_plan);
+  copy_words(sp, gp, endA, false);
+  copy_words(sp + begB, gp + begB, endB - begB, false);
+  __syncthreads();
+  if (threadIdx.x == 0) plan_consume(*s_plan, totals);
+  __syncthreads();
+  for (int k = begCmd + threadIdx.x; k < endA; k += BLOCK) __stcg(gp + k, sp[k]);
+  for (int k = begB + threadIdx.x; k < endB; k += BLOCK) __stcg(gp + k, sp[k]);
+  __threadfence();
+  __syncthreads();
+}
+
+__device__ __forceinline__ void load_cmd(const Plan* plan, Cmd* s_cmd) {
+  const int* src = reinterpret_cast<const int*>(&plan->cmd);
+  int* dst = reinterpret_cast<int*>(s_cmd);
+  for (int k = threadIdx.x; k < (int)(sizeof(Cmd) / sizeof(int)); k += BLOCK)
+    dst[k] = __ldcg(src + k);
+  __syncthreads();
+}
+
+// Multi-launch mode: one launch per pass; the last CTA runs the controller.
+__global__ void __launch_bounds__(BLOCK, 1) k_pass(Plan* plan, double* partials,
                                                 unsigned* counter, double* totals) {
   __shared__ Cmd s_cmd;
   __shared__ double s_red[RED_SCRATCH];
+  __shared__ double s_tot[PMAX];
   __shared__ int s_last;
-  {
-    const int* src = reinterpret_cast<const int*>(&plan->cmd);
-    int* dst = reinterpret_cast<int*>(&s_cmd);
-    for (int k = threadIdx.x; k < (int)(sizeof(Cmd) / sizeof(int)); k += BLOCK) dst[k] = src[k];
-  }
-  __syncthreads();
+  extern __shared__ int4 s_dyn[];
+  load_cmd(plan, &s_cmd);
   if (s_cmd.phase == PH_DONE) return;
   PassCtx c;
   c.plan = plan;
@@ -72,6 +128,10 @@ __global__ void __launch_bounds__(BLOCK) k_pass(Plan* plan, double* partials,
   c.smem = s_red;
   c.i0 = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
   c.stride = (int64_t)gridDim.x * BLOCK;
+  c.list = nullptr;
+  c.list_cnt = nullptr;
+  c.fixC = c.fixS = nullptr;
+  c.list_cap = 0;
   run_pass(c);
   __threadfence();
   __syncthreads();
@@ -79,11 +139,113 @@ __global__ void __launch_bounds__(BLOCK) k_pass(Plan* plan, double* partials,
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  finish_reduce(partials, gridDim.x, s_cmd.nslots, s_cmd.phase, totals, s_red);
+  finish_reduce(partials, gridDim.x, s_cmd.nslots, s_cmd.phase, s_tot, s_red);
+  control_step(plan, reinterpret_cast<Plan*>(s_dyn), s_tot);
   if (threadIdx.x == 0) {
-    plan_consume(*plan, totals);
     *counter = 0u;
     __threadfence();
+  }
+  (void)totals;
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Persistent mode: ONE cooperative launch runs every pass of the job.
+// Every CTA holds a private shared-memory copy of the controller state; after
+// each pass the CTAs meet at a grid barrier, then EVERY CTA combines all
+// partials in the same fixed order and runs the same controller step, so all
+// CTAs hold bit-identical commands without a second barrier or any global
+// command broadcast.  Partials are double-buffered across passes.
+constexpr size_t PLAN_SMEM = (sizeof(Plan) + 255) & ~size_t(255);
+
+struct GatherBufs {
+  int* blk_cnt;
+  double* g_a;
+  double* g_r;
+  int* g_row;
+  double* g_fix;
+};
+
+__global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
+                                                   unsigned long long* trace, GatherBufs gb) {
+  __shared__ double s_red[RED_SCRATCH];
+  __shared__ double s_tot[PMAX];
+  __shared__ double s_fixC[MAX_M], s_fixS[MAX_M];
+  __shared__ int s_lcnt[NWARP];
+  __shared__ int s_nitems;
+  extern __shared__ int4 s_dyn[];
+  Plan& sp = *reinterpret_cast<Plan*>(s_dyn);
+  char* s_work = reinterpret_cast<char*>(s_dyn) + PLAN_SMEM;   // lists, later gathered items
+  uint32_t* s_list = reinterpret_cast<uint32_t*>(s_work);
+  cg::grid_group grid = cg::this_grid();
+  const int nb = gridDim.x;
+  {  // load the controller state (everything but scratch)
+    const int* gp = reinterpret_cast<const int*>(plan);
+    int* spi = reinterpret_cast<int*>(&sp);
+    const int nw = (int)(offsetof(Plan, sc) / 4);
+    for (int k = threadIdx.x; k < nw; k += BLOCK) spi[k] = __ldcg(gp + k);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) g_ctl_marks = nullptr;
+  for (int pass = 0; pass < 8192; ++pass) {
+    if (sp.cmd.phase == PH_DONE) break;
+    unsigned long long* tr = (trace && pass < 64) ? trace + pass * 8 : nullptr;
+    if (tr && blockIdx.x == 0 && threadIdx.x == 0) { tr[0] = gtimer(); tr[5] = sp.cmd.phase; }
+    double* part = partials + (size_t)(pass & 1) * PMAX * nb;
+    PassCtx c;
+    c.plan = &sp;
+    c.cmd = &sp.cmd;
+    c.out = part + (size_t)blockIdx.x * PMAX;
+    c.smem = s_red;
+    c.i0 = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
+    c.stride = (int64_t)nb * BLOCK;
+    c.list = sp.P.compact_cap > 0 ? s_list : nullptr;
+    c.list_cnt = s_lcnt;
+    c.fixC = s_fixC;
+    c.fixS = s_fixS;
+    c.list_cap = sp.P.compact_cap;
+    c.blk_cnt = gb.blk_cnt;
+    c.g_a = gb.g_a;
+    c.g_r = gb.g_r;
+    c.g_row = gb.g_row;
+    c.g_fix = gb.g_fix;
+    c.it_a = reinterpret_cast<double*>(s_work);
+    c.it_r = c.it_a + GATHER_CAP;
+    c.it_row = reinterpret_cast<int8_t*>(c.it_r + GATHER_CAP);
+    c.n_items = &s_nitems;
+    if (sp.cmd.phase == PH_SWEEP && sp.cmd.local) {   // CTA-local sweep: no barrier
+      local_sweep(c, s_tot);
+      if (threadIdx.x < 32) plan_consume_warp(sp, s_tot);
+      __syncthreads();
+      continue;
+    }
+    run_pass(c);
+    if (tr && threadIdx.x == 0) {
+      if (blockIdx.x == 0) tr[1] = gtimer();
+      atomicMax(tr + 6, gtimer());
+    }
+    __threadfence();
+    grid.sync();
+    if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[2] = gtimer();
+    if (sp.cmd.phase == PH_GATHER) gather_load(c, nb);
+    finish_reduce(part, nb, sp.cmd.nslots, sp.cmd.phase, s_tot, s_red);
+    if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
+      tr[3] = gtimer();
+      g_ctl_marks = trace + 512 + pass * 8;
+    }
+    if (threadIdx.x < 32) plan_consume_warp(sp, s_tot);
+    __syncthreads();
+    if (tr && blockIdx.x == 0 && threadIdx.x == 0) { tr[4] = gtimer(); g_ctl_marks = nullptr; }
+  }
+  if (blockIdx.x == 0) {  // publish the final state (results) once
+    int* gp = reinterpret_cast<int*>(plan);
+    const int* spi = reinterpret_cast<const int*>(&sp);
+    const int b0 = (int)(offsetof(Plan, cmd) / 4), nw = (int)(offsetof(Plan, sc) / 4);
+    for (int k = b0 + threadIdx.x; k < nw; k += BLOCK) gp[k] = spi[k];
   }
 }
 
@@ -137,6 +299,17 @@ struct topt_b200_ctx {
   int64_t launches = 0;
   DevBuf bufs[16];
   int profile = 0;
+  int persistent = 1;       // one cooperative launch per job when possible
+  int coop_grid = 0;        // co-resident CTAs for k_step
+  int compact = 1;          // active-set compaction of bisection sweeps
+  int* d_blk_cnt = nullptr;
+  double* d_ga = nullptr;
+  double* d_gr = nullptr;
+  int* d_grow = nullptr;
+  double* d_gfix = nullptr;
+  int max_dyn_smem = 0;
+  int trace_on = 0;
+  unsigned long long* d_trace = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double prof_ms = 0.0, prof_max = 0.0;
   int64_t prof_n = 0;
@@ -188,15 +361,52 @@ const char* status_msg(int st) {
 
 // Run a plan to completion on the device.  hp.P must be filled.
 int run_plan(topt_b200_ctx* ctx, Plan& hp) {
-  const int64_t per_thread = (hp.P.n + (int64_t)ctx->grid * BLOCK - 1) / ((int64_t)ctx->grid * BLOCK);
-  hp.P.ours_len = (double)per_thread + (double)ctx->grid + 64.0;
+  const bool persistent = ctx->persistent && ctx->coop_grid > 0;
+  const int grid = persistent ? ctx->coop_grid : ctx->grid;
+  const int64_t per_thread = (hp.P.n + (int64_t)grid * BLOCK - 1) / ((int64_t)grid * BLOCK);
+  hp.P.ours_len = (double)per_thread + (double)grid + 64.0;
+  size_t dyn_smem = sizeof(Plan);
+  hp.P.compact_cap = 0;
+  if (persistent && ctx->compact) {
+    const int64_t cap = 32 * per_thread;
+    size_t bytes = (size_t)NWARP * (size_t)cap * sizeof(uint32_t);
+    const size_t item_bytes = (size_t)GATHER_CAP * (2 * sizeof(double) + 1);
+    if (bytes < item_bytes) bytes = item_bytes;
+    if (cap > 0 && PLAN_SMEM + bytes <= (size_t)ctx->max_dyn_smem && hp.P.n < (int64_t)4000000000LL) {
+      hp.P.compact_cap = (int32_t)cap;
+      dyn_smem = PLAN_SMEM + bytes;
+    }
+  }
   plan_start(hp);
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_plan, &hp, sizeof(Plan), cudaMemcpyHostToDevice, ctx->stream));
   int phase = hp.cmd.phase;
+  if (persistent && phase != PH_DONE) {
+    unsigned long long* tr = ctx->trace_on ? ctx->d_trace : nullptr;
+    if (tr) cudaMemsetAsync(tr, 0, 128 * 8 * sizeof(unsigned long long), ctx->stream);
+    GatherBufs gb{ctx->d_blk_cnt, ctx->d_ga, ctx->d_gr, ctx->d_grow, ctx->d_gfix};
+    void* args[] = {&ctx->d_plan, &ctx->d_part, &tr, &gb};
+    if (ctx->profile) cudaEventRecord(ctx->ev0, ctx->stream);
+    CUDA_TRY(ctx, cudaLaunchCooperativeKernel((void*)k_step, grid, BLOCK, args, dyn_smem,
+                                              ctx->stream));
+    ctx->launches++;
+    if (ctx->profile) cudaEventRecord(ctx->ev1, ctx->stream);
+    CUDA_TRY(ctx, cudaMemcpyAsync(&hp, ctx->d_plan, sizeof(Plan), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->profile) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+      ctx->prof_ms += ms;
+      ctx->prof_max = std::max(ctx->prof_max, (double)ms);
+      ctx->prof_n++;
+    }
+    if (hp.cmd.phase != PH_DONE) return fail(ctx, TOPT_ERR_INTERNAL, "plan did not terminate");
+    if (hp.res.status != ST_OK) return fail(ctx, hp.res.status, status_msg(hp.res.status));
+    return TOPT_OK;
+  }
   for (int it = 0; phase != PH_DONE && it < 4096; ++it) {
     if (ctx->profile) cudaEventRecord(ctx->ev0, ctx->stream);
-    k_pass<<<ctx->grid, BLOCK, 0, ctx->stream>>>(ctx->d_plan, ctx->d_part, ctx->d_counter,
-                                                 ctx->d_totals);
+    k_pass<<<ctx->grid, BLOCK, sizeof(Plan), ctx->stream>>>(ctx->d_plan, ctx->d_part,
+                                                            ctx->d_counter, ctx->d_totals);
     ctx->launches++;
     CUDA_TRY(ctx, cudaGetLastError());
     if (ctx->profile) cudaEventRecord(ctx->ev1, ctx->stream);
@@ -237,6 +447,9 @@ void fill_meta(const Plan& hp, topt_proj_meta* meta) {
   meta->alpha = r.alpha;
   meta->beta = r.beta;
   meta->fallback = r.fallback;
+  meta->local_sweeps = r.local_sweeps;
+  meta->gathered = r.gathered;
+  meta->active = r.active;
 }
 
 void default_opts(ProjOptions& o) {
@@ -341,16 +554,36 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   cudaDeviceProp prop;
   cudaGetDeviceProperties(&prop, device);
   ctx->nsm = prop.multiProcessorCount;
-  ctx->grid = ctx->nsm * 4;
+  ctx->grid = ctx->nsm * 2;
   bool ok = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) == cudaSuccess;
   ctx->own_stream = ok;
   ok = ok && cudaMalloc(&ctx->d_plan, sizeof(Plan)) == cudaSuccess;
-  ok = ok && cudaMalloc(&ctx->d_part, sizeof(double) * PMAX * ctx->grid) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_part, 2 * sizeof(double) * PMAX * ctx->grid) == cudaSuccess;
   ok = ok && cudaMalloc(&ctx->d_counter, sizeof(unsigned)) == cudaSuccess;
   ok = ok && cudaMalloc(&ctx->d_totals, sizeof(double) * PMAX) == cudaSuccess;
   ok = ok && cudaMalloc(&ctx->d_err, sizeof(int)) == cudaSuccess;
   ok = ok && cudaMallocHost(&ctx->h_phase, sizeof(int)) == cudaSuccess;
   ok = ok && cudaMemset(ctx->d_counter, 0, sizeof(unsigned)) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_trace, 128 * 8 * sizeof(unsigned long long)) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_blk_cnt, sizeof(int) * ctx->grid) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_ga, sizeof(double) * GATHER_CAP) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_gr, sizeof(double) * GATHER_CAP) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_grow, sizeof(int) * GATHER_CAP) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_gfix, sizeof(double) * 2 * MAX_M * ctx->grid) == cudaSuccess;
+  ctx->max_dyn_smem = 160 * 1024;
+  ok = ok && cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  ctx->max_dyn_smem) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(Plan)) == cudaSuccess;
+  if (ok) {
+    int per_sm = 0, coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step, BLOCK, (int)sizeof(Plan));
+    ctx->coop_grid = coop ? per_sm * ctx->nsm : 0;
+    if (ctx->coop_grid > ctx->grid) ctx->coop_grid = ctx->grid;
+    if (const char* e = getenv("TOPT_B200_PERSISTENT")) ctx->persistent = atoi(e);
+    if (const char* e = getenv("TOPT_B200_COMPACT")) ctx->compact = atoi(e);
+  }
   ok = ok && cudaEventCreate(&ctx->ev0) == cudaSuccess;
   ok = ok && cudaEventCreate(&ctx->ev1) == cudaSuccess;
   if (!ok) { topt_b200_ctx_destroy(ctx); return TOPT_ERR_CUDA; }
@@ -369,6 +602,12 @@ void topt_b200_ctx_destroy(topt_b200_ctx* ctx) {
   cudaFree(ctx->d_counter);
   cudaFree(ctx->d_totals);
   cudaFree(ctx->d_err);
+  cudaFree(ctx->d_trace);
+  cudaFree(ctx->d_blk_cnt);
+  cudaFree(ctx->d_ga);
+  cudaFree(ctx->d_gr);
+  cudaFree(ctx->d_grow);
+  cudaFree(ctx->d_gfix);
   if (ctx->h_phase) cudaFreeHost(ctx->h_phase);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -384,6 +623,19 @@ int topt_b200_set_stream(topt_b200_ctx* ctx, void* stream) {
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   ctx->stream = (cudaStream_t)stream;
   ctx->own_stream = false;
+  return TOPT_OK;
+}
+
+// Debug: per-pass device timestamps of the last persistent launch
+// (64 passes x 8 u64: start, block0 pass end, finisher start, reduce end,
+// control end, phase, last CTA pass end).  enable=1 arms, enable=0 reads.
+int topt_b200_debug_trace(topt_b200_ctx* ctx, int enable, unsigned long long* out) {
+  if (!ctx) return TOPT_ERR_INTERNAL;
+  ctx->trace_on = enable;
+  if (out) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaMemcpy(out, ctx->d_trace, 128 * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  }
   return TOPT_OK;
 }
 

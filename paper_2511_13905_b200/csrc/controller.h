@@ -24,12 +24,31 @@
 // reference's own rounding noise (counted in Result::near_ties).
 #pragma once
 #include <math.h>
+#include <string.h>
 
 #include "topt_core.h"
 
 namespace topt_b200 {
 
 constexpr double kUnit = 1.1102230246251565e-16;  // 2^-53
+
+// Optional device-side timeline marks (debug builds of the trace only).
+#if defined(__CUDACC__)
+__device__ unsigned long long* g_ctl_marks = nullptr;
+__host__ __device__ __forceinline__ void ctl_mark(int k) {
+#if defined(__CUDA_ARCH__)
+  if (g_ctl_marks) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_ctl_marks[k] = t;
+  }
+#else
+  (void)k;
+#endif
+}
+#else
+inline void ctl_mark(int) {}
+#endif
 constexpr double kGradFloor = 1e-300;              // projection.cpp:19
 
 TOPT_HD double gamma_k(double k) { return k * kUnit / (1.0 - k * kUnit); }
@@ -64,7 +83,7 @@ TOPT_HD int slot_op(int phase, int slot) {
 // m x m full-pivot LU + solve (mirrors Eigen::FullPivLU as used at
 // projection.cpp:401-407; same algorithm as oracle.c's orc_fullpiv_solve).
 // a is column-major m x m and is destroyed.  Returns false if not invertible.
-TOPT_HDN inline bool fullpiv_solve(int m, double* a, const double* b, double* x) {
+TOPT_NOINLINE bool fullpiv_solve(int m, double* a, const double* b, double* x) {
   int rowperm[MAX_M], colperm[MAX_M];
 #define A_(i, j) a[(j) * m + (i)]
   for (int i = 0; i < m; ++i) rowperm[i] = colperm[i] = i;
@@ -117,78 +136,136 @@ TOPT_HDN inline bool fullpiv_solve(int m, double* a, const double* b, double* x)
 // ---------------------------------------------------------------------------
 // Bisection walk
 
-// Exact evaluation lookup among this sweep's candidates.
-TOPT_HD bool walk_lookup(const Walk& w, double y, double* R) {
-  int hit = -1;
-#pragma unroll
-  for (int k = 0; k < MAX_K; ++k)
-    if (k < w.nc && w.cy[k] == y) hit = k;
-  if (hit < 0) return false;
-  *R = w.cR[hit];
-  return true;
+// This sweep's evaluations for one row: candidate duals cy[k] and the
+// partial slots t2[2k] (sum of terms, not yet offset by -ghat), t2[2k+1] (slope).
+struct Evals {
+  const double* cy;
+  const double* t2;
+  int nc;
+};
+
+// Candidates are mostly consumed in generation order (the predicted path),
+// so the search starts just after the previous hit.
+TOPT_HD bool evals_lookup(const Evals& ev, double ghat, double y, double* R, int* hint) {
+  const int nc = ev.nc;
+  int k = *hint;
+  for (int c = 0; c < nc; ++c) {
+    if (k >= nc) k = 0;
+    if (ev.cy[k] == y) { *R = ev.t2[2 * k] - ghat; *hint = k + 1; return true; }
+    ++k;
+  }
+  return false;
 }
 
-// +1: reference sees r(y) > 0 ; -1: reference sees r(y) <= 0 ; 0: unknown.
-TOPT_HDN inline int walk_decide(Walk& w, double y, bool record) {
-  double R;
-  if (walk_lookup(w, y, &R)) {
-    if (record) {
-      const double mg = fabs(R) / w.E;
-      if (mg < w.min_margin) w.min_margin = mg;
-      if (fabs(R) <= w.E) w.near_ties++;
-      w.n_direct++;
-    }
-    return R > 0.0 ? 1 : -1;
+// Fold this sweep's evaluations into the walk's knowledge (brackets).
+TOPT_HD void walk_ingest(Walk& w, const Evals& ev) {
+  for (int k = 0; k < ev.nc; ++k) {
+    const double y = ev.cy[k], R = ev.t2[2 * k] - w.ghat, S = ev.t2[2 * k + 1];
+    if (R <= 0.0 && (!w.hasA || y > w.ya)) { w.hasA = 1; w.ya = y; w.Ra = R; w.Sa = S; }
+    if (R > 0.0 && (!w.hasB || y < w.yb)) { w.hasB = 1; w.yb = y; w.Rb = R; w.Sb = S; }
+    if (R < -w.E && (!w.hasL || y > w.yL)) { w.hasL = 1; w.yL = y; }
+    if (R > w.E && (!w.hasH || y < w.yH)) { w.hasH = 1; w.yH = y; }
   }
-  if (w.hasH && w.yH <= y) return 1;
-  if (w.hasL && w.yL >= y) return -1;
-  return 0;
 }
 
 // Replay the reference walk as far as evaluations/certificates allow.
-TOPT_HDN inline void walk_advance(Walk& w, const ProjOptions& o) {
+TOPT_HD void walk_advance(Walk& w, const ProjOptions& o, const Evals& ev) {
   if (w.status == WK_DONE || w.status == WK_INFEASIBLE || w.status == WK_IDLE) return;
+  const bool hasL = w.hasL, hasH = w.hasH;
+  const double yL = w.yL, yH = w.yH, E = w.E, ghat = w.ghat;
+  int near = 0, direct = 0, hint = 0;
+  double minm = w.min_margin;
   if (!w.feas_done) {
     // projection.cpp:80-94: r(y_lo) > 0 (down) / r(y_hi) < 0 (up) => infeasible
     const double yb = w.up ? w.bp_hi : w.bp_lo;
     double R;
     int infeasible;
-    if (walk_lookup(w, yb, &R)) {
+    if (evals_lookup(ev, ghat, yb, &R, &hint)) {
       infeasible = w.up ? (R < 0.0) : (R > 0.0);
-      const double mg = fabs(R) / w.E;
-      if (mg < w.min_margin) w.min_margin = mg;
-      if (fabs(R) <= w.E) w.near_ties++;
-    } else if (w.hasH && w.yH <= yb) {
+      minm = dmin_(minm, fabs(R) / E);
+      near += (fabs(R) <= E);
+    } else if (hasH && yH <= yb) {
       infeasible = w.up ? 0 : 1;
-    } else if (w.hasL && w.yL >= yb) {
+    } else if (hasL && yL >= yb) {
       infeasible = w.up ? 1 : 0;
     } else {
       w.status = WK_NEED;
       return;
     }
+    w.near_ties += near;
+    w.min_margin = minm;
+    near = 0;
     if (infeasible) { w.status = WK_INFEASIBLE; return; }
     w.feas_done = 1;
   }
-  while ((w.hi - w.lo) > o.tol_b && w.iters < o.binary_maxiter) {
-    const int d = walk_decide(w, w.ym, true);
-    if (d == 0) { w.status = WK_NEED; return; }
-    if (d > 0) w.hi = w.ym; else w.lo = w.ym;
-    w.ym = 0.5 * (w.lo + w.hi);
-    ++w.iters;
+  double lo = w.lo, hi = w.hi, ym = w.ym;
+  int it = w.iters;
+  const double tol_b = o.tol_b;
+  const int maxit = o.binary_maxiter;
+  int status = WK_DONE;
+  while ((hi - lo) > tol_b && it < maxit) {
+    int d;
+    if (hasH && yH <= ym) {
+      d = 1;
+    } else if (hasL && yL >= ym) {
+      d = -1;
+    } else {
+      double R;
+      if (!evals_lookup(ev, ghat, ym, &R, &hint)) { status = WK_NEED; break; }
+      minm = dmin_(minm, fabs(R) / E);
+      near += (fabs(R) <= E);
+      ++direct;
+      d = R > 0.0 ? 1 : -1;
+    }
+    if (d > 0) hi = ym; else lo = ym;
+    ym = 0.5 * (lo + hi);
+    ++it;
   }
-  w.status = WK_DONE;
-  w.y = w.ym;
+  w.lo = lo; w.hi = hi; w.ym = ym; w.iters = it;
+  w.near_ties += near;
+  w.n_direct += direct;
+  w.min_margin = minm;
+  w.status = status;
+  if (status == WK_DONE) w.y = ym;
+}
+
+// Cheap, host/device-identical approximations used ONLY to rank speculative
+// midpoints (erfc/log cost ~1000 dependent cycles each on one GPU thread).
+TOPT_HD double approx_log2(double x) {
+  uint64_t b;
+  memcpy(&b, &x, sizeof(b));
+  const int64_t e = (int64_t)((b >> 52) & 0x7ff) - 1023;
+  const double m = (double)(b & 0xfffffffffffffull) * 2.220446049250313e-16;  // [0,1)
+  return (double)e + m;
+}
+#if defined(__CUDA_ARCH__)
+#define TOPT_FDIV(a, b) __fdividef((a), (b))
+#else
+#define TOPT_FDIV(a, b) ((a) / (b))
+#endif
+TOPT_HD double approx_ncdf_upper(double t) {  // ~ P(Z > t), monotone, in (0, 1)
+  float u = (float)(2.5 * t);
+  if (!(u == u)) u = 0.0f;
+  if (u > 1e30f) u = 1e30f;
+  if (u < -1e30f) u = -1e30f;
+  return (double)(0.5f - 0.5f * TOPT_FDIV(u, 1.0f + fabsf(u)));
 }
 
 // Root estimate used to choose speculative midpoints (never a decision).
 struct RootEst {
   int kind;        // 0: gaussian(ye, sig) ; 1: log-uniform prior below 0 ; 2: above 0
-  double ye, sig, L;
+  double ye, sig, L, inv_sig;
 };
 
-TOPT_HDN inline RootEst walk_estimate(const Walk& w) {
+TOPT_HD RootEst walk_estimate_(const Walk& w);
+TOPT_NOINLINE RootEst walk_estimate(const Walk& w) {
+  RootEst e = walk_estimate_(w);
+  e.inv_sig = 1.0 / e.sig;
+  return e;
+}
+TOPT_HD RootEst walk_estimate_(const Walk& w) {
   RootEst e;
-  e.kind = 0; e.ye = 0.0; e.sig = 1.0; e.L = 0.0;
+  e.kind = 0; e.ye = 0.0; e.sig = 1.0; e.L = 0.0; e.inv_sig = 1.0;
   if (w.hasA && w.hasB && w.ya < w.yb) {
     const double ya = w.ya, yb = w.yb;
     double sec = ya - w.Ra * (yb - ya) / (w.Rb - w.Ra);
@@ -216,7 +293,7 @@ TOPT_HDN inline RootEst walk_estimate(const Walk& w) {
       return e;
     }
     e.kind = 1;
-    e.L = log(fabs(w.lo) + 1e-300);
+    e.L = approx_log2(fabs(w.lo) + 1e-300);
     return e;
   }
   if (w.hasA && w.Sa > 0.0) {  // root in [0, bp_hi], r(0) < 0 known
@@ -225,89 +302,104 @@ TOPT_HDN inline RootEst walk_estimate(const Walk& w) {
     return e;
   }
   e.kind = 2;
-  e.L = log(fabs(w.hi) + 1e-300);
+  e.L = approx_log2(fabs(w.hi) + 1e-300);
   return e;
 }
 
 // Probability that the root lies above y.
 TOPT_HDN inline double est_p_above(const RootEst& e, double y) {
-  if (e.kind == 0) return 0.5 * erfc((y - e.ye) / (e.sig * 1.4142135623730951));
+  if (e.kind == 0) return approx_ncdf_upper((y - e.ye) * e.inv_sig);
   const double ay = fabs(y);
   if (!(ay > 0.0)) return e.kind == 1 ? 0.0 : 1.0;
-  double p = (log(ay) - (e.L - 46.0)) / 46.0;  // P(|root| < |y|), log-uniform prior
+  double p = (approx_log2(ay) - (e.L - 66.0)) / 66.0;  // P(|root| < |y|), log-uniform prior
   p = dmin_(dmax_(p, 0.0), 1.0);
   return e.kind == 1 ? p : 1.0 - p;
 }
 
 // Choose up to K midpoints of the walk's remaining decision tree to evaluate
 // next: the predicted path (most probable branch at every uncertain level),
-// plus first-level alternatives ("hedges") of its least certain levels,
-// ranked by the probability of being visited.  O(K + certain levels).
-TOPT_HDN inline int walk_candidates(const Walk& w, const ProjOptions& o, int K, double* out,
-                                    Scratch& scr) {
+// plus first-level alternatives ("hedges") at its least certain levels,
+// ranked by the probability of being visited.  O(K + certain levels), all
+// state in registers.
+constexpr int MAX_HEDGE = 4;
+// Predicted path (most probable branch at every uncertain level) plus the
+// MAX_HEDGE most probable first-level alternatives, merged by probability of
+// being visited.  Per-level work is a few register operations (the hedge
+// set is kept in registers; only the path is written to local memory).
+TOPT_HD int walk_candidates(const Walk& w, const ProjOptions& o, int K, double* out,
+                            Scratch& scr) {
+  (void)scr;
   int n = 0;
   if (w.status != WK_NEED || K <= 0) return 0;
   if (!w.feas_done) out[n++] = w.up ? w.bp_hi : w.bp_lo;
+  ctl_mark(4);
   const RootEst e = walk_estimate(w);
-  double* pp = scr.np;    // path node probability
-  double* py = scr.nlo;   // path node y
-  double* hp = scr.nhi;   // hedge probability
-  double* hy = scr.nym;   // hedge y
-  int np = 0, nh = 0;
+  ctl_mark(5);
+  double py[MAX_K], pp[MAX_K];
+  double hy[MAX_HEDGE], hp[MAX_HEDGE];
+#pragma unroll
+  for (int k = 0; k < MAX_HEDGE; ++k) { hy[k] = 0.0; hp[k] = -1.0; }
+  double hpmin = -1.0;      // smallest kept hedge probability
+  int np = 0;
   double lo = w.lo, hi = w.hi, ym = w.ym, p = 1.0;
   int it = w.iters;
-  while (np < K && (hi - lo) > o.tol_b && it < o.binary_maxiter) {
-    int d = 0;
-    if (w.hasH && w.yH <= ym) d = 1;
-    else if (w.hasL && w.yL >= ym) d = -1;
-    if (d == 0) {
+  const bool hasL = w.hasL, hasH = w.hasH;
+  const double yL = w.yL, yH = w.yH;
+  const int Kp = K - n;
+  while (np < Kp && (hi - lo) > o.tol_b && it < o.binary_maxiter) {
+    if (hasH && yH <= ym) {
+      hi = ym;
+    } else if (hasL && yL >= ym) {
+      lo = ym;
+    } else {
       const double pa = est_p_above(e, ym);   // root above ym -> r(ym) <= 0 -> lo = ym
       const bool right = pa >= 0.5;
-      py[np] = ym; pp[np] = p; ++np;
-      const double palt = right ? 1.0 - pa : pa;
-      if (palt > 1e-12 && nh < CAND_CAP) {
-        hy[nh] = right ? 0.5 * (lo + ym) : 0.5 * (ym + hi);
-        hp[nh] = p * palt;
-        ++nh;
+      py[np] = ym;
+      pp[np] = p;
+      ++np;
+      const double palt = p * (right ? 1.0 - pa : pa);
+      if (palt > 1e-12 && palt > hpmin) {
+        const double alt = right ? 0.5 * (lo + ym) : 0.5 * (ym + hi);
+        bool done = false;   // replace the first slot holding the minimum
+#pragma unroll
+        for (int k = 0; k < MAX_HEDGE; ++k)
+          if (!done && hp[k] == hpmin) { hp[k] = palt; hy[k] = alt; done = true; }
+        hpmin = hp[0];
+#pragma unroll
+        for (int k = 1; k < MAX_HEDGE; ++k) hpmin = dmin_(hpmin, hp[k]);
       }
       p = p * (right ? pa : 1.0 - pa);
       if (right) lo = ym; else hi = ym;
-    } else {
-      if (d > 0) hi = ym; else lo = ym;
     }
     ym = 0.5 * (lo + hi);
     ++it;
   }
-  // merge: path nodes are a prefix ordered by decreasing probability; take
-  // hedges greedily when more probable than the next path node.
+  ctl_mark(6);
+  // merge (path nodes are ordered by decreasing probability; a hedge is
+  // taken when more probable than the next path node -- its parent, being
+  // more probable still, has then already been taken).
   int ip = 0;
-  while (n < K && (ip < np || nh > 0)) {
-    int bh = -1;
-    for (int k = 0; k < nh; ++k)
-      if (bh < 0 || hp[k] > hp[bh]) bh = k;
-    if (ip < np && (bh < 0 || pp[ip] >= hp[bh])) {
+  while (n < K) {
+    double hbest = hp[0];
+#pragma unroll
+    for (int k = 1; k < MAX_HEDGE; ++k) hbest = dmax_(hbest, hp[k]);
+    if (ip < np && pp[ip] >= hbest) {
       out[n++] = py[ip++];
+    } else if (hbest > 0.0) {
+      bool done = false;
+#pragma unroll
+      for (int k = 0; k < MAX_HEDGE; ++k)
+        if (!done && hp[k] == hbest) { out[n++] = hy[k]; hp[k] = -1.0; done = true; }
     } else {
-      // a hedge is useless if its parent path node will not be evaluated; its
-      // parent was evaluated iff it was taken (parents precede in pp order).
-      out[n++] = hy[bh];
-      hy[bh] = hy[nh - 1]; hp[bh] = hp[nh - 1]; --nh;
+      break;
     }
   }
+  ctl_mark(7);
   return n;
 }
 
-// Record one evaluation R^(y) (already offset by -ghat) with slope S.
-TOPT_HD void walk_add_point(Walk& w, double y, double R, double S) {
-  if (w.nc < MAX_K) { w.cy[w.nc] = y; w.cR[w.nc] = R; w.cS[w.nc] = S; ++w.nc; }
-  if (R <= 0.0 && (!w.hasA || y > w.ya)) { w.hasA = 1; w.ya = y; w.Ra = R; w.Sa = S; }
-  if (R > 0.0 && (!w.hasB || y < w.yb)) { w.hasB = 1; w.yb = y; w.Rb = R; w.Sb = S; }
-  if (R < -w.E && (!w.hasL || y > w.yL)) { w.hasL = 1; w.yL = y; }
-  if (R > w.E && (!w.hasH || y < w.yH)) { w.hasH = 1; w.yH = y; }
-}
-
 // Initialise a walk from the PREP totals (projection.cpp:53-97).
-TOPT_HDN inline void walk_init(Walk& w, int eq, double ghat, double E, double r0, double S0,
+TOPT_NOINLINE void walk_init(Walk& w, int eq, double ghat, double E, double r0, double S0,
                                double bp_lo, double bp_hi, double any, double count) {
   Walk z = {};
   w = z;
@@ -354,6 +446,7 @@ TOPT_HDN inline void set_error(Plan& pl, int st) {
 TOPT_HDN inline void cmd_final(Plan& pl, const double* y, int resid_rows) {
   Cmd& c = pl.cmd;
   c.phase = PH_FINAL;
+  c.local = 0;
   for (int j = 0; j < MAX_M; ++j) c.y[j] = (j < pl.P.m) ? y[j] : 0.0;
   c.resid_rows = resid_rows;
   c.nslots = resid_rows ? pl.P.m : 0;
@@ -367,6 +460,7 @@ TOPT_HDN inline void cmd_newton(Plan& pl) {
   Cmd& c = pl.cmd;
   const int m = pl.P.m;
   c.phase = PH_NEWTON;
+  c.local = 0;
   for (int j = 0; j < MAX_M; ++j) c.y[j] = (j < m) ? pl.nt.ty[j] : 0.0;
   c.want_gram = 1;
   c.nslots = m + m * (m + 1) / 2;
@@ -384,7 +478,7 @@ TOPT_HDN inline void start_newton(Plan& pl) {
 
 // Build the next sweep over all walks that need evaluations; if none do,
 // advance the stage.  Returns true if a sweep was scheduled.
-TOPT_HDN inline bool schedule_sweep(Plan& pl) {
+TOPT_NOINLINE bool schedule_sweep(Plan& pl) {
   const int m = pl.P.m;
   int need = 0;
   for (int j = 0; j < m; ++j) need += (pl.w[j].status == WK_NEED);
@@ -396,20 +490,27 @@ TOPT_HDN inline bool schedule_sweep(Plan& pl) {
   int tot = 0;
   for (int j = 0; j < m; ++j) {
     c.row_start[j] = tot;
-    Walk& w = pl.w[j];
-    w.nc = 0;
-    if (w.status == WK_NEED) tot += walk_candidates(w, pl.P.opt, per, c.cand_y + tot, pl.sc);
+    if (pl.w[j].status == WK_NEED) {
+      const Walk w = pl.w[j];
+      tot += walk_candidates(w, pl.P.opt, per, c.cand_y + tot, pl.sc);
+    }
   }
   for (int j = m; j <= MAX_M; ++j) c.row_start[j] = tot;
+  c.compact = (pl.P.compact_cap > 0 && (m == 1 || pl.P.has_part)) ? 1 : 0;
+  for (int j = 0; j < m; ++j) {
+    c.wlo[j] = pl.w[j].lo;
+    c.whi[j] = pl.w[j].hi;
+  }
   c.ncand = tot;
-  c.nslots = 2 * tot;
-  pl.res.sweeps++;
+  // compacted global sweeps append one slot: the active elements left
+  c.nslots = 2 * tot + ((c.compact && !c.local) ? 1 : 0);
+  if (c.local) pl.res.local_sweeps++; else pl.res.sweeps++;
   return true;
 }
 
-TOPT_HDN inline void after_walks(Plan& pl);
+TOPT_NOINLINE void after_walks(Plan& pl);
 
-TOPT_HDN inline void finish_newton_or_loop(Plan& pl) {
+TOPT_NOINLINE void finish_newton_or_loop(Plan& pl) {
   Newton& nt = pl.nt;
   const Problem& P = pl.P;
   const int m = P.m;
@@ -472,7 +573,7 @@ TOPT_HDN inline void finish_newton_or_loop(Plan& pl) {
   cmd_final(pl, nt.y, 0);
 }
 
-TOPT_HDN inline void consume_newton(Plan& pl, const double* t) {
+TOPT_NOINLINE void consume_newton(Plan& pl, const double* t) {
   Newton& nt = pl.nt;
   const Problem& P = pl.P;
   const int m = P.m;
@@ -520,6 +621,7 @@ TOPT_HDN inline void schedule_feas(Plan& pl) {
   const int m = pl.P.m;
   Cmd& c = pl.cmd;
   c.phase = PH_FEAS;
+  c.local = 0;
   int nf = 0, zero_idx = -1;
   for (int j = 0; j < m; ++j) {
     Walk& w = pl.w[j];
@@ -538,7 +640,7 @@ TOPT_HDN inline void schedule_feas(Plan& pl) {
   if (nf == 0) start_newton(pl);
 }
 
-TOPT_HDN inline void consume_feas(Plan& pl, const double* t) {
+TOPT_NOINLINE void consume_feas(Plan& pl, const double* t) {
   const Problem& P = pl.P;
   const int m = P.m;
   for (int j = 0; j < m; ++j) {
@@ -571,7 +673,7 @@ TOPT_HDN inline void consume_feas(Plan& pl, const double* t) {
   start_newton(pl);
 }
 
-TOPT_HDN inline void after_walks(Plan& pl) {
+TOPT_NOINLINE void after_walks(Plan& pl) {
   const Problem& P = pl.P;
   const int m = P.m;
   Result& r = pl.res;
@@ -605,7 +707,7 @@ TOPT_HDN inline void after_walks(Plan& pl) {
 }
 
 // PREP totals -> g_hat, error bounds, walks, path dispatch.
-TOPT_HDN inline void consume_prep(Plan& pl, const double* t) {
+TOPT_NOINLINE void consume_prep(Plan& pl, const double* t) {
   Problem& P = pl.P;
   const int m = P.m;
   Result& r = pl.res;
@@ -630,8 +732,11 @@ TOPT_HDN inline void consume_prep(Plan& pl, const double* t) {
     r.ghat[j] = ghat;
     r.ghat_err[j] = (gamma_k((double)P.n_global + 2.0) + gamma_k(ours)) * s[PS_DABS];
     if (pl.cmd.validate_part && s[PS_NZOUT] > 0.0) { set_error(pl, ST_DOMAIN); return; }
+    // + 4u T: compacted sweeps sum the terms of elements that stay free on
+    // the walk interval as y * sum(a^2) instead of sum fl(fl(y a) a).
     const double E = 1.0625 * (gamma_k(cnt + 2.0) * (fabs(ghat) + s[PS_T]) + gerr +
-                               gamma_k(ours) * (fabs(ghat) + s[PS_T])) + 1e-300;
+                               gamma_k(ours) * (fabs(ghat) + s[PS_T]) +
+                               4.0 * kUnit * s[PS_T]) + 1e-300;
     const double r0 = s[PS_S0] - ghat;
     walk_init(pl.w[j], P.is_eq[j], ghat, E, r0, s[PS_SLOPE0], s[PS_BPLO], s[PS_BPHI],
               s[PS_ANY], cnt);
@@ -650,24 +755,50 @@ TOPT_HDN inline void consume_prep(Plan& pl, const double* t) {
   } else {
     pl.stage = SG_STAGE1;
   }
-  for (int j = 0; j < m; ++j) walk_advance(pl.w[j], P.opt);
+  const Evals none = {nullptr, nullptr, 0};
+  for (int j = 0; j < m; ++j) walk_advance(pl.w[j], P.opt, none);
   if (!schedule_sweep(pl)) after_walks(pl);
 }
 
-TOPT_HDN inline void consume_sweep(Plan& pl, const double* t) {
+TOPT_NOINLINE void consume_sweep(Plan& pl, const double* t) {
   const int m = pl.P.m;
-  const Cmd& c = pl.cmd;
+  Cmd& c = pl.cmd;
+  ctl_mark(0);
+  const bool was_global_compact = c.compact && !c.local;
+  if (was_global_compact) pl.res.active = t[2 * c.ncand];
   for (int j = 0; j < m; ++j) {
-    Walk& w = pl.w[j];
     const int b = c.row_start[j], e = c.row_start[j + 1];
     if (e <= b) continue;
-    for (int k = b; k < e; ++k) walk_add_point(w, c.cand_y[k], t[2 * k] - w.ghat, t[2 * k + 1]);
-    walk_advance(w, pl.P.opt);
+    Walk w = pl.w[j];                      // registers for the replay
+    const Evals ev = {c.cand_y + b, t + 2 * b, e - b};
+    walk_ingest(w, ev);
+    ctl_mark(1);
+    walk_advance(w, pl.P.opt, ev);
+    ctl_mark(2);
+    pl.w[j] = w;
   }
+  // few active elements left: gather them into every CTA and finish the
+  // walks CTA-locally (no grid barrier per sweep)
+  int need = 0;
+  for (int j = 0; j < m; ++j) need += (pl.w[j].status == WK_NEED);
+  if (need && was_global_compact && pl.res.active <= (double)GATHER_CAP) {
+    c.phase = PH_GATHER;
+    c.nslots = 0;
+    ctl_mark(3);
+    return;
+  }
+  if (!schedule_sweep(pl)) after_walks(pl);
+  ctl_mark(3);
+}
+
+
+TOPT_NOINLINE void consume_gather(Plan& pl) {
+  pl.cmd.local = 1;
+  pl.res.gathered = 1;
   if (!schedule_sweep(pl)) after_walks(pl);
 }
 
-TOPT_HDN inline void consume_final(Plan& pl, const double* t) {
+TOPT_NOINLINE void consume_final(Plan& pl, const double* t) {
   Problem& P = pl.P;
   Result& r = pl.res;
   const int m = P.m;
@@ -688,7 +819,7 @@ TOPT_HDN inline void consume_final(Plan& pl, const double* t) {
   r.status = ST_OK;
 }
 
-TOPT_HDN inline void consume_step(Plan& pl, const double* t) {
+TOPT_NOINLINE void consume_step(Plan& pl, const double* t) {
   const Problem& P = pl.P;
   const PgdSettings& s = P.set;
   Result& r = pl.res;
@@ -734,6 +865,8 @@ TOPT_HDN inline void plan_start(Plan& pl) {
   Cmd& c = pl.cmd;
   c.compute_dir = 0; c.use_dprev = 0; c.compute_dot = 0; c.validate_part = 0;
   c.write_delta = c.write_x = c.write_mask = 0;
+  c.compact = 0;
+  c.local = 0;
   if (P.job == JOB_PGD_STEP || P.job == JOB_DIRECTION) {
     c.phase = PH_STEP_REDUCE;
     c.nslots = 6;
@@ -752,7 +885,7 @@ TOPT_HDN inline void plan_start(Plan& pl) {
   pl.dot_mode = (P.job == JOB_BUILD);
 }
 
-TOPT_HDN inline void plan_consume(Plan& pl, const double* t) {
+TOPT_NOINLINE void plan_consume(Plan& pl, const double* t) {
   pl.res.passes++;
   switch (pl.cmd.phase) {
     case PH_STEP_REDUCE: consume_step(pl, t); break;
@@ -761,9 +894,162 @@ TOPT_HDN inline void plan_consume(Plan& pl, const double* t) {
     case PH_FEAS: consume_feas(pl, t); break;
     case PH_NEWTON: consume_newton(pl, t); break;
     case PH_FINAL: consume_final(pl, t); break;
+    case PH_GATHER: consume_gather(pl); break;
     default: break;
   }
   if (pl.res.passes > 4096 && pl.cmd.phase != PH_DONE) set_error(pl, ST_INTERNAL);
 }
+
+#if defined(__CUDACC__)
+// Warp-parallel version of consume_sweep (all 32 lanes of one warp): lane k
+// holds candidate k; bracket updates are warp arg-reductions and each
+// replayed midpoint is matched with one ballot.  Same decisions as the
+// scalar consume_sweep (candidates are distinct duals).
+__device__ __forceinline__ void warp_arg(bool valid, double key, bool want_max, int* src) {
+  // lane index holding the max/min key among valid lanes (lowest lane on ties), -1 if none
+  const int lane = threadIdx.x & 31;
+  double k = valid ? key : (want_max ? -1.0 / 0.0 : 1.0 / 0.0);
+  int l = valid ? lane : 32;
+  for (int off = 16; off > 0; off >>= 1) {
+    const double k2 = __shfl_xor_sync(0xffffffffu, k, off);
+    const int l2 = __shfl_xor_sync(0xffffffffu, l, off);
+    const bool take = (l2 < 32) && (l == 32 || (want_max ? (k2 > k || (k2 == k && l2 < l))
+                                                         : (k2 < k || (k2 == k && l2 < l))));
+    if (take) { k = k2; l = l2; }
+  }
+  *src = l < 32 ? l : -1;
+}
+
+__device__ void consume_sweep_warp(Plan& pl, const double* t) {
+  const int lane = threadIdx.x & 31;
+  const int m = pl.P.m;
+  Cmd& c = pl.cmd;
+  const bool was_global_compact = c.compact && !c.local;
+  for (int j = 0; j < m; ++j) {
+    const int b = c.row_start[j], e = c.row_start[j + 1], nc = e - b;
+    if (nc <= 0) continue;
+    Walk w = pl.w[j];
+    const bool mine = lane < nc;
+    const double cy = mine ? c.cand_y[b + lane] : 0.0;
+    const double cR = mine ? t[2 * (b + lane)] - w.ghat : 0.0;
+    const double cS = mine ? t[2 * (b + lane) + 1] : 0.0;
+    int src;
+    warp_arg(mine && cR <= 0.0, cy, true, &src);           // nearest R <= 0 from below
+    if (src >= 0) {
+      const double y = __shfl_sync(0xffffffffu, cy, src);
+      if (!w.hasA || y > w.ya) {
+        w.hasA = 1; w.ya = y;
+        w.Ra = __shfl_sync(0xffffffffu, cR, src); w.Sa = __shfl_sync(0xffffffffu, cS, src);
+      }
+    }
+    warp_arg(mine && cR > 0.0, cy, false, &src);           // nearest R > 0 from above
+    if (src >= 0) {
+      const double y = __shfl_sync(0xffffffffu, cy, src);
+      if (!w.hasB || y < w.yb) {
+        w.hasB = 1; w.yb = y;
+        w.Rb = __shfl_sync(0xffffffffu, cR, src); w.Sb = __shfl_sync(0xffffffffu, cS, src);
+      }
+    }
+    warp_arg(mine && cR < -w.E, cy, true, &src);
+    if (src >= 0) {
+      const double y = __shfl_sync(0xffffffffu, cy, src);
+      if (!w.hasL || y > w.yL) { w.hasL = 1; w.yL = y; }
+    }
+    warp_arg(mine && cR > w.E, cy, false, &src);
+    if (src >= 0) {
+      const double y = __shfl_sync(0xffffffffu, cy, src);
+      if (!w.hasH || y < w.yH) { w.hasH = 1; w.yH = y; }
+    }
+    // replay (every lane runs the same loop; lookups are ballots)
+    if (w.status == WK_NEED) {
+      const bool hasL = w.hasL, hasH = w.hasH;
+      const double yL = w.yL, yH = w.yH, E = w.E;
+      int near = 0, direct = 0;
+      double minm = w.min_margin;
+      bool stop = false;
+      if (!w.feas_done) {
+        const double yb = w.up ? w.bp_hi : w.bp_lo;
+        const unsigned hit = __ballot_sync(0xffffffffu, mine && cy == yb);
+        int infeasible = -1;
+        if (hit) {
+          const double R = __shfl_sync(0xffffffffu, cR, __ffs(hit) - 1);
+          infeasible = w.up ? (R < 0.0) : (R > 0.0);
+          minm = dmin_(minm, fabs(R) / E);
+          near += (fabs(R) <= E);
+        } else if (hasH && yH <= yb) {
+          infeasible = w.up ? 0 : 1;
+        } else if (hasL && yL >= yb) {
+          infeasible = w.up ? 1 : 0;
+        }
+        w.near_ties += near;
+        w.min_margin = minm;
+        near = 0;
+        if (infeasible < 0) { stop = true; }
+        else if (infeasible) { w.status = WK_INFEASIBLE; stop = true; }
+        else w.feas_done = 1;
+      }
+      if (!stop) {
+        double lo = w.lo, hi = w.hi, ym = w.ym;
+        int it = w.iters;
+        const double tol_b = pl.P.opt.tol_b;
+        const int maxit = pl.P.opt.binary_maxiter;
+        int status = WK_DONE;
+        while ((hi - lo) > tol_b && it < maxit) {
+          int d;
+          if (hasH && yH <= ym) {
+            d = 1;
+          } else if (hasL && yL >= ym) {
+            d = -1;
+          } else {
+            const unsigned hit = __ballot_sync(0xffffffffu, mine && cy == ym);
+            if (!hit) { status = WK_NEED; break; }
+            const double R = __shfl_sync(0xffffffffu, cR, __ffs(hit) - 1);
+            minm = dmin_(minm, fabs(R) / E);
+            near += (fabs(R) <= E);
+            ++direct;
+            d = R > 0.0 ? 1 : -1;
+          }
+          if (d > 0) hi = ym; else lo = ym;
+          ym = 0.5 * (lo + hi);
+          ++it;
+        }
+        w.lo = lo; w.hi = hi; w.ym = ym; w.iters = it;
+        w.near_ties += near;
+        w.n_direct += direct;
+        w.min_margin = minm;
+        w.status = status;
+        if (status == WK_DONE) w.y = ym;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) pl.w[j] = w;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (was_global_compact) pl.res.active = t[2 * c.ncand];
+    pl.res.passes++;
+    int need = 0;
+    for (int j = 0; j < m; ++j) need += (pl.w[j].status == WK_NEED);
+    if (need && was_global_compact && pl.res.active <= (double)GATHER_CAP) {
+      c.phase = PH_GATHER;
+      c.nslots = 0;
+    } else if (!schedule_sweep(pl)) {
+      after_walks(pl);
+    }
+    if (pl.res.passes > 4096 && pl.cmd.phase != PH_DONE) set_error(pl, ST_INTERNAL);
+  }
+  __syncwarp();
+}
+
+// Called by all lanes of one warp.
+__device__ void plan_consume_warp(Plan& pl, const double* t) {
+  if (pl.cmd.phase == PH_SWEEP) {
+    consume_sweep_warp(pl, t);
+  } else {
+    if ((threadIdx.x & 31) == 0) plan_consume(pl, t);
+    __syncwarp();
+  }
+}
+#endif
 
 }  // namespace topt_b200

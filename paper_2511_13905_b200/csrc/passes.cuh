@@ -21,7 +21,7 @@
 
 namespace topt_b200 {
 
-constexpr int BLOCK = 256;
+constexpr int BLOCK = 512;
 constexpr int NWARP = BLOCK / 32;
 
 __device__ __forceinline__ double clipd(double v, double lo, double hi) {
@@ -67,141 +67,473 @@ struct PassCtx {
   const Plan* plan;
   const Cmd* cmd;      // shared-memory copy
   double* out;         // this CTA's partial slots
-  double* smem;        // reduction scratch (NWARP * 64 doubles)
+  double* smem;        // reduction scratch (NWARP * 160 doubles)
   int64_t i0, stride;  // grid-stride
+  // persistent-kernel only (null otherwise): per-warp active element lists
+  // and per-CTA fixed sums of the compacted bisection sweeps.
+  uint32_t* list;      // [NWARP][list_cap]
+  int* list_cnt;       // [NWARP]
+  double* fixC;        // [MAX_M]
+  double* fixS;        // [MAX_M]
+  int list_cap;
+  // gather / local sweeps (persistent kernel only)
+  int* blk_cnt;        // global [nb]: active items per CTA after a compacted sweep
+  double* g_a;         // global [GATHER_CAP]
+  double* g_r;
+  int* g_row;
+  double* g_fix;       // global [nb][MAX_M][2]
+  double* it_a;        // shared [GATHER_CAP] gathered items
+  double* it_r;
+  int8_t* it_row;
+  int* n_items;        // shared scalar
 };
 
+// Fill each warp's active list with all of its grid-stride elements (this
+// CTA owns i = blockIdx*BLOCK + tid + k*stride) and clear the fixed sums.
+__device__ void compact_init(const PassCtx& c) {
+  if (!c.list) return;
+  const int64_t n = c.plan->P.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* L = c.list + (size_t)warp * c.list_cap;
+  const int64_t base = c.i0 - lane;   // warp's first element
+  int cnt = 0;
+  const int8_t* __restrict__ owner = c.plan->P.owner;
+  for (int64_t b = base; b < n; b += c.stride) {   // 32 consecutive elements per step
+    const int64_t i = b + lane;
+    const bool take = i < n && (owner == nullptr || owner[i] >= 0);
+    const unsigned ok = __ballot_sync(0xffffffffu, take);
+    if (take) L[cnt + __popc(ok & ((1u << lane) - 1u))] = (uint32_t)i;
+    cnt += __popc(ok);
+  }
+  if (lane == 0) c.list_cnt[warp] = cnt;
+  if (threadIdx.x < MAX_M) { c.fixC[threadIdx.x] = 0.0; c.fixS[threadIdx.x] = 0.0; }
+  __syncthreads();
+}
+
 // ---- PH_STEP_REDUCE: BB / PR+ sums --------------------
-__device__ void pass_step_reduce(const PassCtx& c) {
+__device__ __noinline__ void pass_step_reduce(const PassCtx& c) {
   const Problem& P = c.plan->P;
+  const int64_t n = P.n, st = c.stride;
+  const double* __restrict__ x = P.x;
+  const double* __restrict__ xp = P.x_prev;
+  const double* __restrict__ g = P.g;
+  const double* __restrict__ gp = P.g_prev;
   double v[6] = {0, 0, 0, 0, 0, 0};
-  for (int64_t i = c.i0; i < P.n; i += c.stride) {
-    const double x = P.x[i], xp = P.x_prev[i], g = P.g[i], gp = P.g_prev[i];
-    const double s = x - xp, y = g - gp;
-    v[0] += s * s;
-    v[1] += s * y;
-    v[2] += y * y;
-    v[3] += g * y;
-    v[4] += gp * gp;
-    v[5] = dmax_(v[5], fabs(g));
+  int64_t i = c.i0;
+  for (; i + st < n; i += 2 * st) {   // two independent elements in flight
+    const double x0 = x[i], q0 = xp[i], g0 = g[i], h0 = gp[i];
+    const double x1 = x[i + st], q1 = xp[i + st], g1 = g[i + st], h1 = gp[i + st];
+    const double s0 = x0 - q0, y0 = g0 - h0, s1 = x1 - q1, y1 = g1 - h1;
+    v[0] += s0 * s0; v[1] += s0 * y0; v[2] += y0 * y0; v[3] += g0 * y0; v[4] += h0 * h0;
+    v[5] = dmax_(v[5], fabs(g0));
+    v[0] += s1 * s1; v[1] += s1 * y1; v[2] += y1 * y1; v[3] += g1 * y1; v[4] += h1 * h1;
+    v[5] = dmax_(v[5], fabs(g1));
+  }
+  if (i < n) {
+    const double s = x[i] - xp[i], y = g[i] - gp[i];
+    v[0] += s * s; v[1] += s * y; v[2] += y * y; v[3] += g[i] * y; v[4] += gp[i] * gp[i];
+    v[5] = dmax_(v[5], fabs(g[i]));
   }
   block_reduce_store<6>(v, 6, PH_STEP_REDUCE, 0, c.out, c.smem);
 }
 
 // ---- PH_PREP: direction, rho_tilde, g_hat dots, r(0), slope(0), bounds,
 //      breakpoints (projection.cpp:53-73, :139-145, :150-181) ---------------
-__device__ void pass_prep(const PassCtx& c) {
-  const Plan& pl = *c.plan;
-  const Problem& P = pl.P;
-  const Cmd& cmd = *c.cmd;
-  if (cmd.compute_dir) {  // d = g + beta d_prev ; gd = (omega alpha) d ; rho = x - gd
-    for (int64_t i = c.i0; i < P.n; i += c.stride) {
-      const double g = P.g[i];
-      const double d = cmd.use_dprev ? g + cmd.beta * P.d_prev[i] : g;
-      const double gd = cmd.wa * d;
-      P.d_out[i] = d;
-      P.rho[i] = P.x[i] - gd;
-    }
+struct PrepAcc {
+  double v[PREP_SLOTS];
+};
+
+__device__ __forceinline__ void prep_elem(PrepAcc& A, double a, double r, double gd, bool dot,
+                                          double L, double U) {
+  const double lo = L - r, hi = U - r;
+  if (dot) {
+    const double p = gd * a;
+    A.v[PS_DOT] += p;
+    A.v[PS_DABS] += fabs(p);
   }
-  const double L = P.lower, U = P.upper;
-  for (int j = 0; j < P.m; ++j) {
-    double v[PREP_SLOTS];
-#pragma unroll
-    for (int s = 0; s < PREP_SLOTS; ++s) v[s] = 0.0;
-    v[PS_BPLO] = 0.0;  // projection.cpp:58 bp_lo = bp_hi = 0
-    v[PS_BPHI] = 0.0;
-    const double* a_row = P.grad + (int64_t)j * P.ld;
-    for (int64_t i = c.i0; i < P.n; i += c.stride) {
-      const double a = a_row[i];
-      if (P.owner && P.owner[i] != j) {
-        v[PS_NZOUT] += (a != 0.0) ? 1.0 : 0.0;
-        continue;
-      }
-      const double r = P.rho[i];
-      const double lo = L - r, hi = U - r;
-      if (cmd.compute_dot) {
-        const double gd = cmd.compute_dir ? cmd.wa * P.d_out[i] : P.gd_step[i];
-        const double p = gd * a;
-        v[PS_DOT] += p;
-        v[PS_DABS] += fabs(p);
-      }
-      v[PS_S0] += a * clipd(0.0, lo, hi);
-      if (!(0.0 < lo || 0.0 > hi)) v[PS_SLOPE0] += a * a;
-      v[PS_T] += fabs(a) * dmax_(fabs(lo), fabs(hi));
-      if (fabs(a) >= kGradFloor) {
-        v[PS_ANY] += 1.0;
-        const double c1 = lo / a, c2 = hi / a;
-        v[PS_BPLO] = dmin_(v[PS_BPLO], dmin_(c1, c2));
-        v[PS_BPHI] = dmax_(v[PS_BPHI], dmax_(c1, c2));
-      }
-    }
-    block_reduce_store<PREP_SLOTS>(v, PREP_SLOTS, PH_PREP, j * PREP_SLOTS, c.out, c.smem);
+  A.v[PS_S0] += a * (0.0 < lo ? lo : (0.0 > hi ? hi : 0.0));
+  if (!(0.0 < lo || 0.0 > hi)) A.v[PS_SLOPE0] += a * a;
+  A.v[PS_T] += fabs(a) * dmax_(fabs(lo), fabs(hi));
+  if (fabs(a) >= kGradFloor) {
+    A.v[PS_ANY] += 1.0;
+    const double c1 = lo / a, c2 = hi / a;
+    A.v[PS_BPLO] = dmin_(A.v[PS_BPLO], dmin_(c1, c2));
+    A.v[PS_BPHI] = dmax_(A.v[PS_BPHI], dmax_(c1, c2));
   }
 }
 
-// ---- PH_SWEEP: r_j(y_k) and slope at up to MAX_K candidates per row -------
-__device__ void pass_sweep(const PassCtx& c) {
+__device__ __noinline__ void pass_prep(const PassCtx& c) {
   const Plan& pl = *c.plan;
   const Problem& P = pl.P;
   const Cmd& cmd = *c.cmd;
-  const double L = P.lower, U = P.upper;
-  for (int j = 0; j < P.m; ++j) {
-    const int b = cmd.row_start[j], cnt = cmd.row_start[j + 1] - b;
-    if (cnt <= 0) continue;
-    double y[MAX_K], R[MAX_K], S[MAX_K];
+  const int64_t n = P.n, st = c.stride, ld = P.ld;
+  const int m = P.m;
+  double* __restrict__ rho = P.rho;
+  double* __restrict__ dout = P.d_out;
+  const double* __restrict__ x = P.x;
+  const double* __restrict__ g = P.g;
+  const double* __restrict__ dp = P.d_prev;
+  const double* __restrict__ gd_in = P.gd_step;
+  const int8_t* __restrict__ owner = P.owner;
+  const bool dir = cmd.compute_dir, dot = cmd.compute_dot, use_dp = cmd.use_dprev;
+  const double beta = cmd.beta, wa = cmd.wa;
+  constexpr int U = 4;   // elements in flight per thread
+  if (dir) {  // d = g + beta d_prev ; gd = (omega alpha) d ; rho = x - gd
+    for (int64_t i0 = c.i0; i0 < n; i0 += U * st) {
+      double gv[U], dv[U], xv[U];
 #pragma unroll
-    for (int k = 0; k < MAX_K; ++k) {
-      y[k] = (k < cnt) ? cmd.cand_y[b + k] : 0.0;
-      R[k] = 0.0;
-      S[k] = 0.0;
-    }
-    const double* a_row = P.grad + (int64_t)j * P.ld;
-    for (int64_t i = c.i0; i < P.n; i += c.stride) {
-      if (P.owner && P.owner[i] != j) continue;
-      const double a = a_row[i];
-      const double r = P.rho[i];
-      const double lo = L - r, hi = U - r;
-      const double aa = a * a;
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * st;
+        const bool ok = i < n;
+        gv[u] = ok ? g[i] : 0.0;
+        dv[u] = (ok && use_dp) ? dp[i] : 0.0;
+        xv[u] = ok ? x[i] : 0.0;
+      }
 #pragma unroll
-      for (int k = 0; k < MAX_K; ++k) {
-        if (k < cnt) {
-          const double v = y[k] * a;
-          const bool below = v < lo, above = v > hi;
-          const double cv = below ? lo : (above ? hi : v);
-          R[k] += a * cv;
-          S[k] += (below || above) ? 0.0 : aa;
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * st;
+        if (i < n) {
+          const double d = use_dp ? gv[u] + beta * dv[u] : gv[u];
+          dout[i] = d;
+          rho[i] = xv[u] - wa * d;
         }
       }
     }
-    double v[2 * MAX_K];
+  }
+  const double L = P.lower, U_ = P.upper;
+  for (int j = 0; j < m; ++j) {
+    PrepAcc A;
 #pragma unroll
-    for (int k = 0; k < MAX_K; ++k) { v[2 * k] = R[k]; v[2 * k + 1] = S[k]; }
-    block_reduce_store<2 * MAX_K>(v, 2 * cnt, PH_SWEEP, 2 * b, c.out, c.smem);
+    for (int s = 0; s < PREP_SLOTS; ++s) A.v[s] = 0.0;   // bp_lo = bp_hi = 0 (:58)
+    const double* __restrict__ ar = P.grad + (int64_t)j * ld;
+    for (int64_t i0 = c.i0; i0 < n; i0 += U * st) {
+      double av[U], rv[U], gdv[U];
+      int ov[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * st;
+        const bool ok = i < n;
+        av[u] = ok ? ar[i] : 0.0;
+        rv[u] = ok ? rho[i] : 0.0;
+        gdv[u] = (ok && dot) ? (dir ? wa * dout[i] : gd_in[i]) : 0.0;
+        ov[u] = (ok && owner) ? (int)owner[i] : j;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i0 + u * st >= n) continue;
+        if (ov[u] != j) {
+          A.v[PS_NZOUT] += (av[u] != 0.0) ? 1.0 : 0.0;
+          continue;
+        }
+        prep_elem(A, av[u], rv[u], gdv[u], dot, L, U_);
+      }
+    }
+    block_reduce_store<PREP_SLOTS>(A.v, PREP_SLOTS, PH_PREP, j * PREP_SLOTS, c.out, c.smem);
+  }
+  compact_init(c);
+}
+
+// ---- PH_SWEEP: r_j(y_k) and slope at up to MAX_K candidates per row -------
+template <int KC>
+__device__ __forceinline__ void sweep_elem(double a, double r, const double* y, int cnt,
+                                           double L, double U, double* R, double* S) {
+  const double lo = L - r, hi = U - r;
+  const double aa = a * a;
+#pragma unroll
+  for (int k = 0; k < KC; ++k) {
+    if (k < cnt) {
+      const double v = y[k] * a;
+      const bool below = v < lo, above = v > hi;
+      R[k] += a * (below ? lo : (above ? hi : v));
+      S[k] += (below || above) ? 0.0 : aa;
+    }
+  }
+}
+
+template <int KC>
+__device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int cnt) {
+  const Problem& P = c.plan->P;
+  const int64_t n = P.n, st = c.stride;
+  const double* __restrict__ rho = P.rho;
+  const double* __restrict__ ar = P.grad + (int64_t)j * P.ld;
+  const int8_t* __restrict__ owner = P.owner;
+  const double L = P.lower, U = P.upper;
+  const double* y = c.cmd->cand_y + b;   // shared memory (broadcast)
+  double R[KC], S[KC];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) { R[k] = 0.0; S[k] = 0.0; }
+  int64_t i = c.i0;
+  for (; i + st < n; i += 2 * st) {
+    double a0 = ar[i], a1 = ar[i + st];
+    const double r0 = rho[i], r1 = rho[i + st];
+    if (owner) {   // a masked to 0 outside the row's block: adds exact zeros
+      if (owner[i] != j) a0 = 0.0;
+      if (owner[i + st] != j) a1 = 0.0;
+    }
+    sweep_elem<KC>(a0, r0, y, cnt, L, U, R, S);
+    sweep_elem<KC>(a1, r1, y, cnt, L, U, R, S);
+  }
+  if (i < n) {
+    double a0 = ar[i];
+    if (owner && owner[i] != j) a0 = 0.0;
+    sweep_elem<KC>(a0, rho[i], y, cnt, L, U, R, S);
+  }
+  double v[2 * KC];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) { v[2 * k] = R[k]; v[2 * k + 1] = S[k]; }
+  block_reduce_store<2 * KC>(v, 2 * cnt, PH_SWEEP, 2 * b, c.out, c.smem);
+}
+
+// Compacted sweep of row j over the warps' active lists.  An element whose
+// clip region (the reference's own predicate on fl(y a)) is the same at both
+// ends of the walk interval keeps that region for every candidate in it
+// (fl(y a) is monotone in y): its term is folded into the CTA's fixed sums --
+// exactly a*lo or a*hi when clipped, y * a^2 when free -- and it leaves the
+// list for good (the walk interval only shrinks).
+template <int KC>
+__device__ __noinline__ void pass_sweep_row_compact(const PassCtx& c, int j, int b, int cnt) {
+  const Problem& P = c.plan->P;
+  const Cmd& cmd = *c.cmd;
+  const double* __restrict__ rho = P.rho;
+  const double* __restrict__ ar = P.grad + (int64_t)j * P.ld;
+  const int8_t* __restrict__ owner = P.owner;
+  const double L = P.lower, U = P.upper;
+  const double wlo = cmd.wlo[j], whi = cmd.whi[j];
+  const double* y = cmd.cand_y + b;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* Lst = c.list + (size_t)warp * c.list_cap;
+  const int n_items = c.list_cnt[warp];
+  double R[KC], S[KC];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) { R[k] = 0.0; S[k] = 0.0; }
+  double nC = 0.0, nS = 0.0;
+  int kept = 0;
+  for (int base = 0; base < n_items; base += 32) {
+    const int idx = base + lane;
+    const bool valid = idx < n_items;
+    const uint32_t i = valid ? Lst[idx] : 0u;
+    bool relevant = valid;
+    if (owner && valid) relevant = owner[i] == j;
+    bool fixed = false;
+    if (relevant) {
+      const double a = ar[i];
+      const double r = rho[i];
+      const double lo = L - r, hi = U - r;
+      const double v1 = wlo * a, v2 = whi * a;
+      const int g1 = v1 < lo ? 0 : (v1 > hi ? 2 : 1);
+      const int g2 = v2 < lo ? 0 : (v2 > hi ? 2 : 1);
+      if (g1 == g2) {
+        fixed = true;
+        if (g1 == 0) nC += a * lo;
+        else if (g1 == 2) nC += a * hi;
+        else nS += a * a;
+      } else {
+        sweep_elem<KC>(a, r, y, cnt, L, U, R, S);
+      }
+    }
+    // rows other than j keep their items (partitioned problems)
+    const bool keep = valid && !(relevant && fixed);
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) Lst[kept + __popc(km & ((1u << lane) - 1u))] = i;
+    kept += __popc(km);
+  }
+  __syncwarp();
+  if (lane == 0) c.list_cnt[warp] = kept;
+  // CTA totals of this sweep's active sums and newly fixed sums
+  double v[2 * KC + 2];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) { v[2 * k] = R[k]; v[2 * k + 1] = S[k]; }
+  v[2 * KC] = nC;
+  v[2 * KC + 1] = nS;
+  double* sred = c.smem;
+#pragma unroll
+  for (int s = 0; s < 2 * KC + 2; ++s) {
+    const double r = warp_reduce(0, v[s]);
+    if (lane == 0) sred[warp * (2 * KC + 2) + s] = r;
+  }
+  __syncthreads();
+  double* tot = c.smem + NWARP * (2 * KC + 2);
+  if (threadIdx.x < 2 * KC + 2) {
+    double r = sred[threadIdx.x];
+    for (int w = 1; w < NWARP; ++w) r += sred[w * (2 * KC + 2) + threadIdx.x];
+    tot[threadIdx.x] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    c.fixC[j] += tot[2 * KC];
+    c.fixS[j] += tot[2 * KC + 1];
+  }
+  __syncthreads();
+  if (threadIdx.x < cnt) {
+    const int k = threadIdx.x;
+    c.out[2 * (b + k)] = tot[2 * k] + (c.fixC[j] + y[k] * c.fixS[j]);
+    c.out[2 * (b + k) + 1] = tot[2 * k + 1] + c.fixS[j];
+  }
+  __syncthreads();
+}
+
+__device__ void pass_sweep(const PassCtx& c) {
+  const Cmd& cmd = *c.cmd;
+  const int m = c.plan->P.m;
+  for (int j = 0; j < m; ++j) {
+    const int b = cmd.row_start[j], cnt = cmd.row_start[j + 1] - b;
+    if (cnt <= 0) continue;
+    if (cmd.compact && c.list) {
+      if (cnt <= 4) pass_sweep_row_compact<4>(c, j, b, cnt);
+      else if (cnt <= 8) pass_sweep_row_compact<8>(c, j, b, cnt);
+      else pass_sweep_row_compact<MAX_K>(c, j, b, cnt);
+      continue;
+    }
+    if (cnt <= 4) pass_sweep_row<4>(c, j, b, cnt);
+    else if (cnt <= 8) pass_sweep_row<8>(c, j, b, cnt);
+    else pass_sweep_row<MAX_K>(c, j, b, cnt);
+  }
+  if (cmd.compact && c.list) {   // active elements left in this CTA
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w = 0; w < NWARP; ++w) tot += c.list_cnt[w];
+      c.out[2 * cmd.ncand] = (double)tot;
+      c.blk_cnt[blockIdx.x] = tot;
+    }
+    __syncthreads();
+  }
+}
+
+// ---- PH_GATHER: write this CTA's active items and fixed sums ---------------
+__device__ __noinline__ void pass_gather(const PassCtx& c) {
+  const Problem& P = c.plan->P;
+  const int m = P.m;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int s_off[NWARP + 1];
+  if (threadIdx.x == 0) {
+    int off = 0;
+    for (int b = 0; b < (int)blockIdx.x; ++b) off += __ldcg(c.blk_cnt + b);
+    s_off[0] = off;
+    for (int w = 0; w < NWARP; ++w) s_off[w + 1] = s_off[w] + c.list_cnt[w];
+  }
+  __syncthreads();
+  const uint32_t* Lst = c.list + (size_t)warp * c.list_cap;
+  const int cnt = c.list_cnt[warp], base = s_off[warp];
+  for (int k = lane; k < cnt; k += 32) {
+    const uint32_t i = Lst[k];
+    const int row = P.owner ? (int)P.owner[i] : 0;
+    const int dst = base + k;
+    if (dst < GATHER_CAP) {
+      c.g_a[dst] = P.grad[(int64_t)row * P.ld + i];
+      c.g_r[dst] = P.rho[i];
+      c.g_row[dst] = row;
+    }
+  }
+  if (threadIdx.x < m) {
+    c.g_fix[((size_t)blockIdx.x * MAX_M + threadIdx.x) * 2] = c.fixC[threadIdx.x];
+    c.g_fix[((size_t)blockIdx.x * MAX_M + threadIdx.x) * 2 + 1] = c.fixS[threadIdx.x];
+  }
+  __syncthreads();
+}
+
+// After the gather barrier: every CTA loads all items and the fixed totals
+// (summed over CTAs in index order) into its shared memory.
+__device__ __noinline__ void gather_load(const PassCtx& c, int nb) {
+  const int m = c.plan->P.m;
+  __shared__ int s_total;
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int b = 0; b < nb; ++b) t += __ldcg(c.blk_cnt + b);
+    s_total = t < GATHER_CAP ? t : GATHER_CAP;
+    *c.n_items = s_total;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < s_total; k += BLOCK) {
+    c.it_a[k] = __ldcg(c.g_a + k);
+    c.it_r[k] = __ldcg(c.g_r + k);
+    c.it_row[k] = (int8_t)__ldcg(c.g_row + k);
+  }
+  if (threadIdx.x < m) {
+    double C = 0.0, S = 0.0;
+    for (int b = 0; b < nb; ++b) {
+      C += __ldcg(c.g_fix + ((size_t)b * MAX_M + threadIdx.x) * 2);
+      S += __ldcg(c.g_fix + ((size_t)b * MAX_M + threadIdx.x) * 2 + 1);
+    }
+    c.fixC[threadIdx.x] = C;
+    c.fixS[threadIdx.x] = S;
+  }
+  __syncthreads();
+}
+
+// CTA-local sweep over the gathered items: totals go straight to tot[]
+// (no partials, no grid barrier; every CTA computes the same bits).
+template <int KC>
+__device__ __noinline__ void local_sweep_row(const PassCtx& c, int j, int b, int cnt,
+                                             double* tot) {
+  const Problem& P = c.plan->P;
+  const double L = P.lower, U = P.upper;
+  const double* y = c.cmd->cand_y + b;
+  const int nit = *c.n_items;
+  double R[KC], S[KC];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) { R[k] = 0.0; S[k] = 0.0; }
+  for (int k = threadIdx.x; k < nit; k += BLOCK)
+    if (c.it_row[k] == j) sweep_elem<KC>(c.it_a[k], c.it_r[k], y, cnt, L, U, R, S);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* sred = c.smem;
+#pragma unroll
+  for (int s = 0; s < KC; ++s) {
+    if (s < cnt) {
+      const double r0 = warp_reduce(0, R[s]);
+      const double r1 = warp_reduce(0, S[s]);
+      if (lane == 0) { sred[warp * 2 * KC + 2 * s] = r0; sred[warp * 2 * KC + 2 * s + 1] = r1; }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * cnt) {
+    double r = sred[threadIdx.x];
+    for (int w = 1; w < NWARP; ++w) r += sred[w * 2 * KC + threadIdx.x];
+    const int k = threadIdx.x >> 1;
+    tot[2 * b + threadIdx.x] = (threadIdx.x & 1) ? r + c.fixS[j]
+                                                  : r + (c.fixC[j] + y[k] * c.fixS[j]);
+  }
+  __syncthreads();
+}
+
+__device__ void local_sweep(const PassCtx& c, double* tot) {
+  const Cmd& cmd = *c.cmd;
+  const int m = c.plan->P.m;
+  for (int j = 0; j < m; ++j) {
+    const int b = cmd.row_start[j], cnt = cmd.row_start[j + 1] - b;
+    if (cnt <= 0) continue;
+    if (cnt <= 4) local_sweep_row<4>(c, j, b, cnt, tot);
+    else if (cnt <= 8) local_sweep_row<8>(c, j, b, cnt, tot);
+    else local_sweep_row<MAX_K>(c, j, b, cnt, tot);
   }
 }
 
 // ---- PH_FEAS: stage-1 dots a_k . clip(y_j a_j) (projection.cpp:320-333) ---
-__device__ void pass_feas(const PassCtx& c) {
+__device__ __noinline__ void pass_feas(const PassCtx& c) {
   const Plan& pl = *c.plan;
   const Problem& P = pl.P;
   const Cmd& cmd = *c.cmd;
   const double L = P.lower, U = P.upper;
   const int m = P.m;
+  const int64_t n = P.n, st = c.stride, ld = P.ld;
+  const double* __restrict__ rho = P.rho;
+  const double* __restrict__ grad = P.grad;
   for (int f = 0; f < cmd.nfeas; ++f) {
     const int rj = cmd.feas_row[f];
     const double yj = cmd.feas_y[f];
     double acc[MAX_M];
 #pragma unroll
     for (int k = 0; k < MAX_M; ++k) acc[k] = 0.0;
-    for (int64_t i = c.i0; i < P.n; i += c.stride) {
-      const double r = P.rho[i];
+    for (int64_t i = c.i0; i < n; i += st) {
+      const double r = rho[i];
       const double lo = L - r, hi = U - r;
       double z = 0.0;
-      if (rj >= 0 && yj != 0.0) z = 0.0 + yj * P.grad[(int64_t)rj * P.ld + i];
+      if (rj >= 0 && yj != 0.0) z = 0.0 + yj * grad[(int64_t)rj * ld + i];
       const double dl = clipd(z, lo, hi);
 #pragma unroll
       for (int k = 0; k < MAX_M; ++k)
-        if (k < m) acc[k] += P.grad[(int64_t)k * P.ld + i] * dl;
+        if (k < m) acc[k] += grad[(int64_t)k * ld + i] * dl;
     }
     block_reduce_store<MAX_M>(acc, m, PH_FEAS, f * m, c.out, c.smem);
   }
@@ -216,17 +548,21 @@ __device__ __noinline__ void pass_newton_m(const PassCtx& c) {
   const Cmd& cmd = *c.cmd;
   const double L = P.lower, U = P.upper;
   const int m = P.m;
+  const int64_t n = P.n, st = c.stride, ld = P.ld;
+  const double* __restrict__ rho = P.rho;
+  const double* __restrict__ grad = P.grad;
+  const bool want_gram = cmd.want_gram;
   constexpr int NG = M * (M + 1) / 2;
   double h[M], G[NG], y[M];
 #pragma unroll
   for (int k = 0; k < M; ++k) { h[k] = 0.0; y[k] = (k < m) ? cmd.y[k] : 0.0; }
 #pragma unroll
   for (int k = 0; k < NG; ++k) G[k] = 0.0;
-  for (int64_t i = c.i0; i < P.n; i += c.stride) {
+  for (int64_t i = c.i0; i < n; i += st) {
     double a[M];
 #pragma unroll
-    for (int k = 0; k < M; ++k) a[k] = (k < m) ? P.grad[(int64_t)k * P.ld + i] : 0.0;
-    const double r = P.rho[i];
+    for (int k = 0; k < M; ++k) a[k] = (k < m) ? grad[(int64_t)k * ld + i] : 0.0;
+    const double r = rho[i];
     const double lo = L - r, hi = U - r;
     double z = 0.0;
 #pragma unroll
@@ -236,7 +572,7 @@ __device__ __noinline__ void pass_newton_m(const PassCtx& c) {
     const double dl = clipd(z, lo, hi);
 #pragma unroll
     for (int k = 0; k < M; ++k) h[k] += a[k] * dl;
-    if (cmd.want_gram && !clipped) {
+    if (want_gram && !clipped) {
       int q = 0;
 #pragma unroll
       for (int j = 0; j < M; ++j)
@@ -248,7 +584,6 @@ __device__ __noinline__ void pass_newton_m(const PassCtx& c) {
   double v[M + NG];
 #pragma unroll
   for (int k = 0; k < M; ++k) v[k] = h[k];
-  // re-pack from the M-wide triangle to the m-wide triangle
   {
     int q = 0;
 #pragma unroll
@@ -263,43 +598,79 @@ __device__ __noinline__ void pass_newton_m(const PassCtx& c) {
 }
 
 // ---- PH_FINAL: delta / x_{t+1} / mask writes and residual dots ------------
-__device__ void pass_final(const PassCtx& c) {
+// M: compile-time row bound (>= m); OWN: partition owner map present.
+template <int M, bool OWN>
+__device__ __noinline__ void pass_final_m(const PassCtx& c) {
   const Plan& pl = *c.plan;
   const Problem& P = pl.P;
   const Cmd& cmd = *c.cmd;
-  const double L = P.lower, U = P.upper;
+  const double L = P.lower, Up = P.upper;
   const int m = P.m;
-  double acc[MAX_M];
+  const int64_t n = P.n, st = c.stride, ld = P.ld;
+  const double* __restrict__ rho = P.rho;
+  const double* __restrict__ grad = P.grad;
+  const int8_t* __restrict__ owner = P.owner;
+  double* __restrict__ dout = cmd.write_delta ? P.delta_out : nullptr;
+  double* __restrict__ xout = cmd.write_x ? P.x_out : nullptr;
+  uint8_t* __restrict__ mout = cmd.write_mask ? P.mask_out : nullptr;
+  const bool resid = cmd.resid_rows;
+  double yv[M], acc[M];
 #pragma unroll
-  for (int k = 0; k < MAX_M; ++k) acc[k] = 0.0;
-  for (int64_t i = c.i0; i < P.n; i += c.stride) {
-    const double r = P.rho[i];
-    const double lo = L - r, hi = U - r;
+  for (int k = 0; k < M; ++k) { yv[k] = (k < m) ? cmd.y[k] : 0.0; acc[k] = 0.0; }
+  for (int64_t i = c.i0; i < n; i += st) {
+    const double r = rho[i];
     double z = 0.0;
     int o = -1;
-    if (P.owner) {
-      o = P.owner[i];
-      if (o >= 0 && cmd.y[o] != 0.0) z = 0.0 + cmd.y[o] * P.grad[(int64_t)o * P.ld + i];
+    if (OWN) {
+      o = owner[i];
+      double yo = 0.0;
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+        if (k == o) yo = yv[k];
+      if (o >= 0 && yo != 0.0) z = 0.0 + yo * grad[(int64_t)o * ld + i];
     } else {
-      for (int j = 0; j < m; ++j) {
-        const double yj = cmd.y[j];
-        if (yj != 0.0) z += yj * P.grad[(int64_t)j * P.ld + i];
-      }
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+        if (k < m && yv[k] != 0.0) z += yv[k] * grad[(int64_t)k * ld + i];
     }
+    const double lo = L - r, hi = Up - r;
     const bool below = z < lo, above = z > hi;
     const double dl = below ? lo : (above ? hi : z);
-    if (cmd.write_delta) P.delta_out[i] = dl;
-    if (cmd.write_x) P.x_out[i] = r + dl;
-    if (cmd.write_mask) P.mask_out[i] = below ? 1 : (above ? 2 : 0);
-    if (cmd.resid_rows) {
+    if (dout) dout[i] = dl;
+    if (xout) xout[i] = r + dl;
+    if (mout) mout[i] = below ? 1 : (above ? 2 : 0);
+    if (resid) {
+      if (OWN) {
+        if (o >= 0) {
+          const double t = grad[(int64_t)o * ld + i] * dl;
 #pragma unroll
-      for (int k = 0; k < MAX_M; ++k) {
-        if (k < m && (o < 0 ? P.owner == nullptr : k == o))
-          acc[k] += P.grad[(int64_t)k * P.ld + i] * dl;
+          for (int k = 0; k < M; ++k)
+            if (k == o) acc[k] += t;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          if (k < m) acc[k] += grad[(int64_t)k * ld + i] * dl;
       }
     }
   }
-  if (cmd.resid_rows) block_reduce_store<MAX_M>(acc, m, PH_FINAL, 0, c.out, c.smem);
+  if (resid) block_reduce_store<M>(acc, m, PH_FINAL, 0, c.out, c.smem);
+}
+
+__device__ void pass_final(const PassCtx& c) {
+  const int m = c.plan->P.m;
+  const bool own = c.plan->P.owner != nullptr;
+  if (own) {
+    if (m <= 4) pass_final_m<4, true>(c);
+    else if (m <= 8) pass_final_m<8, true>(c);
+    else pass_final_m<16, true>(c);
+  } else {
+    if (m <= 1) pass_final_m<1, false>(c);
+    else if (m <= 2) pass_final_m<2, false>(c);
+    else if (m <= 4) pass_final_m<4, false>(c);
+    else if (m <= 8) pass_final_m<8, false>(c);
+    else pass_final_m<16, false>(c);
+  }
 }
 
 __device__ void pass_newton(const PassCtx& c) {
@@ -319,6 +690,7 @@ __device__ void run_pass(const PassCtx& c) {
     case PH_FEAS: pass_feas(c); break;
     case PH_NEWTON: pass_newton(c); break;
     case PH_FINAL: pass_final(c); break;
+    case PH_GATHER: pass_gather(c); break;
     default: break;
   }
 }

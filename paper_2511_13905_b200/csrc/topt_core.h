@@ -20,9 +20,11 @@
 #ifdef __CUDACC__
 #define TOPT_HD __host__ __device__ __forceinline__
 #define TOPT_HDN __host__ __device__
+#define TOPT_NOINLINE __host__ __device__ __noinline__
 #else
 #define TOPT_HD inline
 #define TOPT_HDN
+#define TOPT_NOINLINE inline
 #endif
 
 namespace topt_b200 {
@@ -40,8 +42,10 @@ enum Phase : int32_t {
   PH_FEAS = 3,         // K4: stage-1 feasibility dots
   PH_NEWTON = 4,       // K5: delta(y), h-dots and A D A^T at one trial dual
   PH_FINAL = 5,        // K7: delta / x_new writes + residual dots
-  PH_DONE = 6
+  PH_DONE = 6,
+  PH_GATHER = 7        // copy the (small) active sets to every CTA; later sweeps run CTA-locally
 };
+constexpr int GATHER_CAP = 4096;   // max gathered active elements (all rows)
 
 enum Status : int32_t {
   ST_OK = 0,
@@ -83,13 +87,12 @@ struct PgdSettings {
 // One reference bisection (binary_search_row) replayed from evaluations.
 struct Walk {
   int32_t status, eq, up, feas_done;
-  int32_t iters, nc, near_ties, n_direct;
+  int32_t iters, pad_, near_ties, n_direct;
   double ghat, E, r0, S0, bp_lo, bp_hi, count;
   double lo, hi, ym, y, residual, min_margin;
   int32_t hasL, hasH, hasA, hasB;
   double yL, yH;                    // certified: R(yL) < -E, R(yH) > E
   double ya, Ra, Sa, yb, Rb, Sb;    // nearest evaluated points with R<=0 / R>0
-  double cy[MAX_K], cR[MAX_K], cS[MAX_K];   // this sweep's evaluations
 };
 
 struct Newton {
@@ -120,6 +123,11 @@ struct Cmd {
   int32_t want_gram;
   int32_t resid_rows;            // PH_FINAL: accumulate a_j . delta for all rows
   int32_t write_delta, write_x, write_mask;
+  // PH_SWEEP active-set compaction: every candidate of row j lies in the
+  // walk interval [wlo_j, whi_j]; elements whose clip region is the same at
+  // both ends are folded into per-CTA fixed sums and dropped from the list.
+  int32_t compact, local;        // local: sweep runs on the gathered items in each CTA
+  double wlo[MAX_M], whi[MAX_M];
 };
 
 // Problem description (device pointers are filled by the host).
@@ -154,12 +162,16 @@ struct Problem {
   int32_t is_eq[MAX_M];
   double row_count[MAX_M];      // terms summed by the reference per row
   double ours_len;              // bound on our summation depth (error bound)
+  int32_t compact_cap;          // per-warp active-list capacity (0: no compaction)
+  int32_t pad0_;
 };
 
 // Controller-visible result.
 struct Result {
   int32_t status, path, newton_iters, converged, curvature_violations;
   int32_t passes, sweeps, stage1_row, near_ties, fallback;
+  int32_t local_sweeps, gathered;
+  double active;            // active elements after the last compacted sweep
   int32_t bisect_iters[MAX_M];
   double residual, alpha, beta, min_margin;
   double y[MAX_M], slacks[MAX_M], ghat[MAX_M], ghat_err[MAX_M], h[MAX_M];

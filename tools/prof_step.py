@@ -28,8 +28,50 @@ def main():
         r = api.pgd_step(*X, A, p.g_values, p.bounds_g, p.is_eq, p.partition, t=p.t, out=out)
     torch.cuda.synchronize()
     print(p.name, r.projection.path.name, "passes", r.projection.passes, "sweeps",
-          r.projection.sweeps, "alpha", r.alpha)
+          r.projection.sweeps, "local", r.projection.local_sweeps, "alpha", r.alpha)
+
+
+
+
+def trace(config="C2", seed=2):
+    """Per-pass device timeline of one persistent step (us)."""
+    import ctypes as C
+    from paper_2511_13905_b200 import _lib
+    p = synth.CONFIGS[config](seed)
+    cu = lambda v: torch.from_numpy(np.ascontiguousarray(v)).cuda()  # noqa: E731
+    X = [cu(getattr(p, k)) for k in ("x", "x_prev", "g", "g_prev", "d_prev")]
+    A = cu(p.grad.reshape(-1))
+    out = {k: torch.empty(p.n, dtype=torch.float64, device="cuda")
+           for k in ("x_new", "d", "rho_tilde")}
+    ctx = _lib.context(0)
+    for _ in range(2):
+        api.pgd_step(*X, A, p.g_values, p.bounds_g, p.is_eq, p.partition, t=p.t, out=out)
+    ctx.lib.topt_b200_debug_trace(ctx.h, 1, None)
+    api.pgd_step(*X, A, p.g_values, p.bounds_g, p.is_eq, p.partition, t=p.t, out=out)
+    buf = (C.c_ulonglong * 1024)()
+    ctx.lib.topt_b200_debug_trace(ctx.h, 0, buf)
+    allt = np.array(buf, dtype=np.float64).reshape(128, 8)
+    t, mk = allt[:64], allt[64:]
+    t0 = t[0, 0]
+    names = {0: "STEP", 1: "PREP", 2: "SWEEP", 3: "FEAS", 4: "NEWTON", 5: "FINAL", 7: "GATHER"}
+    for k in range(64):
+        if t[k, 0] == 0:
+            break
+        print(f"pass {k:2d} {names.get(int(t[k,5]),'?'):6s} start {1e-3*(t[k,0]-t0):8.2f} "
+              f"b0-end {1e-3*(t[k,1]-t[k,0]):7.2f} last-end {1e-3*(t[k,6]-t[k,0]):7.2f} "
+              f"fin-start {1e-3*(t[k,2]-t[k,0]):7.2f} reduce {1e-3*(t[k,3]-t[k,2]):6.2f} "
+              f"control {1e-3*(t[k,4]-t[k,3]):6.2f}" +
+              (f" | ctl marks add {1e-3*(mk[k,1]-mk[k,0]):6.2f} adv {1e-3*(mk[k,2]-mk[k,1]):6.2f}"
+               f" sched {1e-3*(mk[k,3]-mk[k,2]):6.2f} pre {1e-3*(mk[k,0]-t[k,3]):6.2f}"
+               f" [copy {1e-3*(mk[k,4]-mk[k,2]):5.2f} est {1e-3*(mk[k,5]-mk[k,4]):5.2f}"
+               f" path {1e-3*(mk[k,6]-mk[k,5]):5.2f} merge {1e-3*(mk[k,7]-mk[k,6]):5.2f}"
+               f" tail {1e-3*(mk[k,3]-mk[k,7]):5.2f}]"
+               if mk[k, 0] else ""))
 
 
 if __name__ == "__main__":
-    main()
+    if "--trace" in sys.argv:
+        sys.argv.remove("--trace")
+        trace()
+    else:
+        main()
