@@ -93,9 +93,21 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def make_problem(config, seed, rank=0):
+def make_problem(config, seed, world=1):
+    """The global problem.  N > 1 runs weak scaling: the grid grows along its
+    slowest axis so each rank's slab keeps the single-GPU size (C5 is the
+    fixed-size scale sweep of BASELINE.json and is not grown)."""
     from paper_2511_13905_b200 import synth
-    return synth.CONFIGS[config](seed + 1000 * rank)
+    if world == 1 or config == "C5":
+        return synth.CONFIGS[config](seed)
+    if config == "C1":
+        return synth.min_compliance_volume(256, 128 * world, seed)
+    if config == "C2":
+        return synth.min_volume_compliance(1024, 1024 * world, seed)
+    if config in ("C4", "C4p"):
+        return synth.com_constrained(256, 256, 128 * world, seed,
+                                     com_offset_x=0.02 if config == "C4p" else 0.0)
+    raise SystemExit(f"--gpus > 1 is not supported for {config}")
 
 
 def cpu_reference_sample(p, budget_s=12.0, max_reps=50):
@@ -157,23 +169,34 @@ def run_ours(args, rank, world):
 
     dev = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
-    p = make_problem(args.config, args.seed, rank)
-    n, m = p.n, p.m
+    gp = make_problem(args.config, args.seed, world)
+    # contiguous element slab of this rank (z-slabs for the 3-D grids)
+    lo, hi = rank * gp.n // world, (rank + 1) * gp.n // world
+    n, m = hi - lo, gp.m
     cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{dev}")  # noqa: E731
-    X = {k: cu(getattr(p, k)) for k in ("x", "x_prev", "g", "g_prev", "d_prev")}
-    A = cu(p.grad.reshape(-1))
+    X = {k: cu(getattr(gp, k)[lo:hi]) for k in ("x", "x_prev", "g", "g_prev", "d_prev")}
+    A = cu(gp.grad[:, lo:hi].reshape(-1))
     outs = {k: torch.empty(n, dtype=torch.float64, device=f"cuda:{dev}")
             for k in ("x_new", "d", "rho_tilde")}
-    ctx = _lib.context(dev)
+    if world > 1:
+        import torch.distributed as dist
+        obj = [_lib.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = _lib.Context(dev, rank, world, obj[0])
+        part = None
+    else:
+        ctx = _lib.context(dev)
+        part = gp.partition
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+    p = gp
 
     def step():
         return api.pgd_step(X["x"], X["x_prev"], X["g"], X["g_prev"], X["d_prev"], A,
-                            p.g_values, p.bounds_g, p.is_eq, p.partition, t=p.t,
-                            violation=p.violation, lower=p.lower, upper=p.upper, device=dev,
-                            out=outs)
+                            gp.g_values, gp.bounds_g, gp.is_eq, part, t=gp.t,
+                            violation=gp.violation, lower=gp.lower, upper=gp.upper, device=dev,
+                            out=outs, ctx=ctx, n_global=gp.n)
 
     for _ in range(args.warmup):
         res = step()
@@ -202,43 +225,68 @@ def run_ours(args, rank, world):
         ms = float(t.item())
     clk = clocks.stop()
 
-    # ---- e2e: host-buffer C-ABI call, pinned H2D inputs + D2H x_new, d --------
-    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
-    H = {k: pin(getattr(p, k)) for k in ("x", "x_prev", "g", "g_prev", "d_prev")}
-    HA = pin(p.grad)
+    # ---- e2e: pinned host inputs -> H2D -> step -> D2H x_new, d --------------
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    H = {k: pin(getattr(gp, k)[lo:hi]) for k in ("x", "x_prev", "g", "g_prev", "d_prev")}
+    HA = pin(gp.grad[:, lo:hi].reshape(-1))
+    HO = {k: torch.empty(n, dtype=torch.float64).pin_memory() for k in ("x_new", "d")}
     e2e_steps = max(3, min(args.steps, 10))
-    api.pgd_step(H["x"], H["x_prev"], H["g"], H["g_prev"], H["d_prev"], HA, p.g_values,
-                 p.bounds_g, p.is_eq, p.partition, t=p.t, device=dev, host_outputs=("x_new", "d"))
+
+    def e2e_step():
+        if world == 1:   # the host-buffer C-ABI entry point (copies inside the call)
+            api.pgd_step(H["x"].numpy(), H["x_prev"].numpy(), H["g"].numpy(),
+                         H["g_prev"].numpy(), H["d_prev"].numpy(), HA.numpy(),
+                         gp.g_values, gp.bounds_g, gp.is_eq, part, t=gp.t, device=dev,
+                         host_outputs=("x_new", "d"),
+                         out={"x_new": HO["x_new"].numpy(), "d": HO["d"].numpy()})
+            return
+        for k in ("x", "x_prev", "g", "g_prev", "d_prev"):
+            X[k].copy_(H[k], non_blocking=True)
+        A.copy_(HA, non_blocking=True)
+        step()
+        HO["x_new"].copy_(outs["x_new"], non_blocking=True)
+        HO["d"].copy_(outs["d"], non_blocking=True)
+
+    e2e_step()
     torch.cuda.synchronize()
+    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
+    ee0.record(stream)
     for _ in range(e2e_steps):
-        api.pgd_step(H["x"], H["x_prev"], H["g"], H["g_prev"], H["d_prev"], HA, p.g_values,
-                     p.bounds_g, p.is_eq, p.partition, t=p.t, device=dev,
-                     host_outputs=("x_new", "d"))
+        e2e_step()
+    ee1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    e2e_ms = max((time.perf_counter() - t0) * 1e3, ee0.elapsed_time(ee1)) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
     h2d = 8 * n * (5 + m)
     d2h = 8 * n * 2
+    # dominant kernel timing (all ranks take part: the passes are collective)
+    kern = kernel_pass_stats(ctx, step, min(args.steps, 10), flush)
 
     if rank != 0:
         return
     peak, peak_kind = measured_peak()
     b_alg = BYTES_PER_VAR.get(args.config, 64) * n
-    total_n = n * world
+    total_n = gp.n
     value = total_n / (ms * 1e-3)
     # dominant kernel: k_pass (every pass of the step is one launch of it)
-    kern = kernel_pass_stats(ctx, step, min(args.steps, 10), flush)
     per_launch_bytes = b_alg / max(1.0, kern["launches"] / max(1, min(args.steps, 10)))
     avg_launch_ms = kern.get("avg_ms")
     achieved = (per_launch_bytes / (avg_launch_ms * 1e-3) / 1e9) if avg_launch_ms else \
         (b_alg / (ms * 1e-3) / 1e9)
-    cpu = cpu_reference_sample(make_problem(args.config, args.seed), budget_s=args.cpu_budget)
+    cpu = (cpu_reference_sample(make_problem(args.config, args.seed), budget_s=args.cpu_budget)
+           if world == 1 else None)   # reported at N = 1 only
     line = {
         "metric": METRIC, "value": value, "unit": "design vars/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json config distributions)",
-        "config": {"workload": p.name, "n": n, "m": m, "seed": args.seed,
+        "config": {"workload": p.name, "n": gp.n, "n_per_rank": n, "m": m, "seed": args.seed,
+                   "parallelism": f"element slabs x{world}" + (", NCCL all-gather of pass "
+                                                               "partials" if world > 1 else ""),
                    "l2": "flushed (256 MiB write) between timed steps",
                    "path": res.projection.path.name,
                    "passes_per_step": res.projection.passes,
@@ -247,7 +295,9 @@ def run_ours(args, rank, world):
         "achieved_hbm_gbs_step": b_alg / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
-                     "kernel": "k_pass", "alg_bytes_per_var": BYTES_PER_VAR.get(args.config, 64),
+                     "kernel": ("k_step (persistent: every pass of the step in one launch)"
+                                if kern["launches"] <= min(args.steps, 10) else "k_pass"),
+                     "alg_bytes_per_var": BYTES_PER_VAR.get(args.config, 64),
                      "avg_launch_ms": avg_launch_ms, "max_launch_ms": kern.get("max_ms"),
                      "kernel_ms_per_step": kern.get("total_ms_per_step")},
         "cpu_baseline": cpu,

@@ -218,6 +218,19 @@ int topt_b200_pgd_step_dev(topt_b200_ctx* ctx, const topt_step_problem* prob,
                            const topt_pgd_settings* settings, const topt_proj_options* opts,
                            const topt_step_outputs* out, topt_proj_meta* meta);
 
+/* ---- multi-GPU: one process per GPU, element-slab sharding, NCCL ----------
+ * Each rank passes its contiguous slab of every n-vector (device pointers,
+ * prob->n = slab length); per pass the rank's partial sums are all-gathered
+ * over NCCL and combined in rank order on every GPU, so all ranks take the
+ * same decisions.  n_global / row_counts: global element / row counts. */
+int topt_b200_nccl_unique_id(unsigned char* out, size_t len);   /* 128 bytes */
+int topt_b200_ctx_create_ranks(int device, int rank, int world, const unsigned char* nccl_id,
+                               topt_b200_ctx** out);
+int topt_b200_pgd_step_ranks(topt_b200_ctx* ctx, const topt_step_problem* prob,
+                             int64_t n_global, const int64_t* row_counts,
+                             const topt_pgd_settings* settings, const topt_proj_options* opts,
+                             const topt_step_outputs* out, topt_proj_meta* meta);
+
 /* spectral_step_size + cg_direction + rho_tilde only, host
  * buffers.  d_out = new direction, rho_tilde_out = x - omega*alpha*d. */
 int topt_b200_step_direction(topt_b200_ctx* ctx, int64_t n, const double* x,

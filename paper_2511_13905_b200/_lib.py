@@ -76,6 +76,7 @@ EXPORTS = [
     "topt_b200_project", "topt_b200_project_dev", "topt_b200_owner_map",
     "topt_b200_pgd_step", "topt_b200_pgd_step_dev", "topt_b200_step_direction",
     "topt_b200_set_profiling", "topt_b200_kernel_time", "topt_b200_debug_trace",
+    "topt_b200_nccl_unique_id", "topt_b200_ctx_create_ranks", "topt_b200_pgd_step_ranks",
 ]
 
 _lib = None
@@ -116,6 +117,9 @@ def load():
         "topt_b200_set_profiling": [vp, C.c_int],
         "topt_b200_debug_trace": [vp, C.c_int, vp],
         "topt_b200_kernel_time": [vp, vp, vp, vp],
+        "topt_b200_nccl_unique_id": [vp, C.c_size_t],
+        "topt_b200_ctx_create_ranks": [C.c_int, C.c_int, C.c_int, vp, C.POINTER(C.c_void_p)],
+        "topt_b200_pgd_step_ranks": [vp, vp, i64, vp, vp, vp, vp, vp],
         "topt_b200_default_options": [vp],
         "topt_b200_default_settings": [vp],
     }
@@ -127,18 +131,45 @@ def load():
     return lib
 
 
-class Context:
-    """One CUDA device context of the library (stream, plan, workspaces)."""
+def _preload_torch_nccl():
+    """Make sure the process's NCCL is torch's (loaded with libtorch_cuda)
+    before the library resolves NCCL symbols."""
+    try:
+        import torch  # noqa: F401
+    except Exception:
+        pass
 
-    def __init__(self, device: int = 0):
+
+def nccl_unique_id() -> bytes:
+    _preload_torch_nccl()
+    buf = (C.c_ubyte * 128)()
+    rc = load().topt_b200_nccl_unique_id(buf, 128)
+    if rc != OK:
+        raise RuntimeError(f"topt_b200_nccl_unique_id failed ({rc}): NCCL not loadable")
+    return bytes(buf)
+
+
+class Context:
+    """One CUDA device context of the library (stream, plan, workspaces).
+    With rank/world/nccl_id it is one rank of a multi-GPU (NCCL) job."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes = None):
         self.lib = load()
         h = C.c_void_p()
-        rc = self.lib.topt_b200_ctx_create(int(device), C.byref(h))
+        if nccl_id is not None:
+            _preload_torch_nccl()
+            idb = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
+            rc = self.lib.topt_b200_ctx_create_ranks(int(device), int(rank), int(world), idb,
+                                                     C.byref(h))
+        else:
+            rc = self.lib.topt_b200_ctx_create(int(device), C.byref(h))
         if rc != OK:
             raise RuntimeError(f"topt_b200_ctx_create(device={device}) failed with status {rc} "
                                "(no CUDA device?)")
         self.h = h
         self.device = device
+        self.rank, self.world = rank, world
+        self.distributed = nccl_id is not None
 
     def close(self):
         if self.h:

@@ -394,7 +394,8 @@ def pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_equality
              partition=None, t=1, violation=0.0, lower=0.0, upper=1.0,
              settings: PgdSettings = None, device: int = 0, want_delta=False,
              want_mask=False, out=None,
-             host_outputs=("x_new", "d", "rho_tilde")) -> StepResult:
+             host_outputs=("x_new", "d", "rho_tilde"), ctx: L.Context = None,
+             n_global: int = None, row_counts=None) -> StepResult:
     """One PGD-TO step (Alg. 3 lines 2-15): BB step, PR+ direction, rho_tilde,
     linearization, projection, rho_{t+1} = rho_tilde + delta.
 
@@ -402,7 +403,7 @@ def pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_equality
     torch CUDA tensors -> device C-ABI (no copies; `out` may supply buffers).
     """
     settings = settings or PgdSettings()
-    ctx = L.context(device)
+    ctx = ctx or L.context(device)
     dev = _is_torch_cuda(x)
     n = int(x.numel() if dev else np.asarray(x).size)
     m = int(len(g_values))
@@ -445,8 +446,15 @@ def pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_equality
         o.x_new, o.d, o.rho_tilde = x_new.data_ptr(), d.data_ptr(), rt.data_ptr()
         o.delta = delta.data_ptr() if delta is not None else None
         o.mask = mask.data_ptr() if mask is not None else None
-        _check(ctx, ctx.lib.topt_b200_pgd_step_dev(ctx.h, C.byref(pr), C.byref(sc), C.byref(opts),
-                                                   C.byref(o), C.byref(meta)))
+        if getattr(ctx, "distributed", False):
+            rc_arr = None if row_counts is None else np.ascontiguousarray(row_counts, np.int64)
+            _check(ctx, ctx.lib.topt_b200_pgd_step_ranks(
+                ctx.h, C.byref(pr), int(n_global if n_global is not None else n), _ptr(rc_arr),
+                C.byref(sc), C.byref(opts), C.byref(o), C.byref(meta)))
+        else:
+            _check(ctx, ctx.lib.topt_b200_pgd_step_dev(ctx.h, C.byref(pr), C.byref(sc),
+                                                       C.byref(opts), C.byref(o),
+                                                       C.byref(meta)))
     else:
         arrs = {k: np.ascontiguousarray(v, np.float64) for k, v in
                 (("x", x), ("x_prev", x_prev), ("g", g), ("g_prev", g_prev), ("d_prev", d_prev),
@@ -456,9 +464,13 @@ def pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_equality
         pr.g_values, pr.bounds_g = _ptr(gv), _ptr(bg)
         pr.is_equality = _ptr(ie)
         pr.part_offsets, pr.part_indices = _ptr(off), _ptr(idx)
-        x_new = np.empty(n) if "x_new" in host_outputs else None
-        d = np.empty(n) if "d" in host_outputs else None
-        rt = np.empty(n) if "rho_tilde" in host_outputs else None
+        hb = out or {}
+        x_new = (hb["x_new"] if hb.get("x_new") is not None else np.empty(n)) \
+            if "x_new" in host_outputs else None
+        d = (hb["d"] if hb.get("d") is not None else np.empty(n)) \
+            if "d" in host_outputs else None
+        rt = (hb["rho_tilde"] if hb.get("rho_tilde") is not None else np.empty(n)) \
+            if "rho_tilde" in host_outputs else None
         delta = np.empty(n) if want_delta else None
         mask = np.empty(n, np.uint8) if want_mask else None
         o.x_new, o.d, o.rho_tilde = _ptr(x_new), _ptr(d), _ptr(rt)

@@ -111,7 +111,9 @@ __device__ __forceinline__ void load_cmd(const Plan* plan, Cmd* s_cmd) {
   __syncthreads();
 }
 
-// Multi-launch mode: one launch per pass; the last CTA runs the controller.
+// Multi-launch mode: one launch per pass; the last CTA runs the controller
+// (single rank), or -- rank mode, totals != nullptr -- writes this rank's
+// combined partial vector to totals[] for the cross-rank all-gather.
 __global__ void __launch_bounds__(BLOCK, 1) k_pass(Plan* plan, double* partials,
                                                 unsigned* counter, double* totals) {
   __shared__ Cmd s_cmd;
@@ -140,12 +142,33 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass(Plan* plan, double* partials,
   if (!s_last) return;
   __threadfence();
   finish_reduce(partials, gridDim.x, s_cmd.nslots, s_cmd.phase, s_tot, s_red);
-  control_step(plan, reinterpret_cast<Plan*>(s_dyn), s_tot);
+  if (totals) {   // rank mode: publish this rank's totals, no control here
+    for (int s = threadIdx.x; s < s_cmd.nslots; s += BLOCK) totals[s] = s_tot[s];
+  } else {
+    control_step(plan, reinterpret_cast<Plan*>(s_dyn), s_tot);
+  }
   if (threadIdx.x == 0) {
     *counter = 0u;
     __threadfence();
   }
-  (void)totals;
+}
+
+// Rank mode: combine the all-gathered per-rank totals in rank order (every
+// rank computes the same bits) and run the controller on the device.
+__global__ void __launch_bounds__(BLOCK, 1) k_control(Plan* plan, const double* gathered,
+                                                   int world) {
+  __shared__ double s_tot[PMAX];
+  extern __shared__ int4 s_dyn[];
+  const int ns = plan->cmd.nslots, phase = plan->cmd.phase;
+  if (phase == PH_DONE) return;
+  for (int s = threadIdx.x; s < ns; s += BLOCK) {
+    const int op = slot_op(phase, s);
+    double r = gathered[s];
+    for (int q = 1; q < world; ++q) r = apply_op(op, r, gathered[(size_t)q * PMAX + s]);
+    s_tot[s] = r;
+  }
+  __syncthreads();
+  control_step(plan, reinterpret_cast<Plan*>(s_dyn), s_tot);
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -313,7 +336,53 @@ struct topt_b200_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double prof_ms = 0.0, prof_max = 0.0;
   int64_t prof_n = 0;
+  // multi-rank (one process per GPU, NCCL over NVLink)
+  int rank = 0, world = 1;
+  void* comm = nullptr;          // ncclComm_t
+  double* d_rank_tot = nullptr;  // [PMAX]
+  double* d_gathered = nullptr;  // [world][PMAX]
+  int64_t n_global_override = 0;
+  const int64_t* row_counts_override = nullptr;
 };
+
+// ---- NCCL, resolved at run time (the process may already hold torch's copy)
+#include <dlfcn.h>
+#include <nccl.h>
+namespace {
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    // Prefer a copy already in the process (e.g. torch's, whose libtorch_cuda
+    // needs its own newer NCCL symbols); never inject one into the global
+    // symbol namespace.
+    void* h = nullptr;
+    if (const char* p = getenv("TOPT_B200_NCCL_LIB")) h = dlopen(p, RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
+    if (h) {
+      api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+      api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+      api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+      api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+      api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather;
+    }
+  }
+  return api;
+}
+}  // namespace
 
 namespace {
 
@@ -360,7 +429,10 @@ const char* status_msg(int st) {
 }
 
 // Run a plan to completion on the device.  hp.P must be filled.
+int run_plan_ranks(topt_b200_ctx* ctx, Plan& hp);
+
 int run_plan(topt_b200_ctx* ctx, Plan& hp) {
+  if (ctx->comm) return run_plan_ranks(ctx, hp);
   const bool persistent = ctx->persistent && ctx->coop_grid > 0;
   const int grid = persistent ? ctx->coop_grid : ctx->grid;
   const int64_t per_thread = (hp.P.n + (int64_t)grid * BLOCK - 1) / ((int64_t)grid * BLOCK);
@@ -408,6 +480,53 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp) {
     k_pass<<<ctx->grid, BLOCK, sizeof(Plan), ctx->stream>>>(ctx->d_plan, ctx->d_part,
                                                             ctx->d_counter, ctx->d_totals);
     ctx->launches++;
+    CUDA_TRY(ctx, cudaGetLastError());
+    if (ctx->profile) cudaEventRecord(ctx->ev1, ctx->stream);
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_phase, &ctx->d_plan->cmd.phase, sizeof(int),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->profile) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+      ctx->prof_ms += ms;
+      ctx->prof_max = std::max(ctx->prof_max, (double)ms);
+      ctx->prof_n++;
+    }
+    phase = *ctx->h_phase;
+  }
+  CUDA_TRY(ctx, cudaMemcpyAsync(&hp, ctx->d_plan, sizeof(Plan), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (phase != PH_DONE) return fail(ctx, TOPT_ERR_INTERNAL, "plan did not terminate");
+  if (hp.res.status != ST_OK) return fail(ctx, hp.res.status, status_msg(hp.res.status));
+  return TOPT_OK;
+}
+
+// Multi-rank: per pass, every rank reduces its slab's partials on its GPU,
+// the rank totals are all-gathered over NCCL (NVLink), and every rank
+// combines them in rank order and runs the controller -- identical decisions
+// everywhere, no host arithmetic.  The host only sequences the launches and
+// polls the next phase.
+int run_plan_ranks(topt_b200_ctx* ctx, Plan& hp) {
+  const int grid = ctx->grid;
+  const int64_t per_thread = (hp.P.n + (int64_t)grid * BLOCK - 1) / ((int64_t)grid * BLOCK);
+  hp.P.ours_len = (double)per_thread + (double)grid + 64.0 + (double)ctx->world;
+  hp.P.compact_cap = 0;
+  plan_start(hp);
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_plan, &hp, sizeof(Plan), cudaMemcpyHostToDevice, ctx->stream));
+  int phase = hp.cmd.phase;
+  NcclApi& api = nccl();
+  for (int it = 0; phase != PH_DONE && it < 4096; ++it) {
+    if (ctx->profile) cudaEventRecord(ctx->ev0, ctx->stream);
+    k_pass<<<grid, BLOCK, sizeof(Plan), ctx->stream>>>(ctx->d_plan, ctx->d_part, ctx->d_counter,
+                                                       ctx->d_rank_tot);
+    CUDA_TRY(ctx, cudaGetLastError());
+    const ncclResult_t nr = api.AllGather(ctx->d_rank_tot, ctx->d_gathered, PMAX, ncclDouble,
+                                          (ncclComm_t)ctx->comm, ctx->stream);
+    if (nr != ncclSuccess)
+      return fail(ctx, TOPT_ERR_CUDA, std::string("ncclAllGather: ") +
+                                          (api.GetErrorString ? api.GetErrorString(nr) : "?"));
+    k_control<<<1, BLOCK, sizeof(Plan), ctx->stream>>>(ctx->d_plan, ctx->d_gathered, ctx->world);
+    ctx->launches += 2;
     CUDA_TRY(ctx, cudaGetLastError());
     if (ctx->profile) cudaEventRecord(ctx->ev1, ctx->stream);
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_phase, &ctx->d_plan->cmd.phase, sizeof(int),
@@ -575,6 +694,8 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
                                   ctx->max_dyn_smem) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sizeof(Plan)) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_control, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(Plan)) == cudaSuccess;
   if (ok) {
     int per_sm = 0, coop = 0;
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
@@ -603,6 +724,9 @@ void topt_b200_ctx_destroy(topt_b200_ctx* ctx) {
   cudaFree(ctx->d_totals);
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_trace);
+  if (ctx->comm && nccl().ok) nccl().CommDestroy((ncclComm_t)ctx->comm);
+  cudaFree(ctx->d_rank_tot);
+  cudaFree(ctx->d_gathered);
   cudaFree(ctx->d_blk_cnt);
   cudaFree(ctx->d_ga);
   cudaFree(ctx->d_gr);
@@ -636,6 +760,43 @@ int topt_b200_debug_trace(topt_b200_ctx* ctx, int enable, unsigned long long* ou
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpy(out, ctx->d_trace, 128 * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   }
+  return TOPT_OK;
+}
+
+int topt_b200_nccl_unique_id(unsigned char* out, size_t len) {
+  NcclApi& api = nccl();
+  if (!api.ok) return TOPT_ERR_UNSUPPORTED;
+  if (len < sizeof(ncclUniqueId)) return TOPT_ERR_PARAMETER;
+  ncclUniqueId id;
+  if (api.GetUniqueId(&id) != ncclSuccess) return TOPT_ERR_CUDA;
+  std::memcpy(out, &id, sizeof(id));
+  return TOPT_OK;
+}
+
+int topt_b200_ctx_create_ranks(int device, int rank, int world, const unsigned char* nccl_id,
+                               topt_b200_ctx** out) {
+  *out = nullptr;
+  NcclApi& api = nccl();
+  if (!api.ok) return TOPT_ERR_UNSUPPORTED;
+  if (world < 1 || rank < 0 || rank >= world) return TOPT_ERR_PARAMETER;
+  topt_b200_ctx* ctx = nullptr;
+  int rc = topt_b200_ctx_create(device, &ctx);
+  if (rc) return rc;
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_id, sizeof(id));
+  ncclComm_t comm = nullptr;
+  if (api.CommInitRank(&comm, world, id, rank) != ncclSuccess) {
+    topt_b200_ctx_destroy(ctx);
+    return TOPT_ERR_CUDA;
+  }
+  ctx->comm = comm;
+  ctx->rank = rank;
+  ctx->world = world;
+  bool ok = cudaMalloc(&ctx->d_rank_tot, sizeof(double) * PMAX) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_gathered, sizeof(double) * PMAX * world) == cudaSuccess;
+  ok = ok && cudaMemset(ctx->d_rank_tot, 0, sizeof(double) * PMAX) == cudaSuccess;
+  if (!ok) { topt_b200_ctx_destroy(ctx); return TOPT_ERR_CUDA; }
+  *out = ctx;
   return TOPT_OK;
 }
 
@@ -887,6 +1048,19 @@ static int pgd_step_impl(topt_b200_ctx* ctx, Plan& hp, const topt_step_problem* 
   return TOPT_OK;
 }
 
+int topt_b200_pgd_step_ranks(topt_b200_ctx* ctx, const topt_step_problem* prob,
+                             int64_t n_global, const int64_t* row_counts,
+                             const topt_pgd_settings* settings, const topt_proj_options* opts,
+                             const topt_step_outputs* out, topt_proj_meta* meta) {
+  if (!ctx->comm) return fail(ctx, TOPT_ERR_PARAMETER, "context has no NCCL communicator");
+  ctx->n_global_override = n_global;
+  ctx->row_counts_override = row_counts;
+  const int rc = topt_b200_pgd_step_dev(ctx, prob, settings, opts, out, meta);
+  ctx->n_global_override = 0;
+  ctx->row_counts_override = nullptr;
+  return rc;
+}
+
 int topt_b200_pgd_step_dev(topt_b200_ctx* ctx, const topt_step_problem* prob,
                            const topt_pgd_settings* settings, const topt_proj_options* opts,
                            const topt_step_outputs* out, topt_proj_meta* meta) {
@@ -894,6 +1068,12 @@ int topt_b200_pgd_step_dev(topt_b200_ctx* ctx, const topt_step_problem* prob,
   Plan& hp = ctx->h_plan;
   int rc = init_problem(ctx, hp, prob->n, prob->m, opts);
   if (rc) return rc;
+  if (ctx->n_global_override > 0) {
+    hp.P.n_global = ctx->n_global_override;
+    for (int j = 0; j < prob->m; ++j)
+      hp.P.row_count[j] = ctx->row_counts_override ? (double)ctx->row_counts_override[j]
+                                                   : (double)ctx->n_global_override;
+  }
   if (!out->rho_tilde || !out->d)
     return fail(ctx, TOPT_ERR_DOMAIN, "pgd_step_dev: rho_tilde and d outputs are required");
   Problem& P = hp.P;
