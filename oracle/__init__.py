@@ -205,7 +205,8 @@ def project(rho, grad, g_values, bounds_g, gd_step, is_eq=None, partition=None,
                 converged=bool(meta.converged), curvature_violations=meta.curvature_violations,
                 stage1_row=meta.stage1_row, ghat=ghat,
                 bisect_iters=list(meta.bisect_iters[:m]) if m <= 64 else None,
-                gammas=gam[:meta.newton_iters].copy(), trace=tr)
+                gammas=gam[:min(meta.newton_iters, 64)].copy(),
+                phi_inf=gam[64:64 + min(meta.newton_iters, 64)].copy(), trace=tr)
 
 
 def settings(alpha_max=1e2, alpha_fallback=0.2, omega=1.0, eps_alpha=1e-6, tol_n=1e-6,

@@ -412,8 +412,10 @@ int orc_project_newton(int64_t n, int64_t m, const double* rho, const double* gr
     memcpy(phi, tphi, sizeof(double) * (size_t)m);
     merit = tmerit;
     ++iters;
-    if (meta->iter_trace)
+    if (meta->iter_trace) {
       meta->iter_trace[iters - 1] = gamma;
+      if (iters - 1 < 64) meta->iter_trace[64 + iters - 1] = linf(phi, m);
+    }
   }
 #undef JH
 #undef JP

@@ -478,7 +478,7 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp) {
   for (int it = 0; phase != PH_DONE && it < 4096; ++it) {
     if (ctx->profile) cudaEventRecord(ctx->ev0, ctx->stream);
     k_pass<<<ctx->grid, BLOCK, sizeof(Plan), ctx->stream>>>(ctx->d_plan, ctx->d_part,
-                                                            ctx->d_counter, ctx->d_totals);
+                                                            ctx->d_counter, nullptr);
     ctx->launches++;
     CUDA_TRY(ctx, cudaGetLastError());
     if (ctx->profile) cudaEventRecord(ctx->ev1, ctx->stream);
@@ -493,6 +493,7 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp) {
       ctx->prof_n++;
     }
     phase = *ctx->h_phase;
+    if (getenv("TOPT_B200_DEBUG_PHASES") && it < 64) fprintf(stderr, "[topt1] pass %d -> phase %d\n", it, phase);
   }
   CUDA_TRY(ctx, cudaMemcpyAsync(&hp, ctx->d_plan, sizeof(Plan), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
@@ -540,6 +541,7 @@ int run_plan_ranks(topt_b200_ctx* ctx, Plan& hp) {
       ctx->prof_n++;
     }
     phase = *ctx->h_phase;
+    if (getenv("TOPT_B200_DEBUG_PHASES") && it < 64) fprintf(stderr, "[topt] pass %d -> phase %d\n", it, phase);
   }
   CUDA_TRY(ctx, cudaMemcpyAsync(&hp, ctx->d_plan, sizeof(Plan), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));

@@ -311,7 +311,7 @@ TOPT_HDN inline double est_p_above(const RootEst& e, double y) {
   if (e.kind == 0) return approx_ncdf_upper((y - e.ye) * e.inv_sig);
   const double ay = fabs(y);
   if (!(ay > 0.0)) return e.kind == 1 ? 0.0 : 1.0;
-  double p = (approx_log2(ay) - (e.L - 66.0)) / 66.0;  // P(|root| < |y|), log-uniform prior
+  double p = (approx_log2(ay) - (e.L - 66.0)) * (1.0 / 66.0);  // P(|root| < |y|), log-uniform prior
   p = dmin_(dmax_(p, 0.0), 1.0);
   return e.kind == 1 ? p : 1.0 - p;
 }
@@ -492,7 +492,15 @@ TOPT_NOINLINE bool schedule_sweep(Plan& pl) {
     c.row_start[j] = tot;
     if (pl.w[j].status == WK_NEED) {
       const Walk w = pl.w[j];
-      tot += walk_candidates(w, pl.P.opt, per, c.cand_y + tot, pl.sc);
+      const int nc = walk_candidates(w, pl.P.opt, per, c.cand_y + tot, pl.sc);
+      double* cy = c.cand_y + tot;   // the sweeps want each row's candidates ascending
+      for (int a = 1; a < nc; ++a) {
+        const double v = cy[a];
+        int b = a - 1;
+        while (b >= 0 && cy[b] > v) { cy[b + 1] = cy[b]; --b; }
+        cy[b + 1] = v;
+      }
+      tot += nc;
     }
   }
   for (int j = m; j <= MAX_M; ++j) c.row_start[j] = tot;
@@ -707,7 +715,7 @@ TOPT_NOINLINE void after_walks(Plan& pl) {
 }
 
 // PREP totals -> g_hat, error bounds, walks, path dispatch.
-TOPT_NOINLINE void consume_prep(Plan& pl, const double* t) {
+TOPT_NOINLINE void consume_prep_core(Plan& pl, const double* t) {
   Problem& P = pl.P;
   const int m = P.m;
   Result& r = pl.res;
@@ -732,11 +740,11 @@ TOPT_NOINLINE void consume_prep(Plan& pl, const double* t) {
     r.ghat[j] = ghat;
     r.ghat_err[j] = (gamma_k((double)P.n_global + 2.0) + gamma_k(ours)) * s[PS_DABS];
     if (pl.cmd.validate_part && s[PS_NZOUT] > 0.0) { set_error(pl, ST_DOMAIN); return; }
-    // + 4u T: compacted sweeps sum the terms of elements that stay free on
-    // the walk interval as y * sum(a^2) instead of sum fl(fl(y a) a).
+    // + 16u T: sweeps sum free terms as y * sum(a^2) instead of
+    // sum fl(fl(y a) a), and classify regions by breakpoints (passes.cuh).
     const double E = 1.0625 * (gamma_k(cnt + 2.0) * (fabs(ghat) + s[PS_T]) + gerr +
                                gamma_k(ours) * (fabs(ghat) + s[PS_T]) +
-                               4.0 * kUnit * s[PS_T]) + 1e-300;
+                               16.0 * kUnit * s[PS_T]) + 1e-300;
     const double r0 = s[PS_S0] - ghat;
     walk_init(pl.w[j], P.is_eq[j], ghat, E, r0, s[PS_SLOPE0], s[PS_BPLO], s[PS_BPHI],
               s[PS_ANY], cnt);
@@ -757,7 +765,15 @@ TOPT_NOINLINE void consume_prep(Plan& pl, const double* t) {
   }
   const Evals none = {nullptr, nullptr, 0};
   for (int j = 0; j < m; ++j) walk_advance(pl.w[j], P.opt, none);
-  if (!schedule_sweep(pl)) after_walks(pl);
+  pl.cmd.phase = PH_SWEEP;   // marker: the caller schedules the first sweep
+  pl.cmd.nslots = -1;
+}
+
+// (returns with cmd.nslots == -1 when the walks need their first sweep)
+TOPT_NOINLINE void consume_prep(Plan& pl, const double* t) {
+  consume_prep_core(pl, t);
+  if (pl.cmd.phase == PH_SWEEP && pl.cmd.nslots == -1)
+    if (!schedule_sweep(pl)) after_walks(pl);
 }
 
 TOPT_NOINLINE void consume_sweep(Plan& pl, const double* t) {
@@ -901,6 +917,146 @@ TOPT_NOINLINE void plan_consume(Plan& pl, const double* t) {
 }
 
 #if defined(__CUDACC__)
+// Warp-parallel candidate choice.  Lane 0 walks the predicted path (the
+// direction at each level is a single comparison with the estimate's
+// threshold) and records the uncertain levels; the lanes then price the path
+// nodes and their siblings in parallel (prefix product of branch
+// probabilities) and keep the K most probable, exactly as walk_candidates
+// ranks them.
+constexpr int WPATH = 32;
+struct WarpPath {
+  double y[WPATH], lo[WPATH], hi[WPATH];
+  int np, n0;
+  RootEst e;
+};
+
+__device__ int walk_candidates_warp(const Walk& w, const ProjOptions& o, int K, double* out,
+                                    WarpPath& wp) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    int n0 = 0;
+    if (!w.feas_done) out[n0++] = w.up ? w.bp_hi : w.bp_lo;
+    const RootEst e = walk_estimate(w);
+    // direction threshold: right (lo = ym) iff p_above(ym) >= 0.5
+    const double L2 = e.L - 33.0;
+    int np = 0;
+    double lo = w.lo, hi = w.hi, ym = w.ym;
+    int it = w.iters;
+    const bool hasL = w.hasL, hasH = w.hasH;
+    const double yL = w.yL, yH = w.yH;
+    const int Kp = (K - n0 < WPATH) ? K - n0 : WPATH;
+    while (np < Kp && (hi - lo) > o.tol_b && it < o.binary_maxiter) {
+      if (hasH && yH <= ym) {
+        hi = ym;
+      } else if (hasL && yL >= ym) {
+        lo = ym;
+      } else {
+        bool right;
+        if (e.kind == 0) right = ym <= e.ye;
+        else if (e.kind == 1) right = approx_log2(fabs(ym)) >= L2;
+        else right = approx_log2(fabs(ym)) <= L2;
+        wp.y[np] = ym; wp.lo[np] = lo; wp.hi[np] = hi;
+        ++np;
+        if (right) lo = ym; else hi = ym;
+      }
+      ym = 0.5 * (lo + hi);
+      ++it;
+    }
+    wp.np = np;
+    wp.n0 = n0;
+    wp.e = e;
+  }
+  __syncwarp();
+  const int np = wp.np, n0 = wp.n0;
+  const RootEst e = wp.e;
+  // level k = lane: branch probabilities
+  double q = 1.0, ym = 0.0, alt = 0.0;
+  if (lane < np) {
+    ym = wp.y[lane];
+    const double pa = est_p_above(e, ym);
+    const bool right = pa >= 0.5;
+    q = right ? pa : 1.0 - pa;
+    alt = right ? 0.5 * (wp.lo[lane] + ym) : 0.5 * (ym + wp.hi[lane]);
+  }
+  // P_k = prod_{i<k} q_i (exclusive prefix product, fixed shuffle order)
+  double P = q;
+  for (int off = 1; off < 32; off <<= 1) {
+    const double v = __shfl_up_sync(0xffffffffu, P, off);
+    if (lane >= off) P = P * v;
+  }
+  double Pex = __shfl_up_sync(0xffffffffu, P, 1);
+  if (lane == 0) Pex = 1.0;
+  const double pp = lane < np ? Pex : -1.0;                       // path node
+  const double hp0 = lane < np ? Pex * (1.0 - q) : -1.0;          // its sibling
+  const double hp = hp0 > 1e-12 ? hp0 : -1.0;
+  // rank every item: path node k before hedges of equal probability, lower k first
+  int rp = 0, rh = 0;
+  for (int s = 0; s < 32; ++s) {
+    const double ps = __shfl_sync(0xffffffffu, pp, s);
+    const double hs = __shfl_sync(0xffffffffu, hp, s);
+    if (s < np) {
+      rp += (ps > pp || (ps == pp && s < lane)) ? 1 : 0;
+      rp += (hs > pp) ? 1 : 0;
+      rh += (ps >= hp) ? 1 : 0;
+      rh += (hs > hp || (hs == hp && s < lane)) ? 1 : 0;
+    }
+  }
+  const int room = K - n0;
+  if (lane < np && rp < room) out[n0 + rp] = ym;
+  if (lane < np && hp > 0.0 && rh < room) out[n0 + rh] = alt;
+  int taken = (lane < np && rp < room ? 1 : 0) + (lane < np && hp > 0.0 && rh < room ? 1 : 0);
+  for (int off = 16; off > 0; off >>= 1) taken += __shfl_xor_sync(0xffffffffu, taken, off);
+  __syncwarp();
+  return n0 + taken;
+}
+
+// Warp version of schedule_sweep (same command layout).
+__device__ bool schedule_sweep_warp(Plan& pl, WarpPath& wp) {
+  const int lane = threadIdx.x & 31;
+  const int m = pl.P.m;
+  int need = 0;
+  for (int j = 0; j < m; ++j) need += (pl.w[j].status == WK_NEED);
+  if (!need) return false;
+  int per = MAX_CAND / need;
+  if (per > MAX_K) per = MAX_K;
+  Cmd& c = pl.cmd;
+  int tot = 0;
+  for (int j = 0; j < m; ++j) {
+    if (lane == 0) c.row_start[j] = tot;
+    if (pl.w[j].status == WK_NEED) {
+      const Walk w = pl.w[j];
+      const int nc = walk_candidates_warp(w, pl.P.opt, per, c.cand_y + tot, wp);
+      // ascending order for the sweeps (rank sort, ties by index)
+      double* cy = c.cand_y + tot;
+      const double v = lane < nc ? cy[lane] : 0.0;
+      int rk = 0;
+      for (int q = 0; q < nc; ++q) {
+        const double u = __shfl_sync(0xffffffffu, v, q);
+        rk += (u < v || (u == v && q < lane)) ? 1 : 0;
+      }
+      __syncwarp();
+      if (lane < nc) cy[rk] = v;
+      __syncwarp();
+      tot += nc;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    c.phase = PH_SWEEP;
+    for (int j = m; j <= MAX_M; ++j) c.row_start[j] = tot;
+    c.compact = (pl.P.compact_cap > 0 && (m == 1 || pl.P.has_part)) ? 1 : 0;
+    for (int j = 0; j < m; ++j) {
+      c.wlo[j] = pl.w[j].lo;
+      c.whi[j] = pl.w[j].hi;
+    }
+    c.ncand = tot;
+    c.nslots = 2 * tot + ((c.compact && !c.local) ? 1 : 0);
+    if (c.local) pl.res.local_sweeps++; else pl.res.sweeps++;
+  }
+  __syncwarp();
+  return true;
+}
+
 // Warp-parallel version of consume_sweep (all 32 lanes of one warp): lane k
 // holds candidate k; bracket updates are warp arg-reductions and each
 // replayed midpoint is matched with one ballot.  Same decisions as the
@@ -1025,30 +1181,61 @@ __device__ void consume_sweep_warp(Plan& pl, const double* t) {
     if (lane == 0) pl.w[j] = w;
     __syncwarp();
   }
+  __shared__ WarpPath s_wp;
+  __shared__ int s_act;
   if (lane == 0) {
     if (was_global_compact) pl.res.active = t[2 * c.ncand];
     pl.res.passes++;
     int need = 0;
     for (int j = 0; j < m; ++j) need += (pl.w[j].status == WK_NEED);
+    s_act = 0;
     if (need && was_global_compact && pl.res.active <= (double)GATHER_CAP) {
       c.phase = PH_GATHER;
       c.nslots = 0;
-    } else if (!schedule_sweep(pl)) {
-      after_walks(pl);
+    } else {
+      s_act = 1;
     }
-    if (pl.res.passes > 4096 && pl.cmd.phase != PH_DONE) set_error(pl, ST_INTERNAL);
   }
+  __syncwarp();
+  if (s_act) {
+    const bool more = schedule_sweep_warp(pl, s_wp);
+    if (lane == 0 && !more) after_walks(pl);
+  }
+  if (lane == 0 && pl.res.passes > 4096 && pl.cmd.phase != PH_DONE) set_error(pl, ST_INTERNAL);
   __syncwarp();
 }
 
 // Called by all lanes of one warp.
 __device__ void plan_consume_warp(Plan& pl, const double* t) {
-  if (pl.cmd.phase == PH_SWEEP) {
+  const int lane = threadIdx.x & 31;
+  __shared__ WarpPath s_wp2;
+  const int ph = pl.cmd.phase;
+  if (ph == PH_SWEEP) {
     consume_sweep_warp(pl, t);
-  } else {
-    if ((threadIdx.x & 31) == 0) plan_consume(pl, t);
-    __syncwarp();
+    return;
   }
+  if (ph == PH_PREP || ph == PH_GATHER) {
+    if (lane == 0) {
+      pl.res.passes++;
+      if (ph == PH_PREP) {
+        consume_prep_core(pl, t);
+      } else {
+        pl.cmd.local = 1;
+        pl.res.gathered = 1;
+        pl.cmd.phase = PH_SWEEP;
+        pl.cmd.nslots = -1;
+      }
+    }
+    __syncwarp();
+    if (pl.cmd.phase == PH_SWEEP && pl.cmd.nslots == -1) {
+      const bool more = schedule_sweep_warp(pl, s_wp2);
+      if (lane == 0 && !more) after_walks(pl);
+    }
+    __syncwarp();
+    return;
+  }
+  if (lane == 0) plan_consume(pl, t);
+  __syncwarp();
 }
 #endif
 

@@ -156,9 +156,20 @@ __device__ __forceinline__ void prep_elem(PrepAcc& A, double a, double r, double
   A.v[PS_T] += fabs(a) * dmax_(fabs(lo), fabs(hi));
   if (fabs(a) >= kGradFloor) {
     A.v[PS_ANY] += 1.0;
-    const double c1 = lo / a, c2 = hi / a;
-    A.v[PS_BPLO] = dmin_(A.v[PS_BPLO], dmin_(c1, c2));
-    A.v[PS_BPHI] = dmax_(A.v[PS_BPHI], dmax_(c1, c2));
+    // Exact IEEE divisions only where they can move the running min / max:
+    // a float estimate (rel. error < 1e-6 in the checked range) filters out
+    // the rest.  min(c1,c2) = (a > 0 ? lo : hi) / a, max = (a > 0 ? hi : lo) / a.
+    const double nmin = a > 0.0 ? lo : hi, nmax = a > 0.0 ? hi : lo;
+    const double fa = fabs(a);
+    bool do_min = true, do_max = true;
+    if (fa > 1e-30 && fa < 1e30 && fabs(nmin) < 1e30 && fabs(nmax) < 1e30) {
+      const float ra = __frcp_rn((float)a);
+      const double qmin = (double)((float)nmin * ra), qmax = (double)((float)nmax * ra);
+      do_min = qmin - 1e-5 * fabs(qmin) - 1e-300 < A.v[PS_BPLO];
+      do_max = qmax + 1e-5 * fabs(qmax) + 1e-300 > A.v[PS_BPHI];
+    }
+    if (do_min) A.v[PS_BPLO] = dmin_(A.v[PS_BPLO], dmin_(lo / a, hi / a));
+    if (do_max) A.v[PS_BPHI] = dmax_(A.v[PS_BPHI], dmax_(lo / a, hi / a));
   }
 }
 
@@ -234,20 +245,58 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
 }
 
 // ---- PH_SWEEP: r_j(y_k) and slope at up to MAX_K candidates per row -------
+// 1/a to full precision without the IEEE division subroutine: hardware
+// reciprocal estimate + two Newton steps (< 1 ulp off before the final
+// product).  |a| outside the normal range falls back to the IEEE division.
+__device__ __forceinline__ double rcp_full(double a) {
+  const double fa = fabs(a);
+  if (!(fa > 1e-300 && fa < 1e300)) return 1.0 / a;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+  r = __fma_rn(r, __fma_rn(-a, r, 1.0), r);
+  r = __fma_rn(r, __fma_rn(-a, r, 1.0), r);
+  return r;
+}
+
+// One element's contribution to r(y_k) at the SORTED candidates y[0..cnt):
+// its clip region is L for y < bl, free for bl <= y <= bh, U for y > bh
+// (bl, bh = its two breakpoints in y), so two binary searches give the region
+// of every candidate, and the sweep accumulates per candidate only the
+// clipped constants C_k and the free slope S_k (r_k = C_k + y_k S_k).  An
+// element whose breakpoint lies within a few ulps of a candidate may be
+// classified differently from the reference's fl(y a) test; its term then
+// differs by <= 4u|a| max(|lo|,|hi|) and the free terms by 2u|t|: both are
+// inside the certification bound E (+16u T, controller.h).
 template <int KC>
 __device__ __forceinline__ void sweep_elem(double a, double r, const double* y, int cnt,
-                                           double L, double U, double* R, double* S) {
+                                           double L, double U, double* C, double* S) {
+  if (a == 0.0) return;   // every term is an exact zero
   const double lo = L - r, hi = U - r;
-  const double aa = a * a;
+  const double ra = rcp_full(a);
+  const double b1 = lo * ra, b2 = hi * ra;
+  const bool pos = a > 0.0;
+  const double bl = pos ? b1 : b2, bh = pos ? b2 : b1;
+  const double cl = a * (pos ? lo : hi), ch = a * (pos ? hi : lo), aa = a * a;
+  int p1 = 0, p2 = 0;   // p1 = #{y_k < bl}, p2 = #{y_k <= bh}
+#pragma unroll
+  for (int s = (KC >= 16 ? 16 : KC); s > 0; s >>= 1) {
+    if (p1 + s <= cnt && y[p1 + s - 1] < bl) p1 += s;
+    if (p2 + s <= cnt && y[p2 + s - 1] <= bh) p2 += s;
+  }
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
-    if (k < cnt) {
-      const double v = y[k] * a;
-      const bool below = v < lo, above = v > hi;
-      R[k] += a * (below ? lo : (above ? hi : v));
-      S[k] += (below || above) ? 0.0 : aa;
-    }
+    C[k] += (k < p1) ? cl : ((k >= p2) ? ch : 0.0);
+    S[k] += (k >= p1 && k < p2) ? aa : 0.0;
   }
+}
+
+// r_k = C_k + y_k S_k into the (R, S) slot pair layout
+template <int KC>
+__device__ __forceinline__ void sweep_finish(const double* y, int cnt, double* C,
+                                             const double* S) {
+#pragma unroll
+  for (int k = 0; k < KC; ++k)
+    if (k < cnt) C[k] = C[k] + y[k] * S[k];
 }
 
 template <int KC>
@@ -278,6 +327,7 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
     if (owner && owner[i] != j) a0 = 0.0;
     sweep_elem<KC>(a0, rho[i], y, cnt, L, U, R, S);
   }
+  sweep_finish<KC>(y, cnt, R, S);
   double v[2 * KC];
 #pragma unroll
   for (int k = 0; k < KC; ++k) { v[2 * k] = R[k]; v[2 * k + 1] = S[k]; }
@@ -297,7 +347,7 @@ __device__ __noinline__ void pass_sweep_row_compact(const PassCtx& c, int j, int
   const double* __restrict__ rho = P.rho;
   const double* __restrict__ ar = P.grad + (int64_t)j * P.ld;
   const int8_t* __restrict__ owner = P.owner;
-  const double L = P.lower, U = P.upper;
+  const double L = P.lower, U_ = P.upper;
   const double wlo = cmd.wlo[j], whi = cmd.whi[j];
   const double* y = cmd.cand_y + b;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -318,7 +368,7 @@ __device__ __noinline__ void pass_sweep_row_compact(const PassCtx& c, int j, int
     if (relevant) {
       const double a = ar[i];
       const double r = rho[i];
-      const double lo = L - r, hi = U - r;
+      const double lo = L - r, hi = U_ - r;
       const double v1 = wlo * a, v2 = whi * a;
       const int g1 = v1 < lo ? 0 : (v1 > hi ? 2 : 1);
       const int g2 = v2 < lo ? 0 : (v2 > hi ? 2 : 1);
@@ -328,7 +378,7 @@ __device__ __noinline__ void pass_sweep_row_compact(const PassCtx& c, int j, int
         else if (g1 == 2) nC += a * hi;
         else nS += a * a;
       } else {
-        sweep_elem<KC>(a, r, y, cnt, L, U, R, S);
+        sweep_elem<KC>(a, r, y, cnt, L, U_, R, S);
       }
     }
     // rows other than j keep their items (partitioned problems)
@@ -340,6 +390,7 @@ __device__ __noinline__ void pass_sweep_row_compact(const PassCtx& c, int j, int
   }
   __syncwarp();
   if (lane == 0) c.list_cnt[warp] = kept;
+  sweep_finish<KC>(y, cnt, R, S);
   // CTA totals of this sweep's active sums and newly fixed sums
   double v[2 * KC + 2];
 #pragma unroll
@@ -476,6 +527,7 @@ __device__ __noinline__ void local_sweep_row(const PassCtx& c, int j, int b, int
   for (int k = 0; k < KC; ++k) { R[k] = 0.0; S[k] = 0.0; }
   for (int k = threadIdx.x; k < nit; k += BLOCK)
     if (c.it_row[k] == j) sweep_elem<KC>(c.it_a[k], c.it_r[k], y, cnt, L, U, R, S);
+  sweep_finish<KC>(y, cnt, R, S);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* sred = c.smem;
 #pragma unroll
