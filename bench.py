@@ -294,7 +294,8 @@ def run_ours(args, rank, world):
                    "near_ties": res.projection.near_ties},
         "achieved_hbm_gbs_step": b_alg / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
+                     "frac": achieved / peak, "peak_kind": peak_kind,
+                     "traffic": measured_traffic(p.name, world),
                      "kernel": ("k_step (persistent: every pass of the step in one launch)"
                                 if kern["launches"] <= min(args.steps, 10) else "k_pass"),
                      "alg_bytes_per_var": BYTES_PER_VAR.get(args.config, 64),
@@ -307,6 +308,20 @@ def run_ours(args, rank, world):
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
+
+
+def measured_traffic(workload, world):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed `ncu --set full` capture (profiles/traffic.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+    except (OSError, ValueError):
+        return None
+    if t.get("workload") != workload or world != 1:
+        return None
+    return t.get("bytes_per_launch")
 
 
 def ctx_kernel_stats(ctx):

@@ -37,9 +37,13 @@ constexpr double kUnit = 1.1102230246251565e-16;  // 2^-53
 __device__ unsigned long long* g_ctl_marks = nullptr;
 __host__ __device__ __forceinline__ void ctl_mark(int k) {
 #if defined(__CUDA_ARCH__)
-  if (g_ctl_marks) {
+  if (g_ctl_marks && blockIdx.x == 0) {
     unsigned long long t;
+#if defined(TOPT_CTL_MARK_CLOCK)
+    t = clock64();
+#else
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+#endif
     g_ctl_marks[k] = t;
   }
 #else
@@ -255,6 +259,7 @@ TOPT_HD double approx_ncdf_upper(double t) {  // ~ P(Z > t), monotone, in (0, 1)
 struct RootEst {
   int kind;        // 0: gaussian(ye, sig) ; 1: log-uniform prior below 0 ; 2: above 0
   double ye, sig, L, inv_sig;
+  double sl, E;    // slope scale near the root (0 if unknown) and the walk's bound
 };
 
 TOPT_HD RootEst walk_estimate_(const Walk& w);
@@ -266,6 +271,10 @@ TOPT_NOINLINE RootEst walk_estimate(const Walk& w) {
 TOPT_HD RootEst walk_estimate_(const Walk& w) {
   RootEst e;
   e.kind = 0; e.ye = 0.0; e.sig = 1.0; e.L = 0.0; e.inv_sig = 1.0;
+  e.sl = dmax_(w.hasA ? w.Sa : 0.0, w.hasB ? w.Sb : 0.0);
+  e.E = w.E;
+  // the PREP sketch, while it lies in the walk interval
+  const bool hint = w.hok && w.hy >= w.lo && w.hy <= w.hi && w.hs > 0.0;
   if (w.hasA && w.hasB && w.ya < w.yb) {
     const double ya = w.ya, yb = w.yb;
     double sec = ya - w.Ra * (yb - ya) / (w.Rb - w.Ra);
@@ -284,8 +293,10 @@ TOPT_HD RootEst walk_estimate_(const Walk& w) {
     sig = dmax_(sig, fabs(sec) * 1e-15);
     e.ye = sec;
     e.sig = dmax_(sig, 1e-300);
+    if (hint && w.hy > ya && w.hy < yb && w.hs < e.sig) { e.ye = w.hy; e.sig = w.hs; }
     return e;
   }
+  if (hint) { e.ye = w.hy; e.sig = w.hs; return e; }
   if (!w.up) {  // root in [bp_lo, 0], r(0) > 0 known
     if (w.hasB && w.Sb > 0.0) {
       e.ye = dmax_(w.yb - w.Rb / w.Sb, w.lo);
@@ -306,6 +317,12 @@ TOPT_HD RootEst walk_estimate_(const Walk& w) {
   return e;
 }
 
+TOPT_HDN inline bool est_certain(const RootEst& e, double y) {
+  const double d = fabs(y - e.ye);
+  // 6 sigma away, and far enough that |r| there should clear the bound E
+  return e.kind == 0 && d * e.inv_sig >= 6.0 && (!(e.sl > 0.0) || d * e.sl >= 16.0 * e.E);
+}
+
 // Probability that the root lies above y.
 TOPT_HDN inline double est_p_above(const RootEst& e, double y) {
   if (e.kind == 0) return approx_ncdf_upper((y - e.ye) * e.inv_sig);
@@ -316,12 +333,31 @@ TOPT_HDN inline double est_p_above(const RootEst& e, double y) {
   return e.kind == 1 ? p : 1.0 - p;
 }
 
+// The part of the walk interval where evaluations can still matter: midpoints
+// outside the certified bounds (yL, yH) are decided without evaluation.  Every
+// candidate of a sweep lies in this window, so it also bounds the compacted
+// sweeps (elements of constant clip region over it are folded).
+TOPT_HDN inline void walk_window(const Walk& w, double* clo, double* chi) {
+  double a = w.lo, b = w.hi;
+  if (w.feas_done) {   // before that, the infeasibility probe sits at an interval end
+    if (w.hasL && w.yL > a) a = w.yL;
+    if (w.hasH && w.yH < b) b = w.yH;
+  }
+  *clo = a; *chi = b;
+}
+
+// A level whose midpoint lies more than kCertainSig standard deviations from
+// a point estimate is predicted with near certainty (the ranking CDF above has
+// heavy tails on purpose and is not used for this).
+TOPT_HDN inline bool est_certain(const RootEst& e, double y);
+
 // Choose up to K midpoints of the walk's remaining decision tree to evaluate
 // next: the predicted path (most probable branch at every uncertain level),
 // plus first-level alternatives ("hedges") at its least certain levels,
 // ranked by the probability of being visited.  O(K + certain levels), all
 // state in registers.
 constexpr int MAX_HEDGE = 4;
+constexpr int kMaxPathLevels = 64;               // uncertain + certain levels walked
 // Predicted path (most probable branch at every uncertain level) plus the
 // MAX_HEDGE most probable first-level alternatives, merged by probability of
 // being visited.  Per-level work is a few register operations (the hedge
@@ -346,7 +382,16 @@ TOPT_HD int walk_candidates(const Walk& w, const ProjOptions& o, int K, double* 
   const bool hasL = w.hasL, hasH = w.hasH;
   const double yL = w.yL, yH = w.yH;
   const int Kp = K - n;
-  while (np < Kp && (hi - lo) > o.tol_b && it < o.binary_maxiter) {
+  // levels whose branch is near-certain are not evaluated themselves: one
+  // evaluation at the innermost of them per direction (cert_lo / cert_hi)
+  // certifies the whole run by monotonicity.
+  double cert_lo = 0.0, cert_hi = 0.0;
+  bool has_cl = false, has_ch = false;
+  int lev = 0;
+  double clo, chi;
+  walk_window(w, &clo, &chi);
+  const int Kpath = Kp;
+  while (np < Kpath && lev < kMaxPathLevels && (hi - lo) > o.tol_b && it < o.binary_maxiter) {
     if (hasH && yH <= ym) {
       hi = ym;
     } else if (hasL && yL >= ym) {
@@ -354,26 +399,33 @@ TOPT_HD int walk_candidates(const Walk& w, const ProjOptions& o, int K, double* 
     } else {
       const double pa = est_p_above(e, ym);   // root above ym -> r(ym) <= 0 -> lo = ym
       const bool right = pa >= 0.5;
-      py[np] = ym;
-      pp[np] = p;
-      ++np;
-      const double palt = p * (right ? 1.0 - pa : pa);
-      if (palt > 1e-12 && palt > hpmin) {
+      ++lev;
+      if (lev > 1 && est_certain(e, ym)) {   // the walk's next midpoint is always taken
+        if (right) { cert_lo = ym; has_cl = true; } else { cert_hi = ym; has_ch = true; }
+      } else {
+        py[np] = ym;
+        pp[np] = p;
+        ++np;
+        const double palt = p * (right ? 1.0 - pa : pa);
         const double alt = right ? 0.5 * (lo + ym) : 0.5 * (ym + hi);
-        bool done = false;   // replace the first slot holding the minimum
+        if (palt > 1e-12 && palt > hpmin && alt > clo && alt < chi) {
+          bool done = false;   // replace the first slot holding the minimum
 #pragma unroll
-        for (int k = 0; k < MAX_HEDGE; ++k)
-          if (!done && hp[k] == hpmin) { hp[k] = palt; hy[k] = alt; done = true; }
-        hpmin = hp[0];
+          for (int k = 0; k < MAX_HEDGE; ++k)
+            if (!done && hp[k] == hpmin) { hp[k] = palt; hy[k] = alt; done = true; }
+          hpmin = hp[0];
 #pragma unroll
-        for (int k = 1; k < MAX_HEDGE; ++k) hpmin = dmin_(hpmin, hp[k]);
+          for (int k = 1; k < MAX_HEDGE; ++k) hpmin = dmin_(hpmin, hp[k]);
+        }
+        p = p * (right ? pa : 1.0 - pa);
       }
-      p = p * (right ? pa : 1.0 - pa);
       if (right) lo = ym; else hi = ym;
     }
     ym = 0.5 * (lo + hi);
     ++it;
   }
+  if (has_cl && n < K) out[n++] = cert_lo;
+  if (has_ch && n < K) out[n++] = cert_hi;
   ctl_mark(6);
   // merge (path nodes are ordered by decreasing probability; a hedge is
   // taken when more probable than the next path node -- its parent, being
@@ -505,10 +557,7 @@ TOPT_NOINLINE bool schedule_sweep(Plan& pl) {
   }
   for (int j = m; j <= MAX_M; ++j) c.row_start[j] = tot;
   c.compact = (pl.P.compact_cap > 0 && (m == 1 || pl.P.has_part)) ? 1 : 0;
-  for (int j = 0; j < m; ++j) {
-    c.wlo[j] = pl.w[j].lo;
-    c.whi[j] = pl.w[j].hi;
-  }
+  for (int j = 0; j < m; ++j) walk_window(pl.w[j], &c.wlo[j], &c.whi[j]);
   c.ncand = tot;
   // compacted global sweeps append one slot: the active elements left
   c.nslots = 2 * tot + ((c.compact && !c.local) ? 1 : 0);
@@ -748,6 +797,7 @@ TOPT_NOINLINE void consume_prep_core(Plan& pl, const double* t) {
     const double r0 = s[PS_S0] - ghat;
     walk_init(pl.w[j], P.is_eq[j], ghat, E, r0, s[PS_SLOPE0], s[PS_BPLO], s[PS_BPHI],
               s[PS_ANY], cnt);
+    if (pl.hint_ok[j]) { pl.w[j].hok = 1; pl.w[j].hy = pl.hint_y[j]; pl.w[j].hs = pl.hint_sig[j]; }
   }
   if (P.job == JOB_BUILD || P.job == JOB_DIRECTION) { set_error(pl, ST_OK); return; }
   if (m < 1) { set_error(pl, ST_DOMAIN); return; }
@@ -936,7 +986,9 @@ __device__ int walk_candidates_warp(const Walk& w, const ProjOptions& o, int K, 
   if (lane == 0) {
     int n0 = 0;
     if (!w.feas_done) out[n0++] = w.up ? w.bp_hi : w.bp_lo;
+    ctl_mark(2);
     const RootEst e = walk_estimate(w);
+    ctl_mark(3);
     // direction threshold: right (lo = ym) iff p_above(ym) >= 0.5
     const double L2 = e.L - 33.0;
     int np = 0;
@@ -965,6 +1017,7 @@ __device__ int walk_candidates_warp(const Walk& w, const ProjOptions& o, int K, 
     wp.np = np;
     wp.n0 = n0;
     wp.e = e;
+    ctl_mark(4);
   }
   __syncwarp();
   const int np = wp.np, n0 = wp.n0;
@@ -1001,6 +1054,7 @@ __device__ int walk_candidates_warp(const Walk& w, const ProjOptions& o, int K, 
       rh += (hs > hp || (hs == hp && s < lane)) ? 1 : 0;
     }
   }
+  if (lane == 0) ctl_mark(5);
   const int room = K - n0;
   if (lane < np && rp < room) out[n0 + rp] = ym;
   if (lane < np && hp > 0.0 && rh < room) out[n0 + rh] = alt;
@@ -1024,7 +1078,7 @@ __device__ bool schedule_sweep_warp(Plan& pl, WarpPath& wp) {
   for (int j = 0; j < m; ++j) {
     if (lane == 0) c.row_start[j] = tot;
     if (pl.w[j].status == WK_NEED) {
-      const Walk w = pl.w[j];
+      const Walk& w = pl.w[j];   // shared memory (a copy would live in local memory)
       const int nc = walk_candidates_warp(w, pl.P.opt, per, c.cand_y + tot, wp);
       // ascending order for the sweeps (rank sort, ties by index)
       double* cy = c.cand_y + tot;
@@ -1116,6 +1170,7 @@ __device__ void consume_sweep_warp(Plan& pl, const double* t) {
       const double y = __shfl_sync(0xffffffffu, cy, src);
       if (!w.hasH || y < w.yH) { w.hasH = 1; w.yH = y; }
     }
+    if (lane == 0) ctl_mark(0);
     // replay (every lane runs the same loop; lookups are ballots)
     if (w.status == WK_NEED) {
       const bool hasL = w.hasL, hasH = w.hasH;
@@ -1184,6 +1239,7 @@ __device__ void consume_sweep_warp(Plan& pl, const double* t) {
   __shared__ WarpPath s_wp;
   __shared__ int s_act;
   if (lane == 0) {
+    ctl_mark(1);
     if (was_global_compact) pl.res.active = t[2 * c.ncand];
     pl.res.passes++;
     int need = 0;
@@ -1199,8 +1255,10 @@ __device__ void consume_sweep_warp(Plan& pl, const double* t) {
   __syncwarp();
   if (s_act) {
     const bool more = schedule_sweep_warp(pl, s_wp);
+    if (lane == 0) ctl_mark(6);
     if (lane == 0 && !more) after_walks(pl);
   }
+  if (lane == 0) ctl_mark(7);
   if (lane == 0 && pl.res.passes > 4096 && pl.cmd.phase != PH_DONE) set_error(pl, ST_INTERNAL);
   __syncwarp();
 }
@@ -1217,8 +1275,10 @@ __device__ void plan_consume_warp(Plan& pl, const double* t) {
   if (ph == PH_PREP || ph == PH_GATHER) {
     if (lane == 0) {
       pl.res.passes++;
+      ctl_mark(0);
       if (ph == PH_PREP) {
         consume_prep_core(pl, t);
+        ctl_mark(1);
       } else {
         pl.cmd.local = 1;
         pl.res.gathered = 1;
@@ -1229,8 +1289,10 @@ __device__ void plan_consume_warp(Plan& pl, const double* t) {
     __syncwarp();
     if (pl.cmd.phase == PH_SWEEP && pl.cmd.nslots == -1) {
       const bool more = schedule_sweep_warp(pl, s_wp2);
+      if (lane == 0) ctl_mark(6);
       if (lane == 0 && !more) after_walks(pl);
     }
+    if (lane == 0) ctl_mark(7);
     __syncwarp();
     return;
   }

@@ -39,19 +39,68 @@ __device__ __forceinline__ double warp_reduce(int op, double v) {
   return v;
 }
 
+__host__ __device__ constexpr int pow2_at_least(int n) { return n <= 1 ? 1 : 2 * pow2_at_least((n + 1) / 2); }
+
+// Warp stage of a many-slot reduction by recursive halving: at each of the 5
+// butterfly levels a lane keeps half of its slots and receives the partner's
+// copy of them, so NS slots cost ~NS shuffles instead of 5 NS.  Every lane
+// then writes the warp totals of the slots it ended with to wsum[slot]
+// (slots < NS only; a slot held by several lanes is written by the lowest).
+// The order of the additions is fixed, so results are deterministic.
+// MINMAX: some slots reduce with min/max (slot_op(phase, slot0 + slot)).
+template <int NS, bool MINMAX>
+__device__ __forceinline__ void warp_reduce_slots(const double (&v)[NS], int phase, int slot0,
+                                                  double* wsum) {
+  constexpr int P = pow2_at_least(NS);
+  const int lane = threadIdx.x & 31;
+  double a[NS];   // slots >= NS of the padded power-of-two layout are zeros
+#pragma unroll
+  for (int s = 0; s < NS; ++s) a[s] = v[s];
+  int base = 0;
+  bool writer = true;
+#pragma unroll
+  for (int lev = 0; lev < 5; ++lev) {
+    const int o = 16 >> lev;
+    const int c = (P >> lev) > 1 ? (P >> lev) : 1;   // values held before this level
+    const bool up = (lane & o) != 0;
+    if (c > 1) {
+      const int h = c / 2;
+#pragma unroll
+      for (int i = 0; i < h; ++i) {
+        if (i >= NS) break;
+        const double lo_v = a[i];
+        const double hi_v = (h + i < NS) ? a[h + i] : 0.0;
+        const double keep = up ? hi_v : lo_v;
+        const double send = up ? lo_v : hi_v;
+        const double recv = __shfl_xor_sync(0xffffffffu, send, o);
+        const int op = MINMAX ? slot_op(phase, slot0 + base + (up ? h : 0) + i) : 0;
+        // lower lane of the pair first: the same expression on both sides
+        a[i] = up ? apply_op(op, recv, keep) : apply_op(op, keep, recv);
+      }
+      if (up) base += h;
+    } else {
+      const double recv = __shfl_xor_sync(0xffffffffu, a[0], o);
+      const int op = MINMAX ? slot_op(phase, slot0 + base) : 0;
+      a[0] = up ? apply_op(op, recv, a[0]) : apply_op(op, a[0], recv);
+      if (up) writer = false;
+    }
+  }
+  constexpr int F = P >= 32 ? P / 32 : 1;
+  if (writer) {
+#pragma unroll
+    for (int i = 0; i < F && i < NS; ++i)
+      if (base + i < NS) wsum[base + i] = a[i];
+  }
+}
+
 // Reduce NS per-thread values (compile-time count) across the CTA and write
-// them to out[slot0 + s] for s < ns (ns <= NS, runtime).  One __syncthreads.
+// them to out[slot0 + s] for s < ns (ns <= NS, runtime).
 template <int NS>
 __device__ __forceinline__ void block_reduce_store(const double (&v)[NS], int ns, int phase,
                                                    int slot0, double* out, double* smem) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    if (s < ns) {
-      const double r = warp_reduce(slot_op(phase, slot0 + s), v[s]);
-      if (lane == 0) smem[warp * NS + s] = r;
-    }
-  }
+  const int warp = threadIdx.x >> 5;
+  if (phase == PH_PREP) warp_reduce_slots<NS, true>(v, phase, slot0, smem + warp * NS);
+  else warp_reduce_slots<NS, false>(v, phase, slot0, smem + warp * NS);
   __syncthreads();
   if (threadIdx.x < ns) {
     const int s = threadIdx.x;
@@ -283,10 +332,20 @@ __device__ __forceinline__ void sweep_elem(double a, double r, const double* y, 
     if (p1 + s <= cnt && y[p1 + s - 1] < bl) p1 += s;
     if (p2 + s <= cnt && y[p2 + s - 1] <= bh) p2 += s;
   }
+  // Predicated adds (two compares + three guarded DADDs per candidate) instead
+  // of selects of zero: same sums bit for bit (x + 0.0 == x for the
+  // accumulators, which start at +0.0), half the instructions.
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
-    C[k] += (k < p1) ? cl : ((k >= p2) ? ch : 0.0);
-    S[k] += (k >= p1 && k < p2) ? aa : 0.0;
+    asm("{\n\t.reg .pred pb, pa, pf;\n\t"
+        "setp.lt.s32 pb, %4, %5;\n\t"
+        "setp.ge.s32 pa, %4, %6;\n\t"
+        "or.pred pf, pb, pa;\n\t"
+        "@pb add.rn.f64 %0, %0, %2;\n\t"
+        "@pa add.rn.f64 %0, %0, %3;\n\t"
+        "@!pf add.rn.f64 %1, %1, %7;\n\t}"
+        : "+d"(C[k]), "+d"(S[k])
+        : "d"(cl), "d"(ch), "r"(k), "r"(p1), "r"(p2), "d"(aa));
   }
 }
 
@@ -398,11 +457,7 @@ __device__ __noinline__ void pass_sweep_row_compact(const PassCtx& c, int j, int
   v[2 * KC] = nC;
   v[2 * KC + 1] = nS;
   double* sred = c.smem;
-#pragma unroll
-  for (int s = 0; s < 2 * KC + 2; ++s) {
-    const double r = warp_reduce(0, v[s]);
-    if (lane == 0) sred[warp * (2 * KC + 2) + s] = r;
-  }
+  warp_reduce_slots<2 * KC + 2, false>(v, PH_SWEEP, 0, sred + warp * (2 * KC + 2));
   __syncthreads();
   double* tot = c.smem + NWARP * (2 * KC + 2);
   if (threadIdx.x < 2 * KC + 2) {
@@ -528,15 +583,13 @@ __device__ __noinline__ void local_sweep_row(const PassCtx& c, int j, int b, int
   for (int k = threadIdx.x; k < nit; k += BLOCK)
     if (c.it_row[k] == j) sweep_elem<KC>(c.it_a[k], c.it_r[k], y, cnt, L, U, R, S);
   sweep_finish<KC>(y, cnt, R, S);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5;
   double* sred = c.smem;
+  {
+    double v[2 * KC];
 #pragma unroll
-  for (int s = 0; s < KC; ++s) {
-    if (s < cnt) {
-      const double r0 = warp_reduce(0, R[s]);
-      const double r1 = warp_reduce(0, S[s]);
-      if (lane == 0) { sred[warp * 2 * KC + 2 * s] = r0; sred[warp * 2 * KC + 2 * s + 1] = r1; }
-    }
+    for (int k = 0; k < KC; ++k) { v[2 * k] = R[k]; v[2 * k + 1] = S[k]; }
+    warp_reduce_slots<2 * KC, false>(v, PH_SWEEP, 0, sred + warp * 2 * KC);
   }
   __syncthreads();
   if (threadIdx.x < 2 * cnt) {

@@ -93,6 +93,8 @@ struct Walk {
   int32_t hasL, hasH, hasA, hasB;
   double yL, yH;                    // certified: R(yL) < -E, R(yH) > E
   double ya, Ra, Sa, yb, Rb, Sb;    // nearest evaluated points with R<=0 / R>0
+  double hy, hs;                    // root estimate from the PREP sketch (if hok)
+  int32_t hok, pad2_;
 };
 
 struct Newton {
@@ -194,6 +196,9 @@ struct Plan {
   Newton nt;
   Result res;
   int32_t feas_map[MAX_M];
+  // root sketch from the PREP pass (candidate choice only, never a decision)
+  double hint_y[MAX_M], hint_sig[MAX_M];
+  int32_t hint_ok[MAX_M];
   Scratch sc;
 };
 

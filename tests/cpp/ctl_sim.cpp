@@ -54,6 +54,20 @@ int sim_phase(const Plan* pl) { return pl->cmd.phase; }
 int sim_nslots(const Plan* pl) { return pl->cmd.nslots; }
 int sim_slot_op(const Plan* pl, int s) { return slot_op(pl->cmd.phase, s); }
 void sim_consume(Plan* pl, const double* totals) { plan_consume(*pl, totals); }
+void sim_set_hint(Plan* pl, int j, double y, double sig) {
+  pl->hint_y[j] = y; pl->hint_sig[j] = sig; pl->hint_ok[j] = 1;
+}
+// walk j state: lo hi ym yL yH (nan if absent) iters status; candidates of the next sweep
+void sim_walk(const Plan* pl, int j, double* w, double* cand, int* ncand) {
+  const Walk& k = pl->w[j];
+  const double nan = 0.0 / 0.0;
+  w[0] = k.lo; w[1] = k.hi; w[2] = k.ym; w[3] = k.hasL ? k.yL : nan; w[4] = k.hasH ? k.yH : nan;
+  w[5] = k.iters; w[6] = k.status; w[7] = k.E; w[8] = k.n_direct;
+  w[9] = pl->cmd.wlo[j]; w[10] = pl->cmd.whi[j];
+  const int b = pl->cmd.row_start[j], e = pl->cmd.row_start[j + 1];
+  *ncand = (pl->cmd.phase == PH_SWEEP) ? e - b : 0;
+  for (int q = 0; q < *ncand; ++q) cand[q] = pl->cmd.cand_y[b + q];
+}
 
 void sim_result(const Plan* pl, int32_t* ints /* status path newton_iters converged curv passes sweeps stage1 near_ties fallback */,
                 double* dbl /* residual alpha beta min_margin */, double* y, double* ghat) {

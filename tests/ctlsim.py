@@ -30,6 +30,8 @@ def lib():
         _lib.sim_nslots.argtypes = [vp]
         _lib.sim_slot_op.argtypes = [vp, i32]
         _lib.sim_result.argtypes = [vp, vp, vp, vp, vp]
+        _lib.sim_walk.argtypes = [vp, i32, vp, vp, vp]
+        _lib.sim_set_hint.argtypes = [vp, i32, d, d]
     return _lib
 
 
@@ -89,6 +91,11 @@ class Rank:
             t = np.zeros(1)
         lib().sim_consume(self.plan, _p(t))
 
+    def walk(self, j):
+        w = np.zeros(11); cand = np.zeros(64); nc = C.c_int(0)
+        lib().sim_walk(self.plan, j, _p(w), _p(cand), C.byref(nc))
+        return w, cand[:nc.value]
+
     def result(self, m):
         iv = np.zeros(10, np.int32); dv = np.zeros(4); y = np.zeros(m); gh = np.zeros(m)
         lib().sim_result(self.plan, _p(iv), _p(dv), _p(y), _p(gh))
@@ -112,10 +119,30 @@ def bounds(n, R):
     return [(r * n // R, (r + 1) * n // R) for r in range(R)]
 
 
-def run(prob, R=1, job=JOB_PGD_STEP, rho=None, gd=None, ghat=None, max_passes=4096):
+def run(prob, R=1, job=JOB_PGD_STEP, rho=None, gd=None, ghat=None, max_passes=4096,
+        verbose=False, hints=None):
     ranks = [Rank(prob, lo, hi, job, rho, gd, ghat) for lo, hi in bounds(prob.n, R)]
+    for j, h in enumerate(hints or []):
+        if h is not None:
+            for rk in ranks:
+                lib().sim_set_hint(rk.plan, j, h[0], h[1])
     passes = 0
     while ranks[0].phase() != PH_DONE and passes < max_passes:
+        if verbose:
+            for j in range(prob.m):
+                w, cand = ranks[0].walk(j)
+                print(f"  pass {passes} phase {ranks[0].phase()} row {j}: lo {w[0]:.6g} hi {w[1]:.6g} "
+                      f"ym {w[2]:.6g} yL {w[3]:.6g} yH {w[4]:.6g} it {int(w[5])} st {int(w[6])} "
+                      f"direct {int(w[8])} E {w[7]:.3g}")
+                if len(cand):
+                    rk = ranks[0]
+                    a = rk.grad[j]; lo_ = prob.lower - rk.rho; hi_ = prob.upper - rk.rho
+                    def cls(y):
+                        v = y * a
+                        return np.where(v < lo_, 0, np.where(v > hi_, 2, 1))
+                    act = int(np.count_nonzero((cls(w[9]) != cls(w[10])) & (a != 0)))
+                    print(f"     window [{w[9]:.9g}, {w[10]:.9g}] active {act}")
+                    print("     cand", " ".join(f"{c:.9g}" for c in cand))
         parts = [rk.partials() for rk in ranks]
         ops = ranks[0].ops(len(parts[0]))
         tot = combine(parts, ops)

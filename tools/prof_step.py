@@ -61,12 +61,8 @@ def trace(config="C2", seed=2):
               f"b0-end {1e-3*(t[k,1]-t[k,0]):7.2f} last-end {1e-3*(t[k,6]-t[k,0]):7.2f} "
               f"fin-start {1e-3*(t[k,2]-t[k,0]):7.2f} reduce {1e-3*(t[k,3]-t[k,2]):6.2f} "
               f"control {1e-3*(t[k,4]-t[k,3]):6.2f}" +
-              (f" | ctl marks add {1e-3*(mk[k,1]-mk[k,0]):6.2f} adv {1e-3*(mk[k,2]-mk[k,1]):6.2f}"
-               f" sched {1e-3*(mk[k,3]-mk[k,2]):6.2f} pre {1e-3*(mk[k,0]-t[k,3]):6.2f}"
-               f" [copy {1e-3*(mk[k,4]-mk[k,2]):5.2f} est {1e-3*(mk[k,5]-mk[k,4]):5.2f}"
-               f" path {1e-3*(mk[k,6]-mk[k,5]):5.2f} merge {1e-3*(mk[k,7]-mk[k,6]):5.2f}"
-               f" tail {1e-3*(mk[k,3]-mk[k,7]):5.2f}]"
-               if mk[k, 0] else ""))
+              (" | marks " + " ".join(f"{k2}:{1e-3*(mk[k,k2]-t[k,3]):6.2f}" for k2 in range(8) if mk[k,k2])
+               if mk[k].any() else ""))
 
 
 if __name__ == "__main__":
