@@ -8,6 +8,7 @@
 // relaunches and polls one int (the next phase); no partial sum or decision
 // ever crosses PCIe.
 #include <cooperative_groups.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -134,6 +135,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass(Plan* plan, double* partials,
   c.list_cnt = nullptr;
   c.fixC = c.fixS = nullptr;
   c.list_cap = 0;
+  c.timed_out = nullptr;   // never streamed
   run_pass(c);
   __threadfence();
   __syncthreads();
@@ -191,7 +193,17 @@ struct GatherBufs {
   double* g_r;
   int* g_row;
   double* g_fix;
+  int* timed_out;   // streamed input never arrived (host checks after the launch)
 };
+
+// d is final once PREP's grid barrier has passed: release it to the copy
+// stream waiting on out_flag (system scope: a copy engine reads it).
+__device__ __forceinline__ void signal_out(const Problem& P) {
+  if (P.chunk > 0 && P.out_flag) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(P.out_flag), "r"(P.epoch) : "memory");
+  }
+}
 
 __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
                                                    unsigned long long* trace, GatherBufs gb) {
@@ -240,6 +252,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     c.it_r = c.it_a + GATHER_CAP;
     c.it_row = reinterpret_cast<int8_t*>(c.it_r + GATHER_CAP);
     c.n_items = &s_nitems;
+    c.timed_out = gb.timed_out;
     if (sp.cmd.phase == PH_SWEEP && sp.cmd.local) {   // CTA-local sweep: no barrier
       local_sweep(c, s_tot);
       if (threadIdx.x < 32) plan_consume_warp(sp, s_tot);
@@ -254,6 +267,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     __threadfence();
     grid.sync();
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[2] = gtimer();
+    if (sp.cmd.phase == PH_PREP && blockIdx.x == 0 && threadIdx.x == 0) signal_out(sp.P);
     if (sp.cmd.phase == PH_GATHER) gather_load(c, nb);
     finish_reduce(part, nb, sp.cmd.nslots, sp.cmd.phase, s_tot, s_red);
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -264,6 +278,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     __syncthreads();
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) { tr[4] = gtimer(); g_ctl_marks = nullptr; }
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) signal_out(sp.P);   // also on early exits
   if (blockIdx.x == 0) {  // publish the final state (results) once
     int* gp = reinterpret_cast<int*>(plan);
     const int* spi = reinterpret_cast<const int*>(&sp);
@@ -302,6 +317,35 @@ struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
 };
+
+constexpr int MAX_STREAM_CHUNKS = 32;
+
+// Driver stream memory operations (flag write / wait on a copy stream),
+// resolved through the runtime so no -lcuda link is needed.
+struct MemOps {
+  bool ok = false;
+  CUresult (*write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+  CUresult (*wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+};
+MemOps& memops() {
+  static MemOps m;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* w = nullptr;
+    void* v = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWaitValue32", &v, cudaEnableDefault, &q2) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && w && v) {
+      m.write32 = (decltype(m.write32))w;
+      m.wait32 = (decltype(m.wait32))v;
+      m.ok = true;
+    }
+    cudaGetLastError();
+  }
+  return m;
+}
 
 }  // namespace
 
@@ -343,6 +387,14 @@ struct topt_b200_ctx {
   double* d_gathered = nullptr;  // [world][PMAX]
   int64_t n_global_override = 0;
   const int64_t* row_counts_override = nullptr;
+  // host-buffer streaming (copies overlap the step's first passes)
+  cudaStream_t cstream = nullptr;  // copy stream
+  cudaEvent_t ev_copy = nullptr;
+  unsigned* d_flags = nullptr;     // [2 * MAX_STREAM_CHUNKS] in, [2 * MAX_STREAM_CHUNKS] out
+  int* d_timed_out = nullptr;
+  int* h_timed_out = nullptr;      // pinned
+  uint32_t epoch = 0;
+  int stream_inputs = 1;           // TOPT_B200_STREAM=0 disables
 };
 
 // ---- NCCL, resolved at run time (the process may already hold torch's copy)
@@ -431,7 +483,57 @@ const char* status_msg(int st) {
 // Run a plan to completion on the device.  hp.P must be filled.
 int run_plan_ranks(topt_b200_ctx* ctx, Plan& hp);
 
-int run_plan(topt_b200_ctx* ctx, Plan& hp) {
+// Host-side half of the input streaming: the host arrays of one PGD step and
+// where they go.  Issued on the copy stream right after the kernel launch.
+struct StreamIn {
+  const double *x, *xp, *g, *gp, *dp, *grad;   // host
+  double *dx, *dxp, *dg, *dgp, *ddp, *dgrad;   // device
+  int m;
+  double* d_host;                              // optional: d out (device->host after PREP)
+  const double* d_dev;
+};
+
+int issue_stream(topt_b200_ctx* ctx, const Plan& hp, const StreamIn& si) {
+  const Problem& P = hp.P;
+  MemOps& mo = memops();
+  const int64_t n = P.n, ch = P.chunk;
+  const int nch = P.nchunk;
+  const CUstream cs = (CUstream)ctx->cstream;
+  auto put = [&](double* dst, const double* src, int64_t lo, int64_t cnt) -> int {
+    CUDA_TRY(ctx, cudaMemcpyAsync(dst + lo, src + lo, sizeof(double) * (size_t)cnt,
+                                  cudaMemcpyHostToDevice, ctx->cstream));
+    return TOPT_OK;
+  };
+  int rc;
+  for (int k = 0; k < nch; ++k) {   // group A: what the BB / PR+ pass reads
+    const int64_t lo = (int64_t)k * ch, cnt = std::min<int64_t>(ch, n - lo);
+    if ((rc = put(si.dx, si.x, lo, cnt)) || (rc = put(si.dxp, si.xp, lo, cnt)) ||
+        (rc = put(si.dg, si.g, lo, cnt)) || (rc = put(si.dgp, si.gp, lo, cnt)))
+      return rc;
+    if (mo.write32(cs, (CUdeviceptr)(ctx->d_flags + k), P.epoch, 0) != CUDA_SUCCESS)
+      return fail(ctx, TOPT_ERR_CUDA, "cuStreamWriteValue32 failed");
+  }
+  for (int k = 0; k < nch; ++k) {   // group B: d_prev and the constraint rows
+    const int64_t lo = (int64_t)k * ch, cnt = std::min<int64_t>(ch, n - lo);
+    if ((rc = put(si.ddp, si.dp, lo, cnt))) return rc;
+    for (int j = 0; j < si.m; ++j)
+      if ((rc = put(si.dgrad + (int64_t)j * n, si.grad + (int64_t)j * n, lo, cnt))) return rc;
+    if (mo.write32(cs, (CUdeviceptr)(ctx->d_flags + nch + k), P.epoch, 0) != CUDA_SUCCESS)
+      return fail(ctx, TOPT_ERR_CUDA, "cuStreamWriteValue32 failed");
+  }
+  if (si.d_host && n > 0) {   // d is final after PREP: copy it while the bisection runs
+    if (mo.wait32(cs, (CUdeviceptr)(ctx->d_flags + 2 * MAX_STREAM_CHUNKS), P.epoch,
+                  CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      return fail(ctx, TOPT_ERR_CUDA, "cuStreamWaitValue32 failed");
+    CUDA_TRY(ctx, cudaMemcpyAsync(si.d_host, si.d_dev, sizeof(double) * (size_t)n,
+                                  cudaMemcpyDeviceToHost, ctx->cstream));
+  }
+  CUDA_TRY(ctx, cudaEventRecord(ctx->ev_copy, ctx->cstream));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_copy, 0));
+  return TOPT_OK;
+}
+
+int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
   if (ctx->comm) return run_plan_ranks(ctx, hp);
   const bool persistent = ctx->persistent && ctx->coop_grid > 0;
   const int grid = persistent ? ctx->coop_grid : ctx->grid;
@@ -455,15 +557,25 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp) {
   if (persistent && phase != PH_DONE) {
     unsigned long long* tr = ctx->trace_on ? ctx->d_trace : nullptr;
     if (tr) cudaMemsetAsync(tr, 0, 128 * 8 * sizeof(unsigned long long), ctx->stream);
-    GatherBufs gb{ctx->d_blk_cnt, ctx->d_ga, ctx->d_gr, ctx->d_grow, ctx->d_gfix};
+    GatherBufs gb{ctx->d_blk_cnt, ctx->d_ga, ctx->d_gr, ctx->d_grow, ctx->d_gfix,
+                  ctx->d_timed_out};
     void* args[] = {&ctx->d_plan, &ctx->d_part, &tr, &gb};
+    if (si) CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_timed_out, 0, sizeof(int), ctx->stream));
     if (ctx->profile) cudaEventRecord(ctx->ev0, ctx->stream);
     CUDA_TRY(ctx, cudaLaunchCooperativeKernel((void*)k_step, grid, BLOCK, args, dyn_smem,
                                               ctx->stream));
     ctx->launches++;
     if (ctx->profile) cudaEventRecord(ctx->ev1, ctx->stream);
+    if (si) {
+      const int rc = issue_stream(ctx, hp, *si);
+      if (rc) { cudaStreamSynchronize(ctx->stream); return rc; }
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_timed_out, ctx->d_timed_out, sizeof(int),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+    }
     CUDA_TRY(ctx, cudaMemcpyAsync(&hp, ctx->d_plan, sizeof(Plan), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (si && *ctx->h_timed_out)
+      return fail(ctx, TOPT_ERR_CUDA, "topt_b200: a streamed input chunk never arrived");
     if (ctx->profile) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
@@ -709,6 +821,13 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   }
   ok = ok && cudaEventCreate(&ctx->ev0) == cudaSuccess;
   ok = ok && cudaEventCreate(&ctx->ev1) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking) == cudaSuccess;
+  ok = ok && cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_flags, sizeof(unsigned) * 4 * MAX_STREAM_CHUNKS) == cudaSuccess;
+  ok = ok && cudaMemset(ctx->d_flags, 0, sizeof(unsigned) * 4 * MAX_STREAM_CHUNKS) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_timed_out, sizeof(int)) == cudaSuccess;
+  ok = ok && cudaMallocHost(&ctx->h_timed_out, sizeof(int)) == cudaSuccess;
+  if (const char* e = getenv("TOPT_B200_STREAM")) ctx->stream_inputs = atoi(e);
   if (!ok) { topt_b200_ctx_destroy(ctx); return TOPT_ERR_CUDA; }
   *out = ctx;
   return TOPT_OK;
@@ -735,6 +854,12 @@ void topt_b200_ctx_destroy(topt_b200_ctx* ctx) {
   cudaFree(ctx->d_grow);
   cudaFree(ctx->d_gfix);
   if (ctx->h_phase) cudaFreeHost(ctx->h_phase);
+  if (ctx->cstream) cudaStreamSynchronize(ctx->cstream);
+  cudaFree(ctx->d_flags);
+  cudaFree(ctx->d_timed_out);
+  if (ctx->h_timed_out) cudaFreeHost(ctx->h_timed_out);
+  if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
+  if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1017,7 +1142,7 @@ int topt_b200_project_dev(topt_b200_ctx* ctx, int which, const double* rho_tilde
 static int pgd_step_impl(topt_b200_ctx* ctx, Plan& hp, const topt_step_problem* prob,
                          const topt_pgd_settings* s, const topt_proj_options* opts,
                          topt_proj_meta* meta, double* y, double* slacks, double* ghat,
-                         int job = JOB_PGD_STEP) {
+                         int job = JOB_PGD_STEP, const StreamIn* si = nullptr) {
   Problem& P = hp.P;
   P.job = job;
   P.which = W_AUTO;
@@ -1039,7 +1164,7 @@ static int pgd_step_impl(topt_b200_ctx* ctx, Plan& hp, const topt_step_problem* 
     if (prob->part_offsets)
       P.row_count[j] = (double)(prob->part_offsets[j + 1] - prob->part_offsets[j]);
   }
-  int rc = run_plan(ctx, hp);
+  int rc = run_plan(ctx, hp, si);
   if (rc) return rc;
   for (int j = 0; j < P.m; ++j) {
     if (y) y[j] = hp.res.y[j];
@@ -1099,12 +1224,26 @@ int topt_b200_pgd_step(topt_b200_ctx* ctx, const topt_step_problem* prob,
   if (rc) return rc;
   const size_t nb = sizeof(double) * (size_t)std::max<int64_t>(n, 1);
   void *dx, *dxp, *dg, *dgp, *ddp, *dgrad;
-  if ((rc = upload(ctx, B_X, prob->x, nb, &dx))) return rc;
-  if ((rc = upload(ctx, B_XP, prob->x_prev, nb, &dxp))) return rc;
-  if ((rc = upload(ctx, B_G, prob->g, nb, &dg))) return rc;
-  if ((rc = upload(ctx, B_GP, prob->g_prev, nb, &dgp))) return rc;
-  if ((rc = upload(ctx, B_DP, prob->d_prev, nb, &ddp))) return rc;
-  if ((rc = upload(ctx, B_GRAD, prob->grad, nb * (size_t)m, &dgrad))) return rc;
+  // Stream the inputs into the running kernel (copies overlap the BB/PR+ and
+  // PREP passes) when the persistent path and the stream memory operations
+  // are available; otherwise upload first.
+  const bool streamed = ctx->stream_inputs && !ctx->comm && ctx->persistent &&
+                        ctx->coop_grid > 0 && n > 0 && m >= 1 && memops().ok &&
+                        prob->x && prob->x_prev && prob->g && prob->g_prev && prob->d_prev &&
+                        prob->grad;
+  if (streamed) {
+    dx = buf(ctx, B_X, nb); dxp = buf(ctx, B_XP, nb); dg = buf(ctx, B_G, nb);
+    dgp = buf(ctx, B_GP, nb); ddp = buf(ctx, B_DP, nb); dgrad = buf(ctx, B_GRAD, nb * (size_t)m);
+    if (!dx || !dxp || !dg || !dgp || !ddp || !dgrad)
+      return fail(ctx, TOPT_ERR_CUDA, "cudaMalloc failed");
+  } else {
+    if ((rc = upload(ctx, B_X, prob->x, nb, &dx))) return rc;
+    if ((rc = upload(ctx, B_XP, prob->x_prev, nb, &dxp))) return rc;
+    if ((rc = upload(ctx, B_G, prob->g, nb, &dg))) return rc;
+    if ((rc = upload(ctx, B_GP, prob->g_prev, nb, &dgp))) return rc;
+    if ((rc = upload(ctx, B_DP, prob->d_prev, nb, &ddp))) return rc;
+    if ((rc = upload(ctx, B_GRAD, prob->grad, nb * (size_t)m, &dgrad))) return rc;
+  }
   Problem& P = hp.P;
   P.x = (const double*)dx; P.x_prev = (const double*)dxp; P.g = (const double*)dg;
   P.g_prev = (const double*)dgp; P.d_prev = (const double*)ddp; P.grad = (const double*)dgrad;
@@ -1121,12 +1260,26 @@ int topt_b200_pgd_step(topt_b200_ctx* ctx, const topt_step_problem* prob,
   P.delta_out = out->delta ? (double*)buf(ctx, B_DELTA, nb) : nullptr;
   P.mask_out = out->mask ? (uint8_t*)buf(ctx, B_MASK, (size_t)std::max<int64_t>(n, 1)) : nullptr;
   if (!P.rho || !P.d_out || !P.x_out) return fail(ctx, TOPT_ERR_CUDA, "cudaMalloc failed");
-  rc = pgd_step_impl(ctx, hp, prob, settings, opts, meta, out->y, out->slacks, out->g_hat);
+  StreamIn si{};
+  if (streamed) {
+    int64_t nch = (n + (1 << 18) - 1) >> 18;   // ~2 MB per array per chunk
+    nch = std::max<int64_t>(1, std::min<int64_t>(nch, MAX_STREAM_CHUNKS));
+    P.chunk = (n + nch - 1) / nch;
+    P.nchunk = (int32_t)((n + P.chunk - 1) / P.chunk);
+    P.epoch = ++ctx->epoch;
+    P.in_flags = ctx->d_flags;
+    P.out_flag = ctx->d_flags + 2 * MAX_STREAM_CHUNKS;
+    si = StreamIn{prob->x, prob->x_prev, prob->g, prob->g_prev, prob->d_prev, prob->grad,
+                  (double*)dx, (double*)dxp, (double*)dg, (double*)dgp, (double*)ddp,
+                  (double*)dgrad, m, out->d, P.d_out};
+  }
+  rc = pgd_step_impl(ctx, hp, prob, settings, opts, meta, out->y, out->slacks, out->g_hat,
+                     JOB_PGD_STEP, streamed ? &si : nullptr);
   if (rc) return rc;
   const size_t nbytes = sizeof(double) * (size_t)n;
   if (n > 0) {
     if (out->x_new) CUDA_TRY(ctx, cudaMemcpyAsync(out->x_new, P.x_out, nbytes, cudaMemcpyDeviceToHost, ctx->stream));
-    if (out->d) CUDA_TRY(ctx, cudaMemcpyAsync(out->d, P.d_out, nbytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (out->d && !streamed) CUDA_TRY(ctx, cudaMemcpyAsync(out->d, P.d_out, nbytes, cudaMemcpyDeviceToHost, ctx->stream));
     if (out->rho_tilde) CUDA_TRY(ctx, cudaMemcpyAsync(out->rho_tilde, P.rho, nbytes, cudaMemcpyDeviceToHost, ctx->stream));
     if (out->delta) CUDA_TRY(ctx, cudaMemcpyAsync(out->delta, P.delta_out, nbytes, cudaMemcpyDeviceToHost, ctx->stream));
     if (out->mask) CUDA_TRY(ctx, cudaMemcpyAsync(out->mask, P.mask_out, (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));

@@ -135,6 +135,7 @@ struct PassCtx {
   double* it_r;
   int8_t* it_row;
   int* n_items;        // shared scalar
+  int* timed_out;      // global flag: a streamed input chunk never arrived
 };
 
 // Fill each warp's active list with all of its grid-stride elements (this
@@ -159,29 +160,75 @@ __device__ void compact_init(const PassCtx& c) {
   __syncthreads();
 }
 
+// ---- host-buffer streaming: wait for an input chunk ------------------------
+// One thread per CTA polls the flag the copy stream writes after the chunk's
+// copies (stream-ordered, so the data is in memory once the flag is seen);
+// the CTA then reads the chunk through L2 (it never touched it before).  A
+// copy that never lands stops the wait after ~4 s with *err set, so a broken
+// stream cannot hang the GPU.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __noinline__ void wait_chunk(const unsigned* flag, unsigned epoch, int* timed_out) {
+  if (threadIdx.x == 0) {
+    if ((int)(ld_acquire_u32(flag) - epoch) < 0) {
+      const unsigned long long t0 = global_ns();
+      while ((int)(ld_acquire_u32(flag) - epoch) < 0) {
+        __nanosleep(256);
+        if (global_ns() - t0 > 4000000000ull) { *timed_out = 1; break; }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Element range [lo, hi) of chunk k (the whole slab when not streaming).
+struct ChunkRange {
+  int64_t lo, hi;
+};
+__device__ __forceinline__ int num_chunks(const Problem& P) { return P.chunk > 0 ? P.nchunk : 1; }
+__device__ __forceinline__ ChunkRange chunk_range(const Problem& P, int k) {
+  if (P.chunk <= 0) return {0, P.n};
+  const int64_t lo = (int64_t)k * P.chunk;
+  return {lo, lo + P.chunk < P.n ? lo + P.chunk : P.n};
+}
+
 // ---- PH_STEP_REDUCE: BB / PR+ sums --------------------
 __device__ __noinline__ void pass_step_reduce(const PassCtx& c) {
   const Problem& P = c.plan->P;
-  const int64_t n = P.n, st = c.stride;
+  const int64_t st = c.stride;
   const double* __restrict__ x = P.x;
   const double* __restrict__ xp = P.x_prev;
   const double* __restrict__ g = P.g;
   const double* __restrict__ gp = P.g_prev;
   double v[6] = {0, 0, 0, 0, 0, 0};
-  int64_t i = c.i0;
-  for (; i + st < n; i += 2 * st) {   // two independent elements in flight
-    const double x0 = x[i], q0 = xp[i], g0 = g[i], h0 = gp[i];
-    const double x1 = x[i + st], q1 = xp[i + st], g1 = g[i + st], h1 = gp[i + st];
-    const double s0 = x0 - q0, y0 = g0 - h0, s1 = x1 - q1, y1 = g1 - h1;
-    v[0] += s0 * s0; v[1] += s0 * y0; v[2] += y0 * y0; v[3] += g0 * y0; v[4] += h0 * h0;
-    v[5] = dmax_(v[5], fabs(g0));
-    v[0] += s1 * s1; v[1] += s1 * y1; v[2] += y1 * y1; v[3] += g1 * y1; v[4] += h1 * h1;
-    v[5] = dmax_(v[5], fabs(g1));
-  }
-  if (i < n) {
-    const double s = x[i] - xp[i], y = g[i] - gp[i];
-    v[0] += s * s; v[1] += s * y; v[2] += y * y; v[3] += g[i] * y; v[4] += gp[i] * gp[i];
-    v[5] = dmax_(v[5], fabs(g[i]));
+  const int nch = num_chunks(P);
+  for (int k = 0; k < nch; ++k) {
+    if (P.chunk > 0) wait_chunk(P.in_flags + k, P.epoch, c.timed_out);
+    const ChunkRange cr = chunk_range(P, k);
+    const int64_t n = cr.hi;
+    int64_t i = cr.lo + c.i0;
+    for (; i + st < n; i += 2 * st) {   // two independent elements in flight
+      const double x0 = x[i], q0 = xp[i], g0 = g[i], h0 = gp[i];
+      const double x1 = x[i + st], q1 = xp[i + st], g1 = g[i + st], h1 = gp[i + st];
+      const double s0 = x0 - q0, y0 = g0 - h0, s1 = x1 - q1, y1 = g1 - h1;
+      v[0] += s0 * s0; v[1] += s0 * y0; v[2] += y0 * y0; v[3] += g0 * y0; v[4] += h0 * h0;
+      v[5] = dmax_(v[5], fabs(g0));
+      v[0] += s1 * s1; v[1] += s1 * y1; v[2] += y1 * y1; v[3] += g1 * y1; v[4] += h1 * h1;
+      v[5] = dmax_(v[5], fabs(g1));
+    }
+    if (i < n) {
+      const double s = x[i] - xp[i], y = g[i] - gp[i];
+      v[0] += s * s; v[1] += s * y; v[2] += y * y; v[3] += g[i] * y; v[4] += gp[i] * gp[i];
+      v[5] = dmax_(v[5], fabs(g[i]));
+    }
   }
   block_reduce_store<6>(v, 6, PH_STEP_REDUCE, 0, c.out, c.smem);
 }
@@ -239,12 +286,16 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
   const double beta = cmd.beta, wa = cmd.wa;
   constexpr int U = 4;   // elements in flight per thread
   if (dir) {  // d = g + beta d_prev ; gd = (omega alpha) d ; rho = x - gd
-    for (int64_t i0 = c.i0; i0 < n; i0 += U * st) {
+   const int nch = num_chunks(P);
+   for (int k = 0; k < nch; ++k) {
+    if (P.chunk > 0) wait_chunk(P.in_flags + P.nchunk + k, P.epoch, c.timed_out);
+    const ChunkRange cr = chunk_range(P, k);
+    for (int64_t i0 = cr.lo + c.i0; i0 < cr.hi; i0 += U * st) {
       double gv[U], dv[U], xv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t i = i0 + u * st;
-        const bool ok = i < n;
+        const bool ok = i < cr.hi;
         gv[u] = ok ? g[i] : 0.0;
         dv[u] = (ok && use_dp) ? dp[i] : 0.0;
         xv[u] = ok ? x[i] : 0.0;
@@ -252,13 +303,16 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t i = i0 + u * st;
-        if (i < n) {
+        if (i < cr.hi) {
           const double d = use_dp ? gv[u] + beta * dv[u] : gv[u];
           dout[i] = d;
           rho[i] = xv[u] - wa * d;
         }
       }
     }
+   }
+  } else if (P.chunk > 0) {   // streamed PROJECT-style input: wait for everything
+    for (int k = 0; k < P.nchunk; ++k) wait_chunk(P.in_flags + P.nchunk + k, P.epoch, c.timed_out);
   }
   const double L = P.lower, U_ = P.upper;
   for (int j = 0; j < m; ++j) {

@@ -166,6 +166,17 @@ struct Problem {
   double ours_len;              // bound on our summation depth (error bound)
   int32_t compact_cap;          // per-warp active-list capacity (0: no compaction)
   int32_t pad0_;
+  // Host-buffer streaming (persistent kernel, host C-ABI entry only): the
+  // inputs arrive in `nchunk` element chunks of `chunk` elements while the
+  // kernel runs.  Chunk c of x, x_prev, g, g_prev is resident once
+  // in_flags[c] has reached `epoch`, chunk c of d_prev and every grad row
+  // once in_flags[nchunk + c] has.  The kernel sets *out_flag = epoch once d
+  // is final (after PREP), so its device->host copy overlaps the bisection.
+  const unsigned* in_flags;
+  unsigned* out_flag;
+  int64_t chunk;                // 0: inputs already resident
+  uint32_t epoch;
+  int32_t nchunk;
 };
 
 // Controller-visible result.

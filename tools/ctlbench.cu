@@ -9,7 +9,7 @@
 using namespace topt_b200;
 
 __global__ void __launch_bounds__(512, 1) k_ctl(const Plan* gplan, const double* gt, int nt,
-                                                long long* cyc, int reps, unsigned long long* marks) {
+                                                long long* cyc, int reps, unsigned long long* marks, int scalar) {
   extern __shared__ int4 s_dyn[];
   Plan& sp = *reinterpret_cast<Plan*>(s_dyn);
   __shared__ double s_t[PMAX];
@@ -22,7 +22,8 @@ __global__ void __launch_bounds__(512, 1) k_ctl(const Plan* gplan, const double*
     (void)marks;
     long long t0 = clock64();
 
-    if (threadIdx.x < 32) plan_consume_warp(sp, s_t);
+    if (scalar) { if (threadIdx.x == 0) plan_consume(sp, s_t); }
+    else if (threadIdx.x < 32) plan_consume_warp(sp, s_t);
     __syncthreads();
     long long t1 = clock64();
     if (threadIdx.x == 0) cyc[r] = t1 - t0;
@@ -46,7 +47,7 @@ int main(int argc, char** argv) {
     const int smem = (int)sizeof(Plan);
     cudaFuncSetAttribute(k_ctl, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int reps = getenv("REPS") ? atoi(getenv("REPS")) : 4;
-    k_ctl<<<1, 512, smem>>>(dp, dt, nt, dc, reps, dm);
+    k_ctl<<<1, 512, smem>>>(dp, dt, nt, dc, reps, dm, getenv("CTL_SCALAR") != nullptr);
     long long c[64];
     cudaMemcpy(c, dc, 4 * 8, cudaMemcpyDeviceToHost);
     printf("%s (plan %zu B read %zu, %d totals): cycles %lld %lld %lld %lld  err=%s\n", argv[f],

@@ -43,3 +43,14 @@ for rep in range(5):
                  host_outputs=("x_new", "d"), out=out)
     t1 = time.perf_counter()
     print(f"api.pgd_step host call: {1e3*(t1-t0):.3f} ms")
+from paper_2511_13905_b200 import _lib
+ctx = _lib.context(0)
+ctx.set_profiling(True)
+ctx.kernel_time()
+for rep in range(3):
+    t0 = time.perf_counter()
+    api.pgd_step(*hx[:5], hx[5], p.g_values, p.bounds_g, p.is_eq, p.partition, t=p.t,
+                 host_outputs=("x_new", "d"), out=out)
+    t1 = time.perf_counter()
+    print(f"host call {1e3*(t1-t0):.3f} ms; kernel (launch->end on the stream) {ctx.kernel_time()}")
+ctx.set_profiling(False)
