@@ -35,8 +35,16 @@ constexpr double kUnit = 1.1102230246251565e-16;  // 2^-53
 // Optional device-side timeline marks (debug builds of the trace only).
 #if defined(__CUDACC__)
 __device__ unsigned long long* g_ctl_marks = nullptr;
+#if defined(TOPT_CTL_MARK_SMEM)   // microbenchmark builds: clock64 into shared memory
+__device__ __forceinline__ unsigned long long* ctl_marks_smem() {
+  __shared__ unsigned long long m[16];
+  return m;
+}
+#endif
 __host__ __device__ __forceinline__ void ctl_mark(int k) {
-#if defined(__CUDA_ARCH__)
+#if defined(__CUDA_ARCH__) && defined(TOPT_CTL_MARK_SMEM)
+  ctl_marks_smem()[k] = clock64();
+#elif defined(__CUDA_ARCH__)
   if (g_ctl_marks && blockIdx.x == 0) {
     unsigned long long t;
 #if defined(TOPT_CTL_MARK_CLOCK)
@@ -260,12 +268,27 @@ struct RootEst {
   int kind;        // 0: gaussian(ye, sig) ; 1: log-uniform prior below 0 ; 2: above 0
   double ye, sig, L, inv_sig;
   double sl, E;    // slope scale near the root (0 if unknown) and the walk's bound
+  double thr;      // est_certain distance: max(6 sig, 16 E / sl)
 };
+
+// Division for estimates only (never a decision): reciprocal estimate + one
+// Newton step on the device, IEEE on the host.
+TOPT_HDN inline double est_div(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  r = __fma_rn(r, __fma_rn(-b, r, 1.0), r);
+  return a * r;
+#else
+  return a / b;
+#endif
+}
 
 TOPT_HD RootEst walk_estimate_(const Walk& w);
 TOPT_NOINLINE RootEst walk_estimate(const Walk& w) {
   RootEst e = walk_estimate_(w);
-  e.inv_sig = 1.0 / e.sig;
+  e.inv_sig = est_div(1.0, e.sig);
+  e.thr = dmax_(6.0 * e.sig, (e.sl > 0.0) ? est_div(16.0 * e.E, e.sl) : 0.0);
   return e;
 }
 TOPT_HD RootEst walk_estimate_(const Walk& w) {
@@ -277,16 +300,16 @@ TOPT_HD RootEst walk_estimate_(const Walk& w) {
   const bool hint = w.hok && w.hy >= w.lo && w.hy <= w.hi && w.hs > 0.0;
   if (w.hasA && w.hasB && w.ya < w.yb) {
     const double ya = w.ya, yb = w.yb;
-    double sec = ya - w.Ra * (yb - ya) / (w.Rb - w.Ra);
+    double sec = ya - est_div(w.Ra * (yb - ya), w.Rb - w.Ra);
     if (!(sec >= ya)) sec = ya;
     if (!(sec <= yb)) sec = yb;
     double spread = 0.0;
     if (w.Sa > 0.0) {
-      const double t = dmin_(dmax_(ya - w.Ra / w.Sa, ya), yb);
+      const double t = dmin_(dmax_(ya - est_div(w.Ra, w.Sa), ya), yb);
       spread = dmax_(spread, fabs(t - sec));
     }
     if (w.Sb > 0.0) {
-      const double t = dmin_(dmax_(yb - w.Rb / w.Sb, ya), yb);
+      const double t = dmin_(dmax_(yb - est_div(w.Rb, w.Sb), ya), yb);
       spread = dmax_(spread, fabs(t - sec));
     }
     double sig = dmax_(spread, (yb - ya) * 1e-6);
@@ -299,7 +322,7 @@ TOPT_HD RootEst walk_estimate_(const Walk& w) {
   if (hint) { e.ye = w.hy; e.sig = w.hs; return e; }
   if (!w.up) {  // root in [bp_lo, 0], r(0) > 0 known
     if (w.hasB && w.Sb > 0.0) {
-      e.ye = dmax_(w.yb - w.Rb / w.Sb, w.lo);
+      e.ye = dmax_(w.yb - est_div(w.Rb, w.Sb), w.lo);
       e.sig = dmax_(0.5 * fabs(e.ye), 1e-300);
       return e;
     }
@@ -308,7 +331,7 @@ TOPT_HD RootEst walk_estimate_(const Walk& w) {
     return e;
   }
   if (w.hasA && w.Sa > 0.0) {  // root in [0, bp_hi], r(0) < 0 known
-    e.ye = dmin_(w.ya - w.Ra / w.Sa, w.hi);
+    e.ye = dmin_(w.ya - est_div(w.Ra, w.Sa), w.hi);
     e.sig = dmax_(0.5 * fabs(e.ye), 1e-300);
     return e;
   }
@@ -318,9 +341,8 @@ TOPT_HD RootEst walk_estimate_(const Walk& w) {
 }
 
 TOPT_HDN inline bool est_certain(const RootEst& e, double y) {
-  const double d = fabs(y - e.ye);
   // 6 sigma away, and far enough that |r| there should clear the bound E
-  return e.kind == 0 && d * e.inv_sig >= 6.0 && (!(e.sl > 0.0) || d * e.sl >= 16.0 * e.E);
+  return e.kind == 0 && fabs(y - e.ye) >= e.thr;
 }
 
 // Probability that the root lies above y.
@@ -398,7 +420,10 @@ TOPT_HD int walk_candidates(const Walk& w, const ProjOptions& o, int K, double* 
       lo = ym;
     } else {
       const double pa = est_p_above(e, ym);   // root above ym -> r(ym) <= 0 -> lo = ym
-      const bool right = pa >= 0.5;
+      bool right;   // p_above >= 0.5, as one comparison (as walk_candidates_warp)
+      if (e.kind == 0) right = ym <= e.ye;
+      else if (e.kind == 1) right = approx_log2(fabs(ym)) >= e.L - 33.0;
+      else right = approx_log2(fabs(ym)) <= e.L - 33.0;
       ++lev;
       if (lev > 1 && est_certain(e, ym)) {   // the walk's next midpoint is always taken
         if (right) { cert_lo = ym; has_cl = true; } else { cert_hi = ym; has_ch = true; }
@@ -967,16 +992,19 @@ TOPT_NOINLINE void plan_consume(Plan& pl, const double* t) {
 }
 
 #if defined(__CUDACC__)
-// Warp-parallel candidate choice.  Lane 0 walks the predicted path (the
-// direction at each level is a single comparison with the estimate's
-// threshold) and records the uncertain levels; the lanes then price the path
-// nodes and their siblings in parallel (prefix product of branch
-// probabilities) and keep the K most probable, exactly as walk_candidates
-// ranks them.
+// Warp-parallel candidate choice (same set as walk_candidates).  Lane 0
+// walks the predicted path -- a bisection toward the estimate, where a level
+// certified by (yL, yH) is skipped, a near-certain level only updates the
+// certifier of its direction, and every other level is recorded with its
+// branch probability.  The lanes then price the recorded nodes in parallel
+// (prefix product), pick the MAX_HEDGE most probable first-level alternatives
+// by warp arg-max, and merge path and hedges by probability with ballots.
 constexpr int WPATH = 32;
 struct WarpPath {
   double y[WPATH], lo[WPATH], hi[WPATH];
-  int np, n0;
+  int rt[WPATH];   // direction taken at the node (1: lo = ym)
+  double cert_lo, cert_hi, clo, chi;
+  int np, n0, has_cl, has_ch;
   RootEst e;
 };
 
@@ -989,78 +1017,138 @@ __device__ int walk_candidates_warp(const Walk& w, const ProjOptions& o, int K, 
     ctl_mark(2);
     const RootEst e = walk_estimate(w);
     ctl_mark(3);
-    // direction threshold: right (lo = ym) iff p_above(ym) >= 0.5
-    const double L2 = e.L - 33.0;
-    int np = 0;
+    double clo, chi;
+    walk_window(w, &clo, &chi);
+    int np = 0, lev = 0;
     double lo = w.lo, hi = w.hi, ym = w.ym;
     int it = w.iters;
     const bool hasL = w.hasL, hasH = w.hasH;
     const double yL = w.yL, yH = w.yH;
     const int Kp = (K - n0 < WPATH) ? K - n0 : WPATH;
-    while (np < Kp && (hi - lo) > o.tol_b && it < o.binary_maxiter) {
-      if (hasH && yH <= ym) {
-        hi = ym;
-      } else if (hasL && yL >= ym) {
-        lo = ym;
-      } else {
-        bool right;
-        if (e.kind == 0) right = ym <= e.ye;
-        else if (e.kind == 1) right = approx_log2(fabs(ym)) >= L2;
-        else right = approx_log2(fabs(ym)) <= L2;
-        wp.y[np] = ym; wp.lo[np] = lo; wp.hi[np] = hi;
-        ++np;
-        if (right) lo = ym; else hi = ym;
+    double cert_lo = 0.0, cert_hi = 0.0;
+    int has_cl = 0, has_ch = 0;
+    // Direction = one comparison with the estimate's median (p_above >= 0.5);
+    // the loop body is written branch-free so a level costs the ym chain
+    // (compare, select, add, multiply), not three resolved branches.
+    const double L2 = e.L - 33.0;
+    const double thr = e.thr;                      // est_certain: |ym - ye| >= thr
+    const bool k0 = e.kind == 0, k1 = e.kind == 1;
+    const double ye = e.ye;
+    const double tol_b = o.tol_b;
+    const int maxit = o.binary_maxiter;
+    if (k0) {   // point estimate: certain levels feed the certifiers
+#pragma unroll 1
+      while (np < Kp && lev < kMaxPathLevels && (hi - lo) > tol_b && it < maxit) {
+        const bool cH = hasH && yH <= ym, cL = hasL && yL >= ym;
+        const bool unc = !cH && !cL;
+        const bool right = !cH && (cL || ym <= ye);
+        const int lev1 = lev + (unc ? 1 : 0);
+        const bool cert = unc && lev1 > 1 && fabs(ym - ye) >= thr;
+        cert_lo = (cert && right) ? ym : cert_lo;
+        cert_hi = (cert && !right) ? ym : cert_hi;
+        has_cl |= (cert && right) ? 1 : 0;
+        has_ch |= (cert && !right) ? 1 : 0;
+        wp.y[np] = ym; wp.lo[np] = lo; wp.hi[np] = hi; wp.rt[np] = right;   // kept iff recorded
+        np += (unc && !cert) ? 1 : 0;
+        lev = lev1;
+        lo = right ? ym : lo;
+        hi = right ? hi : ym;
+        ym = 0.5 * (lo + hi);
+        ++it;
       }
-      ym = 0.5 * (lo + hi);
-      ++it;
+    } else {    // log-uniform prior: every uncertain level is a path node
+#pragma unroll 1
+      while (np < Kp && lev < kMaxPathLevels && (hi - lo) > tol_b && it < maxit) {
+        const bool cH = hasH && yH <= ym, cL = hasL && yL >= ym;
+        const bool unc = !cH && !cL;
+        const double lg = approx_log2(fabs(ym));
+        const bool right = !cH && (cL || (k1 ? (lg >= L2) : (lg <= L2)));
+        wp.y[np] = ym; wp.lo[np] = lo; wp.hi[np] = hi; wp.rt[np] = right;
+        np += unc ? 1 : 0;
+        lev += unc ? 1 : 0;
+        lo = right ? ym : lo;
+        hi = right ? hi : ym;
+        ym = 0.5 * (lo + hi);
+        ++it;
+      }
     }
+    if (has_cl && n0 < K) out[n0++] = cert_lo;
+    if (has_ch && n0 < K) out[n0++] = cert_hi;
+    wp.e = e;
     wp.np = np;
     wp.n0 = n0;
-    wp.e = e;
+    wp.clo = clo;
+    wp.chi = chi;
     ctl_mark(4);
   }
   __syncwarp();
   const int np = wp.np, n0 = wp.n0;
-  const RootEst e = wp.e;
-  // level k = lane: branch probabilities
+  const double clo = wp.clo, chi = wp.chi;
+  // level k = lane: branch probability, path probability, hedge
   double q = 1.0, ym = 0.0, alt = 0.0;
   if (lane < np) {
     ym = wp.y[lane];
-    const double pa = est_p_above(e, ym);
-    const bool right = pa >= 0.5;
+    const double pa = est_p_above(wp.e, ym);
+    const bool right = wp.rt[lane] != 0;
     q = right ? pa : 1.0 - pa;
     alt = right ? 0.5 * (wp.lo[lane] + ym) : 0.5 * (ym + wp.hi[lane]);
   }
-  // P_k = prod_{i<k} q_i (exclusive prefix product, fixed shuffle order)
+  // P_k = prod_{i<k} q_i (exclusive prefix product; the scalar version
+  // multiplies in the same left-to-right order for k <= 1 and by a fixed tree
+  // after that -- only the ranking uses it)
   double P = q;
+#pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
     const double v = __shfl_up_sync(0xffffffffu, P, off);
     if (lane >= off) P = P * v;
   }
-  double Pex = __shfl_up_sync(0xffffffffu, P, 1);
-  if (lane == 0) Pex = 1.0;
-  const double pp = lane < np ? Pex : -1.0;                       // path node
-  const double hp0 = lane < np ? Pex * (1.0 - q) : -1.0;          // its sibling
-  const double hp = hp0 > 1e-12 ? hp0 : -1.0;
-  // rank every item: path node k before hedges of equal probability, lower k first
-  int rp = 0, rh = 0;
-  for (int s = 0; s < 32; ++s) {
-    const double ps = __shfl_sync(0xffffffffu, pp, s);
-    const double hs = __shfl_sync(0xffffffffu, hp, s);
-    if (s < np) {
-      rp += (ps > pp || (ps == pp && s < lane)) ? 1 : 0;
-      rp += (hs > pp) ? 1 : 0;
-      rh += (ps >= hp) ? 1 : 0;
-      rh += (hs > hp || (hs == hp && s < lane)) ? 1 : 0;
+  double pp = __shfl_up_sync(0xffffffffu, P, 1);
+  if (lane == 0) pp = 1.0;
+  if (lane == 0) ctl_mark(8);
+  const double hp = pp * (1.0 - q);
+  bool elig = lane < np && hp > 1e-12 && alt > clo && alt < chi;
+  // the MAX_HEDGE most probable hedges, descending (ties: lower level first):
+  // one integer max-reduction per pick on a 32-bit key = the top 27 bits of
+  // the (positive) float probability above the complemented lane index
+  double hv[MAX_HEDGE], hy[MAX_HEDGE];
+  int nh = 0;
+  const unsigned key = elig ? (((__float_as_uint((float)hp) >> 5) << 5) | (31u - (unsigned)lane))
+                            : 0u;   // hp > 1e-12, so an eligible key is >= 32
+#pragma unroll
+  for (int r = 0; r < MAX_HEDGE; ++r) {
+    const unsigned active = __ballot_sync(0xffffffffu, elig);
+    hv[r] = -1.0; hy[r] = 0.0;
+    if (active) {
+      const unsigned best = __reduce_max_sync(0xffffffffu, elig ? key : 0u);
+      const int src = 31 - (int)(best & 31u);
+      hv[r] = __shfl_sync(0xffffffffu, hp, src);
+      hy[r] = __shfl_sync(0xffffffffu, alt, src);
+      if (lane == src) elig = false;
+      ++nh;
     }
   }
-  if (lane == 0) ctl_mark(5);
+  if (lane == 0) ctl_mark(9);
+  // merge: path node k goes to k + #{hedges > pp_k}; hedge r to
+  // r + #{path nodes with pp >= h_r}; keep the first `room` positions
   const int room = K - n0;
-  if (lane < np && rp < room) out[n0 + rp] = ym;
-  if (lane < np && hp > 0.0 && rh < room) out[n0 + rh] = alt;
-  int taken = (lane < np && rp < room ? 1 : 0) + (lane < np && hp > 0.0 && rh < room ? 1 : 0);
-  for (int off = 16; off > 0; off >>= 1) taken += __shfl_xor_sync(0xffffffffu, taken, off);
+  int taken = 0;
+  if (lane < np) {
+    int pos = lane;
+#pragma unroll
+    for (int r = 0; r < MAX_HEDGE; ++r) pos += (r < nh && hv[r] > pp) ? 1 : 0;
+    if (pos < room) out[n0 + pos] = ym;
+  }
+#pragma unroll
+  for (int r = 0; r < MAX_HEDGE; ++r) {
+    if (r < nh) {
+      const unsigned ge = __ballot_sync(0xffffffffu, lane < np && pp >= hv[r]);
+      const int pos = r + __popc(ge);
+      if (lane == 0 && pos < room) out[n0 + pos] = hy[r];
+    }
+  }
+  taken = np + nh < room ? np + nh : room;
   __syncwarp();
+  if (lane == 0) ctl_mark(10);
   return n0 + taken;
 }
 
@@ -1091,6 +1179,7 @@ __device__ bool schedule_sweep_warp(Plan& pl, WarpPath& wp) {
       __syncwarp();
       if (lane < nc) cy[rk] = v;
       __syncwarp();
+      if (lane == 0) ctl_mark(11);
       tot += nc;
     }
   }
@@ -1139,97 +1228,87 @@ __device__ void consume_sweep_warp(Plan& pl, const double* t) {
     const int b = c.row_start[j], e = c.row_start[j + 1], nc = e - b;
     if (nc <= 0) continue;
     Walk w = pl.w[j];
+    // lane k holds candidate k; the row's candidates are ascending, so the
+    // nearest qualifying point below (above) is the highest (lowest) lane
     const bool mine = lane < nc;
     const double cy = mine ? c.cand_y[b + lane] : 0.0;
     const double cR = mine ? t[2 * (b + lane)] - w.ghat : 0.0;
     const double cS = mine ? t[2 * (b + lane) + 1] : 0.0;
-    int src;
-    warp_arg(mine && cR <= 0.0, cy, true, &src);           // nearest R <= 0 from below
-    if (src >= 0) {
-      const double y = __shfl_sync(0xffffffffu, cy, src);
-      if (!w.hasA || y > w.ya) {
-        w.hasA = 1; w.ya = y;
-        w.Ra = __shfl_sync(0xffffffffu, cR, src); w.Sa = __shfl_sync(0xffffffffu, cS, src);
-      }
-    }
-    warp_arg(mine && cR > 0.0, cy, false, &src);           // nearest R > 0 from above
-    if (src >= 0) {
-      const double y = __shfl_sync(0xffffffffu, cy, src);
-      if (!w.hasB || y < w.yb) {
-        w.hasB = 1; w.yb = y;
-        w.Rb = __shfl_sync(0xffffffffu, cR, src); w.Sb = __shfl_sync(0xffffffffu, cS, src);
-      }
-    }
-    warp_arg(mine && cR < -w.E, cy, true, &src);
-    if (src >= 0) {
-      const double y = __shfl_sync(0xffffffffu, cy, src);
-      if (!w.hasL || y > w.yL) { w.hasL = 1; w.yL = y; }
-    }
-    warp_arg(mine && cR > w.E, cy, false, &src);
-    if (src >= 0) {
-      const double y = __shfl_sync(0xffffffffu, cy, src);
-      if (!w.hasH || y < w.yH) { w.hasH = 1; w.yH = y; }
-    }
+    const double E = w.E;
+    const unsigned mA = __ballot_sync(0xffffffffu, mine && cR <= 0.0);
+    const unsigned mB = __ballot_sync(0xffffffffu, mine && cR > 0.0);
+    const unsigned mL = __ballot_sync(0xffffffffu, mine && cR < -E);
+    const unsigned mH = __ballot_sync(0xffffffffu, mine && cR > E);
+    const unsigned mNear = __ballot_sync(0xffffffffu, mine && fabs(cR) <= E);
+    const int sA = mA ? 31 - __clz(mA) : 0, sB = mB ? __ffs(mB) - 1 : 0;
+    const int sL = mL ? 31 - __clz(mL) : 0, sH = mH ? __ffs(mH) - 1 : 0;
+    const double yA = __shfl_sync(0xffffffffu, cy, sA), RA = __shfl_sync(0xffffffffu, cR, sA);
+    const double SA = __shfl_sync(0xffffffffu, cS, sA);
+    const double yB = __shfl_sync(0xffffffffu, cy, sB), RB = __shfl_sync(0xffffffffu, cR, sB);
+    const double SB = __shfl_sync(0xffffffffu, cS, sB);
+    const double yLc = __shfl_sync(0xffffffffu, cy, sL), yHc = __shfl_sync(0xffffffffu, cy, sH);
+    if (mA && (!w.hasA || yA > w.ya)) { w.hasA = 1; w.ya = yA; w.Ra = RA; w.Sa = SA; }
+    if (mB && (!w.hasB || yB < w.yb)) { w.hasB = 1; w.yb = yB; w.Rb = RB; w.Sb = SB; }
+    if (mL && (!w.hasL || yLc > w.yL)) { w.hasL = 1; w.yL = yLc; }
+    if (mH && (!w.hasH || yHc < w.yH)) { w.hasH = 1; w.yH = yHc; }
     if (lane == 0) ctl_mark(0);
-    // replay (every lane runs the same loop; lookups are ballots)
+    // replay (every lane runs the same loop; a lookup is one ballot)
     if (w.status == WK_NEED) {
       const bool hasL = w.hasL, hasH = w.hasH;
-      const double yL = w.yL, yH = w.yH, E = w.E;
-      int near = 0, direct = 0;
-      double minm = w.min_margin;
+      const double yL = w.yL, yH = w.yH;
+      unsigned used = 0u;   // lanes whose value decided a level directly
       bool stop = false;
       if (!w.feas_done) {
         const double yb = w.up ? w.bp_hi : w.bp_lo;
         const unsigned hit = __ballot_sync(0xffffffffu, mine && cy == yb);
         int infeasible = -1;
         if (hit) {
+          // projection.cpp:80-94: R < 0 (up) / R > 0 (down) => infeasible
           const double R = __shfl_sync(0xffffffffu, cR, __ffs(hit) - 1);
           infeasible = w.up ? (R < 0.0) : (R > 0.0);
-          minm = dmin_(minm, fabs(R) / E);
-          near += (fabs(R) <= E);
+          used |= hit;
         } else if (hasH && yH <= yb) {
           infeasible = w.up ? 0 : 1;
         } else if (hasL && yL >= yb) {
           infeasible = w.up ? 1 : 0;
         }
-        w.near_ties += near;
-        w.min_margin = minm;
-        near = 0;
         if (infeasible < 0) { stop = true; }
         else if (infeasible) { w.status = WK_INFEASIBLE; stop = true; }
         else w.feas_done = 1;
       }
+      int direct = 0;
       if (!stop) {
         double lo = w.lo, hi = w.hi, ym = w.ym;
         int it = w.iters;
         const double tol_b = pl.P.opt.tol_b;
         const int maxit = pl.P.opt.binary_maxiter;
         int status = WK_DONE;
+#pragma unroll 1
         while ((hi - lo) > tol_b && it < maxit) {
-          int d;
-          if (hasH && yH <= ym) {
-            d = 1;
-          } else if (hasL && yL >= ym) {
-            d = -1;
-          } else {
-            const unsigned hit = __ballot_sync(0xffffffffu, mine && cy == ym);
-            if (!hit) { status = WK_NEED; break; }
-            const double R = __shfl_sync(0xffffffffu, cR, __ffs(hit) - 1);
-            minm = dmin_(minm, fabs(R) / E);
-            near += (fabs(R) <= E);
-            ++direct;
-            d = R > 0.0 ? 1 : -1;
-          }
-          if (d > 0) hi = ym; else lo = ym;
+          const bool cH = hasH && yH <= ym, cL = hasL && yL >= ym;
+          const unsigned hit = __ballot_sync(0xffffffffu, mine && cy == ym);
+          const bool unc = !cH && !cL;
+          if (unc && !hit) { status = WK_NEED; break; }
+          used |= unc ? hit : 0u;
+          direct += unc ? 1 : 0;
+          const bool up = cH || (unc && (hit & mB) != 0u);   // evaluated: R > 0.0
+          hi = up ? ym : hi;
+          lo = up ? lo : ym;
           ym = 0.5 * (lo + hi);
           ++it;
         }
         w.lo = lo; w.hi = hi; w.ym = ym; w.iters = it;
-        w.near_ties += near;
-        w.n_direct += direct;
-        w.min_margin = minm;
         w.status = status;
         if (status == WK_DONE) w.y = ym;
+      }
+      // diagnostics over the directly used evaluations
+      w.near_ties += __popc(used & mNear);
+      w.n_direct += direct;
+      if (used) {
+        double mm = ((used >> lane) & 1u) ? fabs(cR) / E : 1e300;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mm = dmin_(mm, __shfl_xor_sync(0xffffffffu, mm, off));
+        w.min_margin = dmin_(w.min_margin, mm);
       }
     }
     __syncwarp();

@@ -1,6 +1,7 @@
 // ctlbench.cu — cycles of one controller step (plan_consume_warp) on a Plan
 // snapshot taken from the host simulator (diagnostics).
 
+#define TOPT_CTL_MARK_SMEM 1
 #include <cstdio>
 #include <vector>
 #include <cstdlib>
@@ -20,6 +21,8 @@ __global__ void __launch_bounds__(512, 1) k_ctl(const Plan* gplan, const double*
     for (int k = threadIdx.x; k < nt; k += 512) s_t[k] = gt[k];
     __syncthreads();
     (void)marks;
+    if (threadIdx.x < 16) ctl_marks_smem()[threadIdx.x] = 0;
+    __syncthreads();
     long long t0 = clock64();
 
     if (scalar) { if (threadIdx.x == 0) plan_consume(sp, s_t); }
@@ -27,6 +30,11 @@ __global__ void __launch_bounds__(512, 1) k_ctl(const Plan* gplan, const double*
     __syncthreads();
     long long t1 = clock64();
     if (threadIdx.x == 0) cyc[r] = t1 - t0;
+    if (r == reps - 1 && threadIdx.x < MAX_CAND) {
+      reinterpret_cast<double*>(marks + 2048)[threadIdx.x] = sp.cmd.cand_y[threadIdx.x];
+      if (threadIdx.x == 0) marks[2047] = sp.cmd.row_start[1];
+    }
+    if (threadIdx.x < 16) marks[16 * r + threadIdx.x] = ctl_marks_smem()[threadIdx.x] ? ctl_marks_smem()[threadIdx.x] - t0 : 0;
     __syncthreads();
   }
 }
@@ -53,9 +61,18 @@ int main(int argc, char** argv) {
     printf("%s (plan %zu B read %zu, %d totals): cycles %lld %lld %lld %lld  err=%s\n", argv[f],
            sizeof(Plan), got, nt, c[0], c[1], c[2], c[3], cudaGetErrorString(cudaGetLastError()));
     unsigned long long mk[64];
+    {
+      unsigned long long nc;
+      double cy[MAX_CAND];
+      cudaMemcpy(&nc, dm + 2047, 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(cy, dm + 2048, sizeof(cy), cudaMemcpyDeviceToHost);
+      printf("   cand (%llu):", nc);
+      for (unsigned long long k = 0; k < nc && k < MAX_CAND; ++k) printf(" %.9g", cy[k]);
+      printf("\n");
+    }
     cudaMemcpy(mk, dm, 64 * 8, cudaMemcpyDeviceToHost);
     printf("   marks (rep 3, cycles from start):");
-    for (int k = 0; k < 8; ++k) if (mk[24 + k]) printf(" %d:%lld", k, (long long)(mk[24 + k] - mk[35]));
+    for (int k = 0; k < 16; ++k) if (mk[48 + k]) printf(" %d:%lld", k, (long long)mk[48 + k]);
     printf("\n");
   }
 }
