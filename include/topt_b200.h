@@ -172,6 +172,10 @@ int topt_b200_set_stream(topt_b200_ctx* ctx, void* stream);
 int topt_b200_set_profiling(topt_b200_ctx* ctx, int enabled);
 int topt_b200_kernel_time(topt_b200_ctx* ctx, double* total_ms, int64_t* launches,
                           double* max_ms);
+/* Whole-job device time under profiling: CUDA events on the context's stream
+ * from the plan upload to the results download of each job (step, projection,
+ * ...), accumulated and reset on read. */
+int topt_b200_step_time(topt_b200_ctx* ctx, double* total_ms, int64_t* jobs, double* max_ms);
 
 /* Debug: per-pass device timestamps of the next persistent launch. */
 int topt_b200_debug_trace(topt_b200_ctx* ctx, int enable, unsigned long long* out);

@@ -75,7 +75,8 @@ EXPORTS = [
     "topt_b200_build", "topt_b200_delta_of_y", "topt_b200_constraint_residual_h",
     "topt_b200_project", "topt_b200_project_dev", "topt_b200_owner_map",
     "topt_b200_pgd_step", "topt_b200_pgd_step_dev", "topt_b200_step_direction",
-    "topt_b200_set_profiling", "topt_b200_kernel_time", "topt_b200_debug_trace",
+    "topt_b200_set_profiling", "topt_b200_kernel_time", "topt_b200_step_time",
+    "topt_b200_debug_trace",
     "topt_b200_nccl_unique_id", "topt_b200_ctx_create_ranks", "topt_b200_pgd_step_ranks",
 ]
 
@@ -117,6 +118,7 @@ def load():
         "topt_b200_set_profiling": [vp, C.c_int],
         "topt_b200_debug_trace": [vp, C.c_int, vp],
         "topt_b200_kernel_time": [vp, vp, vp, vp],
+        "topt_b200_step_time": [vp, vp, vp, vp],
         "topt_b200_nccl_unique_id": [vp, C.c_size_t],
         "topt_b200_ctx_create_ranks": [C.c_int, C.c_int, C.c_int, vp, C.POINTER(C.c_void_p)],
         "topt_b200_pgd_step_ranks": [vp, vp, i64, vp, vp, vp, vp, vp],
@@ -198,6 +200,13 @@ class Context:
 
     def set_profiling(self, on: bool):
         self.lib.topt_b200_set_profiling(self.h, 1 if on else 0)
+
+    def step_time(self):
+        """(total_ms, jobs, max_ms) of whole-job device time since the last call
+        (profiling on): plan upload -> kernel(s) -> results download."""
+        t = C.c_double(0); n = C.c_int64(0); mx = C.c_double(0)
+        self.lib.topt_b200_step_time(self.h, C.byref(t), C.byref(n), C.byref(mx))
+        return t.value, n.value, mx.value
 
     def kernel_time(self):
         """(total_ms, launches, max_ms) of profiled pass launches since the last call."""

@@ -390,6 +390,31 @@ class StepResult:
     mask: object = None
 
 
+class PreparedStep:
+    """A PGD step bound to its buffers: the C-ABI call with every argument
+    struct built once, so repeated steps on the same buffers (an optimizer
+    loop, the benchmark) pay only the library call.  `run()` executes the
+    step; `result()` wraps the last outputs like pgd_step's return value."""
+
+    def __init__(self, ctx, fn, args, keep, m, outs):
+        self.ctx, self._fn, self._args, self._keep, self.m = ctx, fn, args, keep, m
+        self._outs = outs
+
+    def run(self):
+        _check(self.ctx, self._fn(*self._args))
+        return self
+
+    def result(self) -> StepResult:
+        o = self._outs
+        meta = o["meta"]
+        proj = _meta_to_result(meta, o["delta"], o["y"].copy(), o["sl"].copy(), self.m, o["mask"])
+        return StepResult(x_new=o["x_new"], d=o["d"], rho_tilde=o["rt"], delta=o["delta"],
+                          y=o["y"].copy(), slacks=o["sl"].copy(), g_hat=o["gh"].copy(),
+                          alpha=meta.alpha,
+                          beta=meta.beta, fallback=bool(meta.fallback), projection=proj,
+                          mask=o["mask"])
+
+
 def pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_equality=None,
              partition=None, t=1, violation=0.0, lower=0.0, upper=1.0,
              settings: PgdSettings = None, device: int = 0, want_delta=False,
@@ -402,6 +427,21 @@ def pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_equality
     numpy inputs -> host-buffer C-ABI (copies inside the call);
     torch CUDA tensors -> device C-ABI (no copies; `out` may supply buffers).
     """
+    return prepare_pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g,
+                            is_equality, partition, t, violation, lower, upper, settings,
+                            device, want_delta, want_mask, out, host_outputs, ctx, n_global,
+                            row_counts).run().result()
+
+
+def prepare_pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_equality=None,
+                     partition=None, t=1, violation=0.0, lower=0.0, upper=1.0,
+                     settings: PgdSettings = None, device: int = 0, want_delta=False,
+                     want_mask=False, out=None,
+                     host_outputs=("x_new", "d", "rho_tilde"), ctx: L.Context = None,
+                     n_global: int = None, row_counts=None) -> PreparedStep:
+    """pgd_step's argument handling without the call: returns a PreparedStep
+    whose run() executes the step on these buffers (the arrays are referenced,
+    not copied, so updating them in place between runs is allowed)."""
     settings = settings or PgdSettings()
     ctx = ctx or L.context(device)
     dev = _is_torch_cuda(x)
@@ -448,13 +488,15 @@ def pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_equality
         o.mask = mask.data_ptr() if mask is not None else None
         if getattr(ctx, "distributed", False):
             rc_arr = None if row_counts is None else np.ascontiguousarray(row_counts, np.int64)
-            _check(ctx, ctx.lib.topt_b200_pgd_step_ranks(
-                ctx.h, C.byref(pr), int(n_global if n_global is not None else n), _ptr(rc_arr),
-                C.byref(sc), C.byref(opts), C.byref(o), C.byref(meta)))
+            fn = ctx.lib.topt_b200_pgd_step_ranks
+            args = (ctx.h, C.byref(pr), int(n_global if n_global is not None else n),
+                    _ptr(rc_arr), C.byref(sc), C.byref(opts), C.byref(o), C.byref(meta))
+            keep = [rc_arr]
         else:
-            _check(ctx, ctx.lib.topt_b200_pgd_step_dev(ctx.h, C.byref(pr), C.byref(sc),
-                                                       C.byref(opts), C.byref(o),
-                                                       C.byref(meta)))
+            fn = ctx.lib.topt_b200_pgd_step_dev
+            args = (ctx.h, C.byref(pr), C.byref(sc), C.byref(opts), C.byref(o), C.byref(meta))
+            keep = []
+        keep += [x, x_prev, g, g_prev, d_prev, grad, owner]
     else:
         arrs = {k: np.ascontiguousarray(v, np.float64) for k, v in
                 (("x", x), ("x_prev", x_prev), ("g", g), ("g_prev", g_prev), ("d_prev", d_prev),
@@ -476,9 +518,10 @@ def pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_equality
         o.x_new, o.d, o.rho_tilde = _ptr(x_new), _ptr(d), _ptr(rt)
         o.delta = _ptr(delta)
         o.mask = _ptr(mask)
-        _check(ctx, ctx.lib.topt_b200_pgd_step(ctx.h, C.byref(pr), C.byref(sc), C.byref(opts),
-                                               C.byref(o), C.byref(meta)))
-    proj = _meta_to_result(meta, delta, y, sl, m, mask)
-    return StepResult(x_new=x_new, d=d, rho_tilde=rt, delta=delta, y=y, slacks=sl, g_hat=gh,
-                      alpha=meta.alpha, beta=meta.beta, fallback=bool(meta.fallback),
-                      projection=proj, mask=mask)
+        fn = ctx.lib.topt_b200_pgd_step
+        args = (ctx.h, C.byref(pr), C.byref(sc), C.byref(opts), C.byref(o), C.byref(meta))
+        keep = [arrs]
+    keep += [pr, sc, opts, o, meta, gv, bg, ie, off, idx]
+    outs = dict(meta=meta, delta=delta, y=y, sl=sl, gh=gh, mask=mask, x_new=x_new, d=d, rt=rt)
+    return PreparedStep(ctx, fn, args, keep, m, outs)
+

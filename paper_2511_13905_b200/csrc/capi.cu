@@ -38,9 +38,11 @@ __device__ void finish_reduce(const double* partials, int nb, int ns, int phase,
                               double* totals, double* smem, int stride = PMAX) {
   for (int s0 = 0; s0 < ns; s0 += BLOCK) {
     const int per = min(ns - s0, BLOCK);
+    // G groups of CTAs per slot: ~sqrt(nb) balances the load chain (nb / G
+    // loads, issued together) against the in-order combine of the G groups
     int G = BLOCK / per;
     if (G > nb) G = nb;
-    if (G > 64) G = 64;
+    if (G > 16) G = 16;
     if (G < 1) G = 1;
     const int t = threadIdx.x;
     const int s = t % per, g = t / per;
@@ -380,6 +382,10 @@ struct topt_b200_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double prof_ms = 0.0, prof_max = 0.0;
   int64_t prof_n = 0;
+  // whole-job device time (plan upload -> results downloaded), when profiling
+  cudaEvent_t evs0 = nullptr, evs1 = nullptr;
+  double step_ms = 0.0, step_max = 0.0;
+  int64_t step_n = 0;
   // multi-rank (one process per GPU, NCCL over NVLink)
   int rank = 0, world = 1;
   void* comm = nullptr;          // ncclComm_t
@@ -395,6 +401,7 @@ struct topt_b200_ctx {
   int* h_timed_out = nullptr;      // pinned
   uint32_t epoch = 0;
   int stream_inputs = 1;           // TOPT_B200_STREAM=0 disables
+  Plan* hp_pin = nullptr;          // pinned staging of the plan (upload / results)
 };
 
 // ---- NCCL, resolved at run time (the process may already hold torch's copy)
@@ -533,6 +540,37 @@ int issue_stream(topt_b200_ctx* ctx, const Plan& hp, const StreamIn& si) {
   return TOPT_OK;
 }
 
+// The device needs the plan up to the scratch area; the host reads back only
+// the next phase and the results.  Both go through pinned staging.
+constexpr size_t PLAN_UP = offsetof(Plan, sc);
+int plan_upload(topt_b200_ctx* ctx, const Plan& hp) {
+  if (ctx->profile) cudaEventRecord(ctx->evs0, ctx->stream);
+  std::memcpy(ctx->hp_pin, &hp, PLAN_UP);
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_plan, ctx->hp_pin, PLAN_UP, cudaMemcpyHostToDevice, ctx->stream));
+  return TOPT_OK;
+}
+int plan_results_async(topt_b200_ctx* ctx) {
+  CUDA_TRY(ctx, cudaMemcpyAsync(&ctx->hp_pin->cmd.phase, &ctx->d_plan->cmd.phase, sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(&ctx->hp_pin->res, &ctx->d_plan->res, sizeof(Result),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+  if (ctx->profile) cudaEventRecord(ctx->evs1, ctx->stream);
+  return TOPT_OK;
+}
+// (after the stream synchronize)
+void plan_results_take(topt_b200_ctx* ctx, Plan& hp) {
+  hp.cmd.phase = ctx->hp_pin->cmd.phase;
+  hp.res = ctx->hp_pin->res;
+  if (ctx->profile) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->evs0, ctx->evs1) == cudaSuccess) {
+      ctx->step_ms += ms;
+      ctx->step_max = std::max(ctx->step_max, (double)ms);
+      ctx->step_n++;
+    }
+  }
+}
+
 int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
   if (ctx->comm) return run_plan_ranks(ctx, hp);
   const bool persistent = ctx->persistent && ctx->coop_grid > 0;
@@ -552,7 +590,7 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
     }
   }
   plan_start(hp);
-  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_plan, &hp, sizeof(Plan), cudaMemcpyHostToDevice, ctx->stream));
+  if (int rc = plan_upload(ctx, hp)) return rc;
   int phase = hp.cmd.phase;
   if (persistent && phase != PH_DONE) {
     unsigned long long* tr = ctx->trace_on ? ctx->d_trace : nullptr;
@@ -572,8 +610,9 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
       CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_timed_out, ctx->d_timed_out, sizeof(int),
                                     cudaMemcpyDeviceToHost, ctx->stream));
     }
-    CUDA_TRY(ctx, cudaMemcpyAsync(&hp, ctx->d_plan, sizeof(Plan), cudaMemcpyDeviceToHost, ctx->stream));
+    if (int rc = plan_results_async(ctx)) return rc;
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    plan_results_take(ctx, hp);
     if (si && *ctx->h_timed_out)
       return fail(ctx, TOPT_ERR_CUDA, "topt_b200: a streamed input chunk never arrived");
     if (ctx->profile) {
@@ -607,8 +646,9 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
     phase = *ctx->h_phase;
     if (getenv("TOPT_B200_DEBUG_PHASES") && it < 64) fprintf(stderr, "[topt1] pass %d -> phase %d\n", it, phase);
   }
-  CUDA_TRY(ctx, cudaMemcpyAsync(&hp, ctx->d_plan, sizeof(Plan), cudaMemcpyDeviceToHost, ctx->stream));
+  if (int rc = plan_results_async(ctx)) return rc;
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  plan_results_take(ctx, hp);
   if (phase != PH_DONE) return fail(ctx, TOPT_ERR_INTERNAL, "plan did not terminate");
   if (hp.res.status != ST_OK) return fail(ctx, hp.res.status, status_msg(hp.res.status));
   return TOPT_OK;
@@ -625,7 +665,7 @@ int run_plan_ranks(topt_b200_ctx* ctx, Plan& hp) {
   hp.P.ours_len = (double)per_thread + (double)grid + 64.0 + (double)ctx->world;
   hp.P.compact_cap = 0;
   plan_start(hp);
-  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_plan, &hp, sizeof(Plan), cudaMemcpyHostToDevice, ctx->stream));
+  if (int rc = plan_upload(ctx, hp)) return rc;
   int phase = hp.cmd.phase;
   NcclApi& api = nccl();
   for (int it = 0; phase != PH_DONE && it < 4096; ++it) {
@@ -655,8 +695,9 @@ int run_plan_ranks(topt_b200_ctx* ctx, Plan& hp) {
     phase = *ctx->h_phase;
     if (getenv("TOPT_B200_DEBUG_PHASES") && it < 64) fprintf(stderr, "[topt] pass %d -> phase %d\n", it, phase);
   }
-  CUDA_TRY(ctx, cudaMemcpyAsync(&hp, ctx->d_plan, sizeof(Plan), cudaMemcpyDeviceToHost, ctx->stream));
+  if (int rc = plan_results_async(ctx)) return rc;
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  plan_results_take(ctx, hp);
   if (phase != PH_DONE) return fail(ctx, TOPT_ERR_INTERNAL, "plan did not terminate");
   if (hp.res.status != ST_OK) return fail(ctx, hp.res.status, status_msg(hp.res.status));
   return TOPT_OK;
@@ -821,12 +862,15 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   }
   ok = ok && cudaEventCreate(&ctx->ev0) == cudaSuccess;
   ok = ok && cudaEventCreate(&ctx->ev1) == cudaSuccess;
+  ok = ok && cudaEventCreate(&ctx->evs0) == cudaSuccess;
+  ok = ok && cudaEventCreate(&ctx->evs1) == cudaSuccess;
   ok = ok && cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking) == cudaSuccess;
   ok = ok && cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming) == cudaSuccess;
   ok = ok && cudaMalloc(&ctx->d_flags, sizeof(unsigned) * 4 * MAX_STREAM_CHUNKS) == cudaSuccess;
   ok = ok && cudaMemset(ctx->d_flags, 0, sizeof(unsigned) * 4 * MAX_STREAM_CHUNKS) == cudaSuccess;
   ok = ok && cudaMalloc(&ctx->d_timed_out, sizeof(int)) == cudaSuccess;
   ok = ok && cudaMallocHost(&ctx->h_timed_out, sizeof(int)) == cudaSuccess;
+  ok = ok && cudaMallocHost(&ctx->hp_pin, sizeof(Plan)) == cudaSuccess;
   if (const char* e = getenv("TOPT_B200_STREAM")) ctx->stream_inputs = atoi(e);
   if (!ok) { topt_b200_ctx_destroy(ctx); return TOPT_ERR_CUDA; }
   *out = ctx;
@@ -858,10 +902,13 @@ void topt_b200_ctx_destroy(topt_b200_ctx* ctx) {
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_timed_out);
   if (ctx->h_timed_out) cudaFreeHost(ctx->h_timed_out);
+  if (ctx->hp_pin) cudaFreeHost(ctx->hp_pin);
   if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
   if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->evs0) cudaEventDestroy(ctx->evs0);
+  if (ctx->evs1) cudaEventDestroy(ctx->evs1);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -942,6 +989,17 @@ int topt_b200_kernel_time(topt_b200_ctx* ctx, double* total_ms, int64_t* launche
   ctx->prof_ms = 0.0;
   ctx->prof_max = 0.0;
   ctx->prof_n = 0;
+  return TOPT_OK;
+}
+
+int topt_b200_step_time(topt_b200_ctx* ctx, double* total_ms, int64_t* jobs, double* max_ms) {
+  if (!ctx) return TOPT_ERR_INTERNAL;
+  if (total_ms) *total_ms = ctx->step_ms;
+  if (jobs) *jobs = ctx->step_n;
+  if (max_ms) *max_ms = ctx->step_max;
+  ctx->step_ms = 0.0;
+  ctx->step_max = 0.0;
+  ctx->step_n = 0;
   return TOPT_OK;
 }
 

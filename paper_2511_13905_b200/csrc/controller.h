@@ -1008,7 +1008,7 @@ struct WarpPath {
   RootEst e;
 };
 
-__device__ int walk_candidates_warp(const Walk& w, const ProjOptions& o, int K, double* out,
+__device__ __noinline__ int walk_candidates_warp(const Walk& w, const ProjOptions& o, int K, double* out,
                                     WarpPath& wp) {
   const int lane = threadIdx.x & 31;
   if (lane == 0) {
@@ -1153,7 +1153,7 @@ __device__ int walk_candidates_warp(const Walk& w, const ProjOptions& o, int K, 
 }
 
 // Warp version of schedule_sweep (same command layout).
-__device__ bool schedule_sweep_warp(Plan& pl, WarpPath& wp) {
+__device__ __noinline__ bool schedule_sweep_warp(Plan& pl, WarpPath& wp) {
   const int lane = threadIdx.x & 31;
   const int m = pl.P.m;
   int need = 0;
@@ -1204,22 +1204,7 @@ __device__ bool schedule_sweep_warp(Plan& pl, WarpPath& wp) {
 // holds candidate k; bracket updates are warp arg-reductions and each
 // replayed midpoint is matched with one ballot.  Same decisions as the
 // scalar consume_sweep (candidates are distinct duals).
-__device__ __forceinline__ void warp_arg(bool valid, double key, bool want_max, int* src) {
-  // lane index holding the max/min key among valid lanes (lowest lane on ties), -1 if none
-  const int lane = threadIdx.x & 31;
-  double k = valid ? key : (want_max ? -1.0 / 0.0 : 1.0 / 0.0);
-  int l = valid ? lane : 32;
-  for (int off = 16; off > 0; off >>= 1) {
-    const double k2 = __shfl_xor_sync(0xffffffffu, k, off);
-    const int l2 = __shfl_xor_sync(0xffffffffu, l, off);
-    const bool take = (l2 < 32) && (l == 32 || (want_max ? (k2 > k || (k2 == k && l2 < l))
-                                                         : (k2 < k || (k2 == k && l2 < l))));
-    if (take) { k = k2; l = l2; }
-  }
-  *src = l < 32 ? l : -1;
-}
-
-__device__ void consume_sweep_warp(Plan& pl, const double* t) {
+__device__ __noinline__ void consume_sweep_warp(Plan& pl, const double* t) {
   const int lane = threadIdx.x & 31;
   const int m = pl.P.m;
   Cmd& c = pl.cmd;

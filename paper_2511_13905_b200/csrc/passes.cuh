@@ -285,6 +285,46 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
   const bool dir = cmd.compute_dir, dot = cmd.compute_dot, use_dp = cmd.use_dprev;
   const double beta = cmd.beta, wa = cmd.wa;
   constexpr int U = 4;   // elements in flight per thread
+  const double L = P.lower, U_ = P.upper;
+  if (dir && m == 1 && !owner) {
+    // One row, no partition (C1/C2): direction and row sums in one sweep, so
+    // rho and d are not read back.  Same per-thread element order as below.
+    PrepAcc A;
+#pragma unroll
+    for (int s = 0; s < PREP_SLOTS; ++s) A.v[s] = 0.0;   // bp_lo = bp_hi = 0 (:58)
+    const double* __restrict__ ar = P.grad;
+    const int nch = num_chunks(P);
+    for (int k = 0; k < nch; ++k) {
+      if (P.chunk > 0) wait_chunk(P.in_flags + P.nchunk + k, P.epoch, c.timed_out);
+      const ChunkRange cr = chunk_range(P, k);
+      for (int64_t i0 = cr.lo + c.i0; i0 < cr.hi; i0 += U * st) {
+        double gv[U], dv[U], xv[U], av[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t i = i0 + u * st;
+          const bool ok = i < cr.hi;
+          gv[u] = ok ? g[i] : 0.0;
+          dv[u] = (ok && use_dp) ? dp[i] : 0.0;
+          xv[u] = ok ? x[i] : 0.0;
+          av[u] = ok ? ar[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t i = i0 + u * st;
+          if (i < cr.hi) {
+            const double d = use_dp ? gv[u] + beta * dv[u] : gv[u];
+            const double r = xv[u] - wa * d;
+            dout[i] = d;
+            rho[i] = r;
+            prep_elem(A, av[u], r, dot ? wa * d : 0.0, dot, L, U_);
+          }
+        }
+      }
+    }
+    block_reduce_store<PREP_SLOTS>(A.v, PREP_SLOTS, PH_PREP, 0, c.out, c.smem);
+    compact_init(c);
+    return;
+  }
   if (dir) {  // d = g + beta d_prev ; gd = (omega alpha) d ; rho = x - gd
    const int nch = num_chunks(P);
    for (int k = 0; k < nch; ++k) {
@@ -314,7 +354,6 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
   } else if (P.chunk > 0) {   // streamed PROJECT-style input: wait for everything
     for (int k = 0; k < P.nchunk; ++k) wait_chunk(P.in_flags + P.nchunk + k, P.epoch, c.timed_out);
   }
-  const double L = P.lower, U_ = P.upper;
   for (int j = 0; j < m; ++j) {
     PrepAcc A;
 #pragma unroll
