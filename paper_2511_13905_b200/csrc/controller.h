@@ -303,18 +303,29 @@ TOPT_HD RootEst walk_estimate_(const Walk& w) {
     double sec = ya - est_div(w.Ra * (yb - ya), w.Rb - w.Ra);
     if (!(sec >= ya)) sec = ya;
     if (!(sec <= yb)) sec = yb;
-    double spread = 0.0;
-    if (w.Sa > 0.0) {
-      const double t = dmin_(dmax_(ya - est_div(w.Ra, w.Sa), ya), yb);
-      spread = dmax_(spread, fabs(t - sec));
+    // Newton from the bracket end closer to the root (smaller |R|); its error
+    // is ~ curvature * step^2 / (2 slope), the curvature taken from the two
+    // end slopes.  Without a usable slope: the secant, its spread as sigma.
+    const bool na = w.Sa > 0.0, nb = w.Sb > 0.0;
+    const double Na = na ? dmin_(dmax_(ya - est_div(w.Ra, w.Sa), ya), yb) : sec;
+    const double Nb = nb ? dmin_(dmax_(yb - est_div(w.Rb, w.Sb), ya), yb) : sec;
+    double ye = sec, sig;
+    if (na && nb) {
+      const bool use_a = fabs(w.Ra) <= fabs(w.Rb);
+      ye = use_a ? Na : Nb;
+      const double S = use_a ? w.Sa : w.Sb, d = ye - (use_a ? ya : yb);
+      const double curv = est_div(fabs(w.Sb - w.Sa), yb - ya);
+      sig = 2.0 * curv * est_div(d * d, S);
+      sig = dmax_(sig, 1e-3 * fabs(Na - Nb));
+    } else if (na || nb) {   // one slope: Newton from that end, a quarter of
+      ye = na ? Na : Nb;      // its distance to the secant as sigma
+      sig = 0.25 * fabs(ye - sec);
+    } else {
+      sig = 0.5 * (yb - ya);
     }
-    if (w.Sb > 0.0) {
-      const double t = dmin_(dmax_(yb - est_div(w.Rb, w.Sb), ya), yb);
-      spread = dmax_(spread, fabs(t - sec));
-    }
-    double sig = dmax_(spread, (yb - ya) * 1e-6);
-    sig = dmax_(sig, fabs(sec) * 1e-15);
-    e.ye = sec;
+    sig = dmax_(sig, (yb - ya) * 1e-6);
+    sig = dmax_(sig, fabs(ye) * 1e-15);
+    e.ye = ye;
     e.sig = dmax_(sig, 1e-300);
     if (hint && w.hy > ya && w.hy < yb && w.hs < e.sig) { e.ye = w.hy; e.sig = w.hs; }
     return e;

@@ -64,6 +64,7 @@ void sim_walk(const Plan* pl, int j, double* w, double* cand, int* ncand) {
   w[0] = k.lo; w[1] = k.hi; w[2] = k.ym; w[3] = k.hasL ? k.yL : nan; w[4] = k.hasH ? k.yH : nan;
   w[5] = k.iters; w[6] = k.status; w[7] = k.E; w[8] = k.n_direct;
   w[9] = pl->cmd.wlo[j]; w[10] = pl->cmd.whi[j];
+  { const RootEst e = walk_estimate(k); w[11] = e.kind; w[12] = e.ye; w[13] = e.sig; }
   const int b = pl->cmd.row_start[j], e = pl->cmd.row_start[j + 1];
   *ncand = (pl->cmd.phase == PH_SWEEP) ? e - b : 0;
   for (int q = 0; q < *ncand; ++q) cand[q] = pl->cmd.cand_y[b + q];

@@ -92,7 +92,7 @@ class Rank:
         lib().sim_consume(self.plan, _p(t))
 
     def walk(self, j):
-        w = np.zeros(11); cand = np.zeros(64); nc = C.c_int(0)
+        w = np.zeros(14); cand = np.zeros(64); nc = C.c_int(0)
         lib().sim_walk(self.plan, j, _p(w), _p(cand), C.byref(nc))
         return w, cand[:nc.value]
 
@@ -141,7 +141,7 @@ def run(prob, R=1, job=JOB_PGD_STEP, rho=None, gd=None, ghat=None, max_passes=40
                         v = y * a
                         return np.where(v < lo_, 0, np.where(v > hi_, 2, 1))
                     act = int(np.count_nonzero((cls(w[9]) != cls(w[10])) & (a != 0)))
-                    print(f"     window [{w[9]:.9g}, {w[10]:.9g}] active {act}")
+                    print(f"     window [{w[9]:.9g}, {w[10]:.9g}] active {act}  est kind {int(w[11])} ye {w[12]:.9g} sig {w[13]:.3g}")
                     print("     cand", " ".join(f"{c:.9g}" for c in cand))
         parts = [rk.partials() for rk in ranks]
         ops = ranks[0].ops(len(parts[0]))
