@@ -606,11 +606,16 @@ __device__ __noinline__ void pass_gather(const PassCtx& c) {
   const int m = P.m;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ int s_off[NWARP + 1];
-  if (threadIdx.x == 0) {
+  if (warp == 0) {   // items of the CTAs before this one: loads issued together
     int off = 0;
-    for (int b = 0; b < (int)blockIdx.x; ++b) off += __ldcg(c.blk_cnt + b);
-    s_off[0] = off;
-    for (int w = 0; w < NWARP; ++w) s_off[w + 1] = s_off[w] + c.list_cnt[w];
+    for (int b0 = 0; b0 < (int)blockIdx.x; b0 += 32) {
+      const int b = b0 + lane;
+      off += __reduce_add_sync(0xffffffffu, b < (int)blockIdx.x ? __ldcg(c.blk_cnt + b) : 0);
+    }
+    if (lane == 0) {
+      s_off[0] = off;
+      for (int w = 0; w < NWARP; ++w) s_off[w + 1] = s_off[w] + c.list_cnt[w];
+    }
   }
   __syncthreads();
   const uint32_t* Lst = c.list + (size_t)warp * c.list_cap;
@@ -636,12 +641,18 @@ __device__ __noinline__ void pass_gather(const PassCtx& c) {
 // (summed over CTAs in index order) into its shared memory.
 __device__ __noinline__ void gather_load(const PassCtx& c, int nb) {
   const int m = c.plan->P.m;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ int s_total;
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
     int t = 0;
-    for (int b = 0; b < nb; ++b) t += __ldcg(c.blk_cnt + b);
-    s_total = t < GATHER_CAP ? t : GATHER_CAP;
-    *c.n_items = s_total;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+      const int b = b0 + lane;
+      t += __reduce_add_sync(0xffffffffu, b < nb ? __ldcg(c.blk_cnt + b) : 0);
+    }
+    if (lane == 0) {
+      s_total = t < GATHER_CAP ? t : GATHER_CAP;
+      *c.n_items = s_total;
+    }
   }
   __syncthreads();
   for (int k = threadIdx.x; k < s_total; k += BLOCK) {
@@ -649,14 +660,15 @@ __device__ __noinline__ void gather_load(const PassCtx& c, int nb) {
     c.it_r[k] = __ldcg(c.g_r + k);
     c.it_row[k] = (int8_t)__ldcg(c.g_row + k);
   }
-  if (threadIdx.x < m) {
-    double C = 0.0, S = 0.0;
-    for (int b = 0; b < nb; ++b) {
-      C += __ldcg(c.g_fix + ((size_t)b * MAX_M + threadIdx.x) * 2);
-      S += __ldcg(c.g_fix + ((size_t)b * MAX_M + threadIdx.x) * 2 + 1);
+  // fixed sums over the CTAs: warp w takes slot w (C_j, S_j interleaved);
+  // lane l sums CTAs l, l+32, ... then a fixed shuffle tree (deterministic)
+  for (int sl = warp; sl < 2 * m; sl += NWARP) {
+    double v = 0.0;
+    for (int b = lane; b < nb; b += 32) v += __ldcg(c.g_fix + (size_t)b * MAX_M * 2 + sl);
+    v = warp_reduce(0, v);
+    if (lane == 0) {
+      if (sl & 1) c.fixS[sl >> 1] = v; else c.fixC[sl >> 1] = v;
     }
-    c.fixC[threadIdx.x] = C;
-    c.fixS[threadIdx.x] = S;
   }
   __syncthreads();
 }
