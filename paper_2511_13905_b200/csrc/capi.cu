@@ -207,8 +207,15 @@ __device__ __forceinline__ void signal_out(const Problem& P) {
   }
 }
 
+// The controller state travels as a kernel parameter (no separate upload).
+constexpr size_t PLAN_WORDS = offsetof(Plan, sc) / 4;
+struct PlanBlob {
+  int w[PLAN_WORDS];
+};
+
 __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
-                                                   unsigned long long* trace, GatherBufs gb) {
+                                                   unsigned long long* trace, GatherBufs gb,
+                                                   const __grid_constant__ PlanBlob blob) {
   __shared__ double s_red[RED_SCRATCH];
   __shared__ double s_tot[PMAX];
   __shared__ double s_fixC[MAX_M], s_fixS[MAX_M];
@@ -220,11 +227,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
   uint32_t* s_list = reinterpret_cast<uint32_t*>(s_work);
   cg::grid_group grid = cg::this_grid();
   const int nb = gridDim.x;
-  {  // load the controller state (everything but scratch)
-    const int* gp = reinterpret_cast<const int*>(plan);
+  {  // load the controller state (everything but scratch) from the parameter
     int* spi = reinterpret_cast<int*>(&sp);
-    const int nw = (int)(offsetof(Plan, sc) / 4);
-    for (int k = threadIdx.x; k < nw; k += BLOCK) spi[k] = __ldcg(gp + k);
+    for (int k = threadIdx.x; k < (int)PLAN_WORDS; k += BLOCK) spi[k] = blob.w[k];
   }
   __syncthreads();
   if (threadIdx.x == 0) g_ctl_marks = nullptr;
@@ -281,6 +286,8 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) { tr[4] = gtimer(); g_ctl_marks = nullptr; }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) signal_out(sp.P);   // also on early exits
+  if (blockIdx.x == 0 && threadIdx.x == 0) sp.res.final_phase = sp.cmd.phase;
+  __syncthreads();
   if (blockIdx.x == 0) {  // publish the final state (results) once
     int* gp = reinterpret_cast<int*>(plan);
     const int* spi = reinterpret_cast<const int*>(&sp);
@@ -590,14 +597,16 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
     }
   }
   plan_start(hp);
-  if (int rc = plan_upload(ctx, hp)) return rc;
   int phase = hp.cmd.phase;
   if (persistent && phase != PH_DONE) {
+    if (ctx->profile) cudaEventRecord(ctx->evs0, ctx->stream);
+    PlanBlob* blob = reinterpret_cast<PlanBlob*>(ctx->hp_pin);
+    std::memcpy(blob, &hp, sizeof(PlanBlob));
     unsigned long long* tr = ctx->trace_on ? ctx->d_trace : nullptr;
     if (tr) cudaMemsetAsync(tr, 0, 128 * 8 * sizeof(unsigned long long), ctx->stream);
     GatherBufs gb{ctx->d_blk_cnt, ctx->d_ga, ctx->d_gr, ctx->d_grow, ctx->d_gfix,
                   ctx->d_timed_out};
-    void* args[] = {&ctx->d_plan, &ctx->d_part, &tr, &gb};
+    void* args[] = {&ctx->d_plan, &ctx->d_part, &tr, &gb, blob};
     if (si) CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_timed_out, 0, sizeof(int), ctx->stream));
     if (ctx->profile) cudaEventRecord(ctx->ev0, ctx->stream);
     CUDA_TRY(ctx, cudaLaunchCooperativeKernel((void*)k_step, grid, BLOCK, args, dyn_smem,
@@ -610,8 +619,11 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
       CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_timed_out, ctx->d_timed_out, sizeof(int),
                                     cudaMemcpyDeviceToHost, ctx->stream));
     }
-    if (int rc = plan_results_async(ctx)) return rc;
+    CUDA_TRY(ctx, cudaMemcpyAsync(&ctx->hp_pin->res, &ctx->d_plan->res, sizeof(Result),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+    if (ctx->profile) cudaEventRecord(ctx->evs1, ctx->stream);
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    ctx->hp_pin->cmd.phase = ctx->hp_pin->res.final_phase;
     plan_results_take(ctx, hp);
     if (si && *ctx->h_timed_out)
       return fail(ctx, TOPT_ERR_CUDA, "topt_b200: a streamed input chunk never arrived");
@@ -626,6 +638,7 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
     if (hp.res.status != ST_OK) return fail(ctx, hp.res.status, status_msg(hp.res.status));
     return TOPT_OK;
   }
+  if (int rc = plan_upload(ctx, hp)) return rc;
   for (int it = 0; phase != PH_DONE && it < 4096; ++it) {
     if (ctx->profile) cudaEventRecord(ctx->ev0, ctx->stream);
     k_pass<<<ctx->grid, BLOCK, sizeof(Plan), ctx->stream>>>(ctx->d_plan, ctx->d_part,

@@ -184,6 +184,7 @@ struct Result {
   int32_t status, path, newton_iters, converged, curvature_violations;
   int32_t passes, sweeps, stage1_row, near_ties, fallback;
   int32_t local_sweeps, gathered;
+  int32_t final_phase, pad_r_;  // cmd.phase when the persistent kernel returned
   double active;            // active elements after the last compacted sweep
   int32_t bisect_iters[MAX_M];
   double residual, alpha, beta, min_margin;
