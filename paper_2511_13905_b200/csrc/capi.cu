@@ -583,7 +583,9 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
   const bool persistent = ctx->persistent && ctx->coop_grid > 0;
   const int grid = persistent ? ctx->coop_grid : ctx->grid;
   const int64_t per_thread = (hp.P.n + (int64_t)grid * BLOCK - 1) / ((int64_t)grid * BLOCK);
-  hp.P.ours_len = (double)per_thread + (double)grid + 64.0;
+  // per-thread summation depth: own elements + queued elements taken over
+  // from other lanes (SweepAcc) + the CTA tree and the CTA combine
+  hp.P.ours_len = 2.0 * (double)per_thread + (double)grid + 64.0;
   size_t dyn_smem = sizeof(Plan);
   hp.P.compact_cap = 0;
   if (persistent && ctx->compact) {
@@ -675,7 +677,7 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
 int run_plan_ranks(topt_b200_ctx* ctx, Plan& hp) {
   const int grid = ctx->grid;
   const int64_t per_thread = (hp.P.n + (int64_t)grid * BLOCK - 1) / ((int64_t)grid * BLOCK);
-  hp.P.ours_len = (double)per_thread + (double)grid + 64.0 + (double)ctx->world;
+  hp.P.ours_len = 2.0 * (double)per_thread + (double)grid + 64.0 + (double)ctx->world;
   hp.P.compact_cap = 0;
   plan_start(hp);
   if (int rc = plan_upload(ctx, hp)) return rc;

@@ -1199,10 +1199,7 @@ __device__ __noinline__ bool schedule_sweep_warp(Plan& pl, WarpPath& wp) {
     c.phase = PH_SWEEP;
     for (int j = m; j <= MAX_M; ++j) c.row_start[j] = tot;
     c.compact = (pl.P.compact_cap > 0 && (m == 1 || pl.P.has_part)) ? 1 : 0;
-    for (int j = 0; j < m; ++j) {
-      c.wlo[j] = pl.w[j].lo;
-      c.whi[j] = pl.w[j].hi;
-    }
+    for (int j = 0; j < m; ++j) walk_window(pl.w[j], &c.wlo[j], &c.whi[j]);
     c.ncand = tot;
     c.nslots = 2 * tot + ((c.compact && !c.local) ? 1 : 0);
     if (c.local) pl.res.local_sweeps++; else pl.res.sweeps++;

@@ -425,22 +425,81 @@ __device__ __forceinline__ void sweep_elem(double a, double r, const double* y, 
     if (p1 + s <= cnt && y[p1 + s - 1] < bl) p1 += s;
     if (p2 + s <= cnt && y[p2 + s - 1] <= bh) p2 += s;
   }
-  // Predicated adds (two compares + three guarded DADDs per candidate) instead
-  // of selects of zero: same sums bit for bit (x + 0.0 == x for the
-  // accumulators, which start at +0.0), half the instructions.
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
-    asm("{\n\t.reg .pred pb, pa, pf;\n\t"
-        "setp.lt.s32 pb, %4, %5;\n\t"
-        "setp.ge.s32 pa, %4, %6;\n\t"
-        "or.pred pf, pb, pa;\n\t"
-        "@pb add.rn.f64 %0, %0, %2;\n\t"
-        "@pa add.rn.f64 %0, %0, %3;\n\t"
-        "@!pf add.rn.f64 %1, %1, %7;\n\t}"
-        : "+d"(C[k]), "+d"(S[k])
-        : "d"(cl), "d"(ch), "r"(k), "r"(p1), "r"(p2), "d"(aa));
+    C[k] += (k < p1) ? cl : ((k >= p2) ? ch : 0.0);
+    S[k] += (k >= p1 && k < p2) ? aa : 0.0;
   }
 }
+
+// Most elements have no candidate inside their free window [bl, bh] (p1 ==
+// p2): every candidate then sees a clipped constant -- cl below the window,
+// ch above -- which costs one compare, one select pair and one add per
+// candidate.  The others are queued per warp and run through the full loop
+// 32 at a time, so no warp step is held by a few lanes.  The sums per
+// candidate get the same terms (in a different, still fixed, order).
+constexpr int SQ_CAP = 64;   // NWARP * 2 * SQ_CAP doubles fit the reduction scratch
+template <int KC>
+struct SweepAcc {
+  double C[KC], S[KC];
+  double* qa;    // this warp's queue (shared memory, SQ_CAP entries)
+  double* qr;
+  int qn;
+  const double* y;
+  int cnt;
+  double L, U;
+  __device__ __forceinline__ void init(double* qa_, double* qr_, const double* y_, int cnt_,
+                                       double L_, double U_) {
+#pragma unroll
+    for (int k = 0; k < KC; ++k) { C[k] = 0.0; S[k] = 0.0; }
+    qa = qa_; qr = qr_; qn = 0; y = y_; cnt = cnt_; L = L_; U = U_;
+  }
+  // all 32 lanes call push together (valid = this lane holds an element)
+  __device__ __forceinline__ void push(bool valid, double a, double r) {
+    const int lane = threadIdx.x & 31;
+    bool need = false;
+    if (valid && a != 0.0) {
+      const double lo = L - r, hi = U - r;
+      const double ra = rcp_full(a);
+      const double b1 = lo * ra, b2 = hi * ra;
+      const bool pos = a > 0.0;
+      const double bl = pos ? b1 : b2, bh = pos ? b2 : b1;
+      int p1 = 0, p2 = 0;
+#pragma unroll
+      for (int s = (KC >= 16 ? 16 : KC); s > 0; s >>= 1) {
+        if (p1 + s <= cnt && y[p1 + s - 1] < bl) p1 += s;
+        if (p2 + s <= cnt && y[p2 + s - 1] <= bh) p2 += s;
+      }
+      if (p1 == p2) {
+        const double cl = a * (pos ? lo : hi), ch = a * (pos ? hi : lo);
+#pragma unroll
+        for (int k = 0; k < KC; ++k) C[k] += (k < p1) ? cl : ch;
+      } else {
+        need = true;
+      }
+    }
+    const unsigned nm = __ballot_sync(0xffffffffu, need);
+    if (need) {
+      const int slot = qn + __popc(nm & ((1u << lane) - 1u));
+      qa[slot] = a;
+      qr[slot] = r;
+    }
+    qn += __popc(nm);
+    __syncwarp();
+    if (qn >= 32) {
+      const int s2 = qn - 32 + lane;
+      sweep_elem<KC>(qa[s2], qr[s2], y, cnt, L, U, C, S);
+      qn -= 32;
+      __syncwarp();
+    }
+  }
+  __device__ __forceinline__ void flush() {
+    const int lane = threadIdx.x & 31;
+    if (lane < qn) sweep_elem<KC>(qa[lane], qr[lane], y, cnt, L, U, C, S);
+    qn = 0;
+    __syncwarp();
+  }
+};
 
 // r_k = C_k + y_k S_k into the (R, S) slot pair layout
 template <int KC>
@@ -458,31 +517,31 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
   const double* __restrict__ rho = P.rho;
   const double* __restrict__ ar = P.grad + (int64_t)j * P.ld;
   const int8_t* __restrict__ owner = P.owner;
-  const double L = P.lower, U = P.upper;
-  const double* y = c.cmd->cand_y + b;   // shared memory (broadcast)
-  double R[KC], S[KC];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the warps' queues live in the reduction scratch (free until the end)
+  SweepAcc<KC> acc;
+  acc.init(c.smem + warp * 2 * SQ_CAP, c.smem + warp * 2 * SQ_CAP + SQ_CAP, c.cmd->cand_y + b,
+           cnt, P.lower, P.upper);
+  constexpr int UL = 4;   // elements' loads in flight per lane
+  for (int64_t i0 = c.i0 - lane; i0 < n; i0 += UL * st) {   // warp-uniform trip count
+    double av[UL], rv[UL];
+    bool ok[UL];
 #pragma unroll
-  for (int k = 0; k < KC; ++k) { R[k] = 0.0; S[k] = 0.0; }
-  int64_t i = c.i0;
-  for (; i + st < n; i += 2 * st) {
-    double a0 = ar[i], a1 = ar[i + st];
-    const double r0 = rho[i], r1 = rho[i + st];
-    if (owner) {   // a masked to 0 outside the row's block: adds exact zeros
-      if (owner[i] != j) a0 = 0.0;
-      if (owner[i + st] != j) a1 = 0.0;
+    for (int u = 0; u < UL; ++u) {
+      const int64_t i = i0 + u * st + lane;
+      ok[u] = i < n && (owner == nullptr || owner[i] == j);
+      av[u] = ok[u] ? ar[i] : 0.0;
+      rv[u] = ok[u] ? rho[i] : 0.0;
     }
-    sweep_elem<KC>(a0, r0, y, cnt, L, U, R, S);
-    sweep_elem<KC>(a1, r1, y, cnt, L, U, R, S);
+#pragma unroll
+    for (int u = 0; u < UL; ++u) acc.push(ok[u], av[u], rv[u]);
   }
-  if (i < n) {
-    double a0 = ar[i];
-    if (owner && owner[i] != j) a0 = 0.0;
-    sweep_elem<KC>(a0, rho[i], y, cnt, L, U, R, S);
-  }
-  sweep_finish<KC>(y, cnt, R, S);
+  acc.flush();
+  __syncthreads();   // queues (in c.smem) drained before the reduction reuses it
+  sweep_finish<KC>(acc.y, cnt, acc.C, acc.S);
   double v[2 * KC];
 #pragma unroll
-  for (int k = 0; k < KC; ++k) { v[2 * k] = R[k]; v[2 * k + 1] = S[k]; }
+  for (int k = 0; k < KC; ++k) { v[2 * k] = acc.C[k]; v[2 * k + 1] = acc.S[k]; }
   block_reduce_store<2 * KC>(v, 2 * cnt, PH_SWEEP, 2 * b, c.out, c.smem);
 }
 
@@ -510,35 +569,55 @@ __device__ __noinline__ void pass_sweep_row_compact(const PassCtx& c, int j, int
   for (int k = 0; k < KC; ++k) { R[k] = 0.0; S[k] = 0.0; }
   double nC = 0.0, nS = 0.0;
   int kept = 0;
-  for (int base = 0; base < n_items; base += 32) {
-    const int idx = base + lane;
-    const bool valid = idx < n_items;
-    const uint32_t i = valid ? Lst[idx] : 0u;
-    bool relevant = valid;
-    if (owner && valid) relevant = owner[i] == j;
-    bool fixed = false;
-    if (relevant) {
-      const double a = ar[i];
-      const double r = rho[i];
-      const double lo = L - r, hi = U_ - r;
-      const double v1 = wlo * a, v2 = whi * a;
-      const int g1 = v1 < lo ? 0 : (v1 > hi ? 2 : 1);
-      const int g2 = v2 < lo ? 0 : (v2 > hi ? 2 : 1);
-      if (g1 == g2) {
-        fixed = true;
-        if (g1 == 0) nC += a * lo;
-        else if (g1 == 2) nC += a * hi;
-        else nS += a * a;
-      } else {
-        sweep_elem<KC>(a, r, y, cnt, L, U_, R, S);
-      }
+  // Phase 1: classify every listed element against the window (loads of UC
+  // entries in flight per lane), fold the fixed ones and compact the list in
+  // order.  Phase 2 then evaluates the kept elements only, 32 per warp step,
+  // so a warp is not held by one active lane.
+  constexpr int UC = 4;
+  for (int base = 0; base < n_items; base += 32 * UC) {
+    uint32_t iv[UC];
+    double av[UC], rv[UC];
+    bool rel[UC];
+#pragma unroll
+    for (int u = 0; u < UC; ++u) {
+      const int idx = base + u * 32 + lane;
+      const bool valid = idx < n_items;
+      iv[u] = valid ? Lst[idx] : 0u;
+      rel[u] = valid && (owner == nullptr || owner[iv[u]] == j);
+      av[u] = rel[u] ? ar[iv[u]] : 0.0;
+      rv[u] = rel[u] ? rho[iv[u]] : 0.0;
     }
-    // rows other than j keep their items (partitioned problems)
-    const bool keep = valid && !(relevant && fixed);
-    const unsigned km = __ballot_sync(0xffffffffu, keep);
-    __syncwarp();
-    if (keep) Lst[kept + __popc(km & ((1u << lane) - 1u))] = i;
-    kept += __popc(km);
+#pragma unroll
+    for (int u = 0; u < UC; ++u) {
+      const int idx = base + u * 32 + lane;
+      const bool valid = idx < n_items;
+      bool fixed = false;
+      if (rel[u]) {
+        const double a = av[u], r = rv[u];
+        const double lo = L - r, hi = U_ - r;
+        const double v1 = wlo * a, v2 = whi * a;
+        const int g1 = v1 < lo ? 0 : (v1 > hi ? 2 : 1);
+        const int g2 = v2 < lo ? 0 : (v2 > hi ? 2 : 1);
+        if (g1 == g2) {
+          fixed = true;
+          if (g1 == 0) nC += a * lo;
+          else if (g1 == 2) nC += a * hi;
+          else nS += a * a;
+        }
+      }
+      // rows other than j keep their items (partitioned problems)
+      const bool keep = valid && !(rel[u] && fixed);
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      if (keep) Lst[kept + __popc(km & ((1u << lane) - 1u))] = iv[u];
+      kept += __popc(km);
+    }
+  }
+  __syncwarp();
+  // Phase 2: the window's active elements of row j
+  for (int k = lane; k < kept; k += 32) {
+    const uint32_t i = Lst[k];
+    if (owner && owner[i] != j) continue;
+    sweep_elem<KC>(ar[i], rho[i], y, cnt, L, U_, R, S);
   }
   __syncwarp();
   if (lane == 0) c.list_cnt[warp] = kept;

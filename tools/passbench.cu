@@ -2,6 +2,7 @@
 // (diagnostics): a fake Plan, L2-resident inputs, CUDA-event timing.
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <vector>
 #include <cuda_runtime.h>
 #include "../paper_2511_13905_b200/csrc/passes.cuh"
@@ -31,7 +32,10 @@ int main() {
   const int64_t n = 1 << 20;
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   std::vector<double> ha(n), hr(n);
-  for (int64_t i = 0; i < n; ++i) { ha[i] = -3.0 * (0.1 + (i % 97) * 0.009); hr[i] = -99.5 + (i % 89) * 0.01; }
+  FILE* fa = fopen("tools/c2_a.bin", "rb");
+  FILE* fr = fopen("tools/c2_rho.bin", "rb");
+  if (fa && fr) { fread(ha.data(), 8, n, fa); fread(hr.data(), 8, n, fr); fclose(fa); fclose(fr); }
+  else for (int64_t i = 0; i < n; ++i) { ha[i] = -3.0 * (0.1 + (i % 97) * 0.009); hr[i] = -99.5 + (i % 89) * 0.01; }
   double *a, *r, *x, *part, *d;
   cudaMalloc(&a, n * 8); cudaMalloc(&r, n * 8); cudaMalloc(&x, n * 8); cudaMalloc(&d, n * 8);
   cudaMalloc(&part, (size_t)PMAX * 8 * 4096);
@@ -43,7 +47,17 @@ int main() {
   hp->P.d_prev = r; hp->P.d_out = d;
   hp->cmd.ncand = 16; hp->cmd.row_start[0] = 0;
   for (int j = 1; j <= MAX_M; ++j) hp->cmd.row_start[j] = 16;
-  for (int k = 0; k < 16; ++k) hp->cmd.cand_y[k] = -45.0 + k * 0.5;
+  // candidates of the first C2 sweep (octave-spaced path) or of a later one
+  const double first[16] = {-1411062.76, -705531.381, -352765.691, -176382.845, -88191.4226,
+                            -44095.7113, -22047.8557, -11023.9278, -5511.96392, -2755.98196,
+                            -1377.99098, -688.995489, -344.497745, -172.248872, -86.1244362,
+                            -43.0622181};
+  const double second[16] = {-42.3893709, -41.7165238, -41.3801002, -41.0436766, -40.9595707,
+                             -40.9175178, -40.8964913, -40.8859781, -40.8754648, -40.707253,
+                             -40.3708295, -39.0251351, -37.6794408, -34.9880522, -32.2966636,
+                             -21.531109};
+  const bool use_second = getenv("SECOND") != nullptr;
+  for (int k = 0; k < 16; ++k) hp->cmd.cand_y[k] = use_second ? second[k] : first[k];
   hp->cmd.y[0] = -38.0; hp->cmd.write_x = 1; hp->cmd.resid_rows = 1;
   hp->cmd.compute_dir = 1; hp->cmd.use_dprev = 1; hp->cmd.beta = 0.1; hp->cmd.wa = 1.0; hp->cmd.compute_dot = 1;
   Plan* dp; cudaMalloc(&dp, sizeof(Plan)); cudaMemcpy(dp, hp, sizeof(Plan), cudaMemcpyHostToDevice);
