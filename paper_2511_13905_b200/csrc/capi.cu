@@ -262,8 +262,18 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     c.timed_out = gb.timed_out;
     if (sp.cmd.phase == PH_SWEEP && sp.cmd.local) {   // CTA-local sweep: no barrier
       local_sweep(c, s_tot);
+#ifdef TOPT_ICACHE_EXPERIMENT
+      if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[7] = gtimer();
+      __syncthreads();
+      local_sweep(c, s_tot);
+#endif
+      if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
+        tr[1] = tr[6] = tr[2] = tr[3] = gtimer();
+        g_ctl_marks = trace + 512 + pass * 8;
+      }
       if (threadIdx.x < 32) plan_consume_warp(sp, s_tot);
       __syncthreads();
+      if (tr && blockIdx.x == 0 && threadIdx.x == 0) { tr[4] = gtimer(); g_ctl_marks = nullptr; }
       continue;
     }
     run_pass(c);
@@ -283,6 +293,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     }
     if (threadIdx.x < 32) plan_consume_warp(sp, s_tot);
     __syncthreads();
+    if (sp.cmd.load_fused) {   // fused gather: the items were published by the sweep
+      gather_load_fused(c, nb);
+      if (threadIdx.x == 0) sp.cmd.load_fused = 0;
+      __syncthreads();
+    }
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) { tr[4] = gtimer(); g_ctl_marks = nullptr; }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) signal_out(sp.P);   // also on early exits
@@ -855,9 +870,11 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   ok = ok && cudaMemset(ctx->d_counter, 0, sizeof(unsigned)) == cudaSuccess;
   ok = ok && cudaMalloc(&ctx->d_trace, 128 * 8 * sizeof(unsigned long long)) == cudaSuccess;
   ok = ok && cudaMalloc(&ctx->d_blk_cnt, sizeof(int) * ctx->grid) == cudaSuccess;
-  ok = ok && cudaMalloc(&ctx->d_ga, sizeof(double) * GATHER_CAP) == cudaSuccess;
-  ok = ok && cudaMalloc(&ctx->d_gr, sizeof(double) * GATHER_CAP) == cudaSuccess;
-  ok = ok && cudaMalloc(&ctx->d_grow, sizeof(int) * GATHER_CAP) == cudaSuccess;
+  // gather buffers: contiguous (gather pass) or one GATHER_BLK region per CTA (fused)
+  const size_t gcap = std::max<size_t>(GATHER_CAP, (size_t)ctx->grid * GATHER_BLK);
+  ok = ok && cudaMalloc(&ctx->d_ga, sizeof(double) * gcap) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_gr, sizeof(double) * gcap) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_grow, sizeof(int) * gcap) == cudaSuccess;
   ok = ok && cudaMalloc(&ctx->d_gfix, sizeof(double) * 2 * MAX_M * ctx->grid) == cudaSuccess;
   ctx->max_dyn_smem = 160 * 1024;
   ok = ok && cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1337,7 +1354,7 @@ int topt_b200_pgd_step(topt_b200_ctx* ctx, const topt_step_problem* prob,
   if (streamed) {
     int64_t nch = (n + (1 << 18) - 1) >> 18;   // ~2 MB per array per chunk
     nch = std::max<int64_t>(1, std::min<int64_t>(nch, MAX_STREAM_CHUNKS));
-    P.chunk = (n + nch - 1) / nch;
+    P.chunk = (((n + nch - 1) / nch) + 63) & ~int64_t(63);   // even: 16-byte pairs
     P.nchunk = (int32_t)((n + P.chunk - 1) / P.chunk);
     P.epoch = ++ctx->epoch;
     P.in_flags = ctx->d_flags;

@@ -592,11 +592,13 @@ TOPT_NOINLINE bool schedule_sweep(Plan& pl) {
     }
   }
   for (int j = m; j <= MAX_M; ++j) c.row_start[j] = tot;
-  c.compact = (pl.P.compact_cap > 0 && (m == 1 || pl.P.has_part)) ? 1 : 0;
+  c.compact = (pl.P.compact_cap > 0 && (m == 1 || pl.P.has_part) &&
+               (c.local || pl.res.sweeps > 0)) ? 1 : 0;   // see schedule_sweep_warp
   for (int j = 0; j < m; ++j) walk_window(pl.w[j], &c.wlo[j], &c.whi[j]);
   c.ncand = tot;
-  // compacted global sweeps append one slot: the active elements left
-  c.nslots = 2 * tot + ((c.compact && !c.local) ? 1 : 0);
+  // compacted global sweeps append two slots: the active elements left and
+  // the CTAs holding more than GATHER_BLK of them
+  c.nslots = 2 * tot + ((c.compact && !c.local) ? 2 : 0);
   if (c.local) pl.res.local_sweeps++; else pl.res.sweeps++;
   return true;
 }
@@ -883,7 +885,15 @@ TOPT_NOINLINE void consume_sweep(Plan& pl, const double* t) {
   // walks CTA-locally (no grid barrier per sweep)
   int need = 0;
   for (int j = 0; j < m; ++j) need += (pl.w[j].status == WK_NEED);
-  if (need && was_global_compact && pl.res.active <= (double)GATHER_CAP) {
+  if (need && was_global_compact && pl.res.active <= (double)GATHER_TRIGGER) {
+    if (t[2 * c.ncand + 1] == 0.0) {   // every CTA published its items (fused gather)
+      c.local = 1;
+      c.load_fused = 1;
+      pl.res.gathered = 1;
+      if (!schedule_sweep(pl)) after_walks(pl);
+      ctl_mark(3);
+      return;
+    }
     c.phase = PH_GATHER;
     c.nslots = 0;
     ctl_mark(3);
@@ -1198,10 +1208,14 @@ __device__ __noinline__ bool schedule_sweep_warp(Plan& pl, WarpPath& wp) {
   if (lane == 0) {
     c.phase = PH_SWEEP;
     for (int j = m; j <= MAX_M; ++j) c.row_start[j] = tot;
-    c.compact = (pl.P.compact_cap > 0 && (m == 1 || pl.P.has_part)) ? 1 : 0;
+    // the first global sweep of a job classifies nothing away (its window is
+    // the whole bracket): it runs the plain full sweep with the queued
+    // fast path; the active lists start with the second
+    c.compact = (pl.P.compact_cap > 0 && (m == 1 || pl.P.has_part) &&
+                 (c.local || pl.res.sweeps > 0)) ? 1 : 0;
     for (int j = 0; j < m; ++j) walk_window(pl.w[j], &c.wlo[j], &c.whi[j]);
     c.ncand = tot;
-    c.nslots = 2 * tot + ((c.compact && !c.local) ? 1 : 0);
+    c.nslots = 2 * tot + ((c.compact && !c.local) ? 2 : 0);
     if (c.local) pl.res.local_sweeps++; else pl.res.sweeps++;
   }
   __syncwarp();
@@ -1317,9 +1331,16 @@ __device__ __noinline__ void consume_sweep_warp(Plan& pl, const double* t) {
     int need = 0;
     for (int j = 0; j < m; ++j) need += (pl.w[j].status == WK_NEED);
     s_act = 0;
-    if (need && was_global_compact && pl.res.active <= (double)GATHER_CAP) {
-      c.phase = PH_GATHER;
-      c.nslots = 0;
+    if (need && was_global_compact && pl.res.active <= (double)GATHER_TRIGGER) {
+      if (t[2 * c.ncand + 1] == 0.0) {   // every CTA published its items (fused gather)
+        c.local = 1;
+        c.load_fused = 1;
+        pl.res.gathered = 1;
+        s_act = 1;
+      } else {
+        c.phase = PH_GATHER;
+        c.nslots = 0;
+      }
     } else {
       s_act = 1;
     }

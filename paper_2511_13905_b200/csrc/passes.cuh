@@ -200,7 +200,22 @@ __device__ __forceinline__ ChunkRange chunk_range(const Problem& P, int k) {
   return {lo, lo + P.chunk < P.n ? lo + P.chunk : P.n};
 }
 
+// 16-byte vector access is used when every array of a pass is 16-byte
+// aligned (torch / cudaMalloc buffers are; an offset user pointer may not be).
+__device__ __forceinline__ bool al16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
 // ---- PH_STEP_REDUCE: BB / PR+ sums --------------------
+struct StepAcc {
+  double v[6];
+  __device__ __forceinline__ void add(double x0, double q0, double g0, double h0) {
+    const double s0 = x0 - q0, y0 = g0 - h0;
+    v[0] += s0 * s0; v[1] += s0 * y0; v[2] += y0 * y0; v[3] += g0 * y0; v[4] += h0 * h0;
+    v[5] = dmax_(v[5], fabs(g0));
+  }
+};
+
 __device__ __noinline__ void pass_step_reduce(const PassCtx& c) {
   const Problem& P = c.plan->P;
   const int64_t st = c.stride;
@@ -208,29 +223,46 @@ __device__ __noinline__ void pass_step_reduce(const PassCtx& c) {
   const double* __restrict__ xp = P.x_prev;
   const double* __restrict__ g = P.g;
   const double* __restrict__ gp = P.g_prev;
-  double v[6] = {0, 0, 0, 0, 0, 0};
+  StepAcc A = {{0, 0, 0, 0, 0, 0}};
   const int nch = num_chunks(P);
+  const bool vec = al16(x) && al16(xp) && al16(g) && al16(gp);
   for (int k = 0; k < nch; ++k) {
     if (P.chunk > 0) wait_chunk(P.in_flags + k, P.epoch, c.timed_out);
     const ChunkRange cr = chunk_range(P, k);
+    if (vec) {   // element pairs (chunk starts are even), two pairs in flight
+      const double2* __restrict__ X = reinterpret_cast<const double2*>(x);
+      const double2* __restrict__ Q = reinterpret_cast<const double2*>(xp);
+      const double2* __restrict__ Gv = reinterpret_cast<const double2*>(g);
+      const double2* __restrict__ H = reinterpret_cast<const double2*>(gp);
+      const int64_t q1 = cr.hi >> 1;
+      int64_t q = (cr.lo >> 1) + c.i0;
+      for (; q + st < q1; q += 2 * st) {
+        const double2 x0 = X[q], p0 = Q[q], g0 = Gv[q], h0 = H[q];
+        const double2 x1 = X[q + st], p1 = Q[q + st], g1 = Gv[q + st], h1 = H[q + st];
+        A.add(x0.x, p0.x, g0.x, h0.x); A.add(x0.y, p0.y, g0.y, h0.y);
+        A.add(x1.x, p1.x, g1.x, h1.x); A.add(x1.y, p1.y, g1.y, h1.y);
+      }
+      if (q < q1) {
+        const double2 x0 = X[q], p0 = Q[q], g0 = Gv[q], h0 = H[q];
+        A.add(x0.x, p0.x, g0.x, h0.x); A.add(x0.y, p0.y, g0.y, h0.y);
+      }
+      if ((cr.hi & 1) && c.i0 == 0) {   // odd tail element
+        const int64_t i = cr.hi - 1;
+        A.add(x[i], xp[i], g[i], gp[i]);
+      }
+      continue;
+    }
     const int64_t n = cr.hi;
     int64_t i = cr.lo + c.i0;
     for (; i + st < n; i += 2 * st) {   // two independent elements in flight
       const double x0 = x[i], q0 = xp[i], g0 = g[i], h0 = gp[i];
       const double x1 = x[i + st], q1 = xp[i + st], g1 = g[i + st], h1 = gp[i + st];
-      const double s0 = x0 - q0, y0 = g0 - h0, s1 = x1 - q1, y1 = g1 - h1;
-      v[0] += s0 * s0; v[1] += s0 * y0; v[2] += y0 * y0; v[3] += g0 * y0; v[4] += h0 * h0;
-      v[5] = dmax_(v[5], fabs(g0));
-      v[0] += s1 * s1; v[1] += s1 * y1; v[2] += y1 * y1; v[3] += g1 * y1; v[4] += h1 * h1;
-      v[5] = dmax_(v[5], fabs(g1));
+      A.add(x0, q0, g0, h0);
+      A.add(x1, q1, g1, h1);
     }
-    if (i < n) {
-      const double s = x[i] - xp[i], y = g[i] - gp[i];
-      v[0] += s * s; v[1] += s * y; v[2] += y * y; v[3] += g[i] * y; v[4] += gp[i] * gp[i];
-      v[5] = dmax_(v[5], fabs(g[i]));
-    }
+    if (i < n) A.add(x[i], xp[i], g[i], gp[i]);
   }
-  block_reduce_store<6>(v, 6, PH_STEP_REDUCE, 0, c.out, c.smem);
+  block_reduce_store<6>(A.v, 6, PH_STEP_REDUCE, 0, c.out, c.smem);
 }
 
 // ---- PH_PREP: direction, rho_tilde, g_hat dots, r(0), slope(0), bounds,
@@ -288,37 +320,66 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
   const double L = P.lower, U_ = P.upper;
   if (dir && m == 1 && !owner) {
     // One row, no partition (C1/C2): direction and row sums in one sweep, so
-    // rho and d are not read back.  Same per-thread element order as below.
+    // rho and d are not read back.
     PrepAcc A;
 #pragma unroll
     for (int s = 0; s < PREP_SLOTS; ++s) A.v[s] = 0.0;   // bp_lo = bp_hi = 0 (:58)
     const double* __restrict__ ar = P.grad;
     const int nch = num_chunks(P);
+    const bool vec = al16(g) && al16(x) && al16(ar) && al16(dout) && al16(rho) &&
+                     (!use_dp || al16(dp));
+    // d = g + beta d_prev ; gd = (omega alpha) d ; rho = x - gd
+    auto elem = [&](double gv, double dv, double xv, double av, double& d, double& r) {
+      d = use_dp ? gv + beta * dv : gv;
+      const double gd = wa * d;
+      r = xv - gd;
+      prep_elem(A, av, r, gd, dot, L, U_);
+    };
     for (int k = 0; k < nch; ++k) {
       if (P.chunk > 0) wait_chunk(P.in_flags + P.nchunk + k, P.epoch, c.timed_out);
       const ChunkRange cr = chunk_range(P, k);
-      for (int64_t i0 = cr.lo + c.i0; i0 < cr.hi; i0 += U * st) {
-        double gv[U], dv[U], xv[U], av[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t i = i0 + u * st;
-          const bool ok = i < cr.hi;
-          gv[u] = ok ? g[i] : 0.0;
-          dv[u] = (ok && use_dp) ? dp[i] : 0.0;
-          xv[u] = ok ? x[i] : 0.0;
-          av[u] = ok ? ar[i] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t i = i0 + u * st;
-          if (i < cr.hi) {
-            const double d = use_dp ? gv[u] + beta * dv[u] : gv[u];
-            const double r = xv[u] - wa * d;
-            dout[i] = d;
-            rho[i] = r;
-            prep_elem(A, av[u], r, dot ? wa * d : 0.0, dot, L, U_);
+      if (vec) {   // element pairs, two pairs in flight per thread
+        const double2* __restrict__ G2 = reinterpret_cast<const double2*>(g);
+        const double2* __restrict__ D2 = reinterpret_cast<const double2*>(dp);
+        const double2* __restrict__ X2 = reinterpret_cast<const double2*>(x);
+        const double2* __restrict__ A2 = reinterpret_cast<const double2*>(ar);
+        double2* __restrict__ DO = reinterpret_cast<double2*>(dout);
+        double2* __restrict__ RO = reinterpret_cast<double2*>(rho);
+        const int64_t q1 = cr.hi >> 1;
+        for (int64_t q = (cr.lo >> 1) + c.i0; q < q1; q += 2 * st) {
+          const bool ok1 = q + st < q1;
+          const double2 z2 = make_double2(0.0, 0.0);
+          const double2 g0 = G2[q], x0 = X2[q], a0 = A2[q];
+          const double2 d0 = use_dp ? D2[q] : z2;
+          const double2 g1 = ok1 ? G2[q + st] : z2, x1 = ok1 ? X2[q + st] : z2;
+          const double2 a1 = ok1 ? A2[q + st] : z2;
+          const double2 d1 = (ok1 && use_dp) ? D2[q + st] : z2;
+          double2 dd, rr;
+          elem(g0.x, d0.x, x0.x, a0.x, dd.x, rr.x);
+          elem(g0.y, d0.y, x0.y, a0.y, dd.y, rr.y);
+          DO[q] = dd;
+          RO[q] = rr;
+          if (ok1) {
+            elem(g1.x, d1.x, x1.x, a1.x, dd.x, rr.x);
+            elem(g1.y, d1.y, x1.y, a1.y, dd.y, rr.y);
+            DO[q + st] = dd;
+            RO[q + st] = rr;
           }
         }
+        if ((cr.hi & 1) && c.i0 == 0) {   // odd tail element
+          const int64_t i = cr.hi - 1;
+          double dd, rr;
+          elem(g[i], use_dp ? dp[i] : 0.0, x[i], ar[i], dd, rr);
+          dout[i] = dd;
+          rho[i] = rr;
+        }
+        continue;
+      }
+      for (int64_t i = cr.lo + c.i0; i < cr.hi; i += st) {
+        double dd, rr;
+        elem(g[i], use_dp ? dp[i] : 0.0, x[i], ar[i], dd, rr);
+        dout[i] = dd;
+        rho[i] = rr;
       }
     }
     block_reduce_store<PREP_SLOTS>(A.v, PREP_SLOTS, PH_PREP, 0, c.out, c.smem);
@@ -668,14 +729,45 @@ __device__ void pass_sweep(const PassCtx& c) {
     else pass_sweep_row<MAX_K>(c, j, b, cnt);
   }
   if (cmd.compact && c.list) {   // active elements left in this CTA
+    __shared__ int s_woff[NWARP + 1];
     __syncthreads();
     if (threadIdx.x == 0) {
       int tot = 0;
-      for (int w = 0; w < NWARP; ++w) tot += c.list_cnt[w];
+      for (int w = 0; w < NWARP; ++w) { s_woff[w] = tot; tot += c.list_cnt[w]; }
+      s_woff[NWARP] = tot;
       c.out[2 * cmd.ncand] = (double)tot;
+      c.out[2 * cmd.ncand + 1] = tot > GATHER_BLK ? 1.0 : 0.0;
       c.blk_cnt[blockIdx.x] = tot;
     }
     __syncthreads();
+    if (s_woff[NWARP] <= GATHER_BLK) {
+      // publish this CTA's items and fixed sums in its own region: when the
+      // total is small enough, every CTA loads them after the barrier and
+      // the walk continues CTA-locally without a separate gather pass
+      const Problem& P = c.plan->P;
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      const uint32_t* __restrict__ Lst = c.list + (size_t)warp * c.list_cap;
+      const int cnt = c.list_cnt[warp];
+      const size_t base = (size_t)blockIdx.x * GATHER_BLK + s_woff[warp];
+      double* __restrict__ g_a = c.g_a;
+      double* __restrict__ g_r = c.g_r;
+      int* __restrict__ g_row = c.g_row;
+      const int8_t* __restrict__ owner = P.owner;
+      const double* __restrict__ grad = P.grad;
+      const double* __restrict__ rho = P.rho;
+      const int64_t ld = P.ld;
+      for (int k = lane; k < cnt; k += 32) {
+        const uint32_t i = Lst[k];
+        const int row = owner ? (int)owner[i] : 0;
+        g_a[base + k] = grad[(int64_t)row * ld + i];
+        g_r[base + k] = rho[i];
+        g_row[base + k] = row;
+      }
+      if (threadIdx.x < m) {
+        c.g_fix[((size_t)blockIdx.x * MAX_M + threadIdx.x) * 2] = c.fixC[threadIdx.x];
+        c.g_fix[((size_t)blockIdx.x * MAX_M + threadIdx.x) * 2 + 1] = c.fixS[threadIdx.x];
+      }
+    }
   }
 }
 
@@ -752,6 +844,154 @@ __device__ __noinline__ void gather_load(const PassCtx& c, int nb) {
   __syncthreads();
 }
 
+// Fused gather: after the barrier of a compacted sweep in which every CTA
+// published its (<= GATHER_BLK) items in its own region, every CTA loads all
+// of them in CTA order (the order pass_gather + gather_load would give) and
+// sums the fixed totals over the CTAs in index order.
+__device__ __noinline__ void gather_load_fused(const PassCtx& c, int nb) {
+  const int m = c.plan->P.m;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // locals: stores through the (generic) item pointers would otherwise force
+  // a reload of every context field after each store
+  int* __restrict__ s_off = reinterpret_cast<int*>(c.smem);   // [nb + 1] item offsets
+  const int* __restrict__ blk_cnt = c.blk_cnt;
+  const double* __restrict__ g_a = c.g_a;
+  const double* __restrict__ g_r = c.g_r;
+  const int* __restrict__ g_row = c.g_row;
+  const double* __restrict__ g_fix = c.g_fix;
+  double* __restrict__ it_a = c.it_a;
+  double* __restrict__ it_r = c.it_r;
+  int8_t* __restrict__ it_row = c.it_row;
+  double* __restrict__ fixC = c.fixC;
+  double* __restrict__ fixS = c.fixS;
+  int* __restrict__ n_items = c.n_items;
+  if (warp == 0) {
+    int run = 0;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+      const int b = b0 + lane;
+      const int v = b < nb ? __ldcg(blk_cnt + b) : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (b < nb) s_off[b] = run + incl - v;
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) {
+      s_off[nb] = run;
+      *n_items = run < GATHER_CAP ? run : GATHER_CAP;
+    }
+  }
+  __syncthreads();
+  // destination-major: item t sits in the CTA b with s_off[b] <= t < s_off[b+1]
+  // (binary search); four items' loads are issued together per thread
+  const int total = *n_items;
+  for (int t0 = threadIdx.x; t0 < total; t0 += 4 * BLOCK) {
+    double va[4], vr[4];
+    int vw[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u * BLOCK;
+      va[u] = 0.0; vr[u] = 0.0; vw[u] = 0;
+      if (t < total) {
+        int lo = 0, hi = nb;   // s_off[lo] <= t < s_off[hi]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_off[mid] <= t) lo = mid; else hi = mid;
+        }
+        const size_t src = (size_t)lo * GATHER_BLK + (t - s_off[lo]);
+        va[u] = __ldcg(g_a + src);
+        vr[u] = __ldcg(g_r + src);
+        vw[u] = __ldcg(g_row + src);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u * BLOCK;
+      if (t < total) { it_a[t] = va[u]; it_r[t] = vr[u]; it_row[t] = (int8_t)vw[u]; }
+    }
+  }
+  for (int sl = warp; sl < 2 * m; sl += NWARP) {
+    double v = 0.0;
+    for (int b = lane; b < nb; b += 32) v += __ldcg(g_fix + (size_t)b * MAX_M * 2 + sl);
+    v = warp_reduce(0, v);
+    if (lane == 0) {
+      if (sl & 1) fixS[sl >> 1] = v; else fixC[sl >> 1] = v;
+    }
+  }
+  __syncthreads();
+}
+
+// CTA-local compaction of row j's gathered items against the walk window
+// (same predicate and folding as pass_sweep_row_compact): fixed items go
+// into fixC / fixS, the rest are compacted in order.  Every CTA holds the
+// same items and does the same arithmetic in the same order.
+__device__ __noinline__ void local_compact_row(const PassCtx& c, int j) {
+  const Problem& P = c.plan->P;
+  const double L = P.lower, U = P.upper;
+  const double wlo = c.cmd->wlo[j], whi = c.cmd->whi[j];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int s_wc[NWARP];
+  __shared__ int s_base;
+  double* __restrict__ it_a = c.it_a;
+  double* __restrict__ it_r = c.it_r;
+  int8_t* __restrict__ it_row = c.it_row;
+  double* __restrict__ sm = c.smem;
+  const int nit = *c.n_items;
+  if (threadIdx.x == 0) s_base = 0;
+  double nC = 0.0, nS = 0.0;
+  for (int c0 = 0; c0 < nit; c0 += BLOCK) {
+    const int k = c0 + threadIdx.x;
+    const bool valid = k < nit;
+    const double a = valid ? it_a[k] : 0.0, r = valid ? it_r[k] : 0.0;
+    const int8_t row = valid ? it_row[k] : (int8_t)-1;
+    bool fixed = false;
+    if (valid && row == j) {
+      const double lo = L - r, hi = U - r;
+      const double v1 = wlo * a, v2 = whi * a;
+      const int g1 = v1 < lo ? 0 : (v1 > hi ? 2 : 1);
+      const int g2 = v2 < lo ? 0 : (v2 > hi ? 2 : 1);
+      if (g1 == g2) {
+        fixed = true;
+        if (g1 == 0) nC += a * lo;
+        else if (g1 == 2) nC += a * hi;
+        else nS += a * a;
+      }
+    }
+    const bool keep = valid && !fixed;
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_wc[warp] = __popc(km);
+    __syncthreads();   // every read of this chunk is done before any write
+    int off = s_base;
+    for (int w = 0; w < warp; ++w) off += s_wc[w];
+    if (keep) {
+      const int dst = off + __popc(km & ((1u << lane) - 1u));
+      it_a[dst] = a; it_r[dst] = r; it_row[dst] = row;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w = 0; w < NWARP; ++w) tot += s_wc[w];
+      s_base += tot;
+    }
+  }
+  // fixed sums: fixed shuffle tree, warps in order
+  nC = warp_reduce(0, nC);
+  nS = warp_reduce(0, nS);
+  if (lane == 0) { sm[warp] = nC; sm[NWARP + warp] = nS; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double C = sm[0], S = sm[NWARP];
+    for (int w = 1; w < NWARP; ++w) { C += sm[w]; S += sm[NWARP + w]; }
+    c.fixC[j] += C;
+    c.fixS[j] += S;
+    *c.n_items = s_base;
+  }
+  __syncthreads();
+}
+
 // CTA-local sweep over the gathered items: totals go straight to tot[]
 // (no partials, no grid barrier; every CTA computes the same bits).
 template <int KC>
@@ -764,8 +1004,11 @@ __device__ __noinline__ void local_sweep_row(const PassCtx& c, int j, int b, int
   double R[KC], S[KC];
 #pragma unroll
   for (int k = 0; k < KC; ++k) { R[k] = 0.0; S[k] = 0.0; }
+  const double* __restrict__ it_a = c.it_a;
+  const double* __restrict__ it_r = c.it_r;
+  const int8_t* __restrict__ it_row = c.it_row;
   for (int k = threadIdx.x; k < nit; k += BLOCK)
-    if (c.it_row[k] == j) sweep_elem<KC>(c.it_a[k], c.it_r[k], y, cnt, L, U, R, S);
+    if (it_row[k] == j) sweep_elem<KC>(it_a[k], it_r[k], y, cnt, L, U, R, S);
   sweep_finish<KC>(y, cnt, R, S);
   const int warp = threadIdx.x >> 5;
   double* sred = c.smem;
@@ -792,6 +1035,7 @@ __device__ void local_sweep(const PassCtx& c, double* tot) {
   for (int j = 0; j < m; ++j) {
     const int b = cmd.row_start[j], cnt = cmd.row_start[j + 1] - b;
     if (cnt <= 0) continue;
+    if (cmd.compact) local_compact_row(c, j);
     if (cnt <= 4) local_sweep_row<4>(c, j, b, cnt, tot);
     else if (cnt <= 8) local_sweep_row<8>(c, j, b, cnt, tot);
     else local_sweep_row<MAX_K>(c, j, b, cnt, tot);

@@ -45,7 +45,9 @@ enum Phase : int32_t {
   PH_DONE = 6,
   PH_GATHER = 7        // copy the (small) active sets to every CTA; later sweeps run CTA-locally
 };
-constexpr int GATHER_CAP = 4096;   // max gathered active elements (all rows)
+constexpr int GATHER_CAP = 8192;   // max gathered active elements (all rows)
+constexpr int GATHER_BLK = 128;    // per-CTA items a compacted sweep publishes (fused gather)
+constexpr int GATHER_TRIGGER = 1024;   // go CTA-local at or below this many active items
 
 enum Status : int32_t {
   ST_OK = 0,
@@ -129,6 +131,8 @@ struct Cmd {
   // walk interval [wlo_j, whi_j]; elements whose clip region is the same at
   // both ends are folded into per-CTA fixed sums and dropped from the list.
   int32_t compact, local;        // local: sweep runs on the gathered items in each CTA
+  int32_t load_fused;            // the items were published by the last global sweep:
+  int32_t pad_cmd_;              // every CTA loads them before the first local sweep
   double wlo[MAX_M], whi[MAX_M];
 };
 

@@ -5,7 +5,9 @@
 #include <cstdlib>
 #include <vector>
 #include <cuda_runtime.h>
+#define TOPT_PB_VARIANT 1
 #include "../paper_2511_13905_b200/csrc/passes.cuh"
+__device__ int g_pb_variant;
 using namespace topt_b200;
 
 __global__ void __launch_bounds__(BLOCK, 1) k_sweep(const Plan* plan, double* part, int mode) {
@@ -63,6 +65,25 @@ int main() {
   Plan* dp; cudaMalloc(&dp, sizeof(Plan)); cudaMemcpy(dp, hp, sizeof(Plan), cudaMemcpyHostToDevice);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   const char* names[] = {"sweep K=16", "sweep K=8", "final", "prep", "step_reduce"};
+  if (getenv("PB_PREP")) {
+    for (int var = 0; var < 4; ++var) {
+      cudaMemcpyToSymbol(g_pb_variant, &var, sizeof(int));
+      for (int w = 0; w < 3; ++w) k_sweep<<<nsm, BLOCK>>>(dp, part, 3);
+      cudaEventRecord(e0);
+      for (int w = 0; w < 20; ++w) k_sweep<<<nsm, BLOCK>>>(dp, part, 3);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      printf("prep variant %d %8.2f us/launch\n", var, ms * 1e3 / 20);
+    }
+    for (int var = 0; var < 2; ++var) {   // empty kernel baseline
+      cudaEventRecord(e0);
+      for (int w = 0; w < 20; ++w) k_sweep<<<nsm, BLOCK>>>(dp, part, 99);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      printf("empty launch %8.2f us/launch\n", ms * 1e3 / 20);
+    }
+    return 0;
+  }
   for (int grid_mult : {1, 2, 4})
   for (int mode = 0; mode < 5; ++mode) {
     const int grid = nsm * grid_mult;
