@@ -29,6 +29,8 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int RED_SCRATCH = NWARP * 160;   // doubles (max NS = 16 + 136)
+constexpr size_t PLAN_SMEM = (sizeof(Plan) + 255) & ~size_t(255);
+constexpr size_t KPASS_SMEM = PLAN_SMEM + sizeof(double) * (size_t)NEWTON_STAGE;
 
 // Combine all CTAs' partial slots in a fixed order into totals[].  Group g
 // sums CTAs g, g+G, g+2G, ... sequentially (loads batched 8 deep, the
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass(Plan* plan, double* partials,
   c.fixC = c.fixS = nullptr;
   c.list_cap = 0;
   c.timed_out = nullptr;   // never streamed
+  c.stage = reinterpret_cast<double*>(reinterpret_cast<char*>(s_dyn) + PLAN_SMEM);
   run_pass(c);
   __threadfence();
   __syncthreads();
@@ -187,7 +190,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // partials in the same fixed order and runs the same controller step, so all
 // CTAs hold bit-identical commands without a second barrier or any global
 // command broadcast.  Partials are double-buffered across passes.
-constexpr size_t PLAN_SMEM = (sizeof(Plan) + 255) & ~size_t(255);
 
 struct GatherBufs {
   int* blk_cnt;
@@ -260,6 +262,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     c.it_row = reinterpret_cast<int8_t*>(c.it_r + GATHER_CAP);
     c.n_items = &s_nitems;
     c.timed_out = gb.timed_out;
+    c.stage = reinterpret_cast<double*>(s_work);   // lists / items / Newton staging
     if (sp.cmd.phase == PH_SWEEP && sp.cmd.local) {   // CTA-local sweep: no barrier
       local_sweep(c, s_tot);
 #ifdef TOPT_ICACHE_EXPERIMENT
@@ -613,6 +616,8 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
       dyn_smem = PLAN_SMEM + bytes;
     }
   }
+  // the work area also stages the Newton pass's Gram columns
+  dyn_smem = std::max(dyn_smem, PLAN_SMEM + sizeof(double) * (size_t)NEWTON_STAGE);
   plan_start(hp);
   int phase = hp.cmd.phase;
   if (persistent && phase != PH_DONE) {
@@ -658,7 +663,7 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
   if (int rc = plan_upload(ctx, hp)) return rc;
   for (int it = 0; phase != PH_DONE && it < 4096; ++it) {
     if (ctx->profile) cudaEventRecord(ctx->ev0, ctx->stream);
-    k_pass<<<ctx->grid, BLOCK, sizeof(Plan), ctx->stream>>>(ctx->d_plan, ctx->d_part,
+    k_pass<<<ctx->grid, BLOCK, KPASS_SMEM, ctx->stream>>>(ctx->d_plan, ctx->d_part,
                                                             ctx->d_counter, nullptr);
     ctx->launches++;
     CUDA_TRY(ctx, cudaGetLastError());
@@ -700,7 +705,7 @@ int run_plan_ranks(topt_b200_ctx* ctx, Plan& hp) {
   NcclApi& api = nccl();
   for (int it = 0; phase != PH_DONE && it < 4096; ++it) {
     if (ctx->profile) cudaEventRecord(ctx->ev0, ctx->stream);
-    k_pass<<<grid, BLOCK, sizeof(Plan), ctx->stream>>>(ctx->d_plan, ctx->d_part, ctx->d_counter,
+    k_pass<<<grid, BLOCK, KPASS_SMEM, ctx->stream>>>(ctx->d_plan, ctx->d_part, ctx->d_counter,
                                                        ctx->d_rank_tot);
     CUDA_TRY(ctx, cudaGetLastError());
     const ncclResult_t nr = api.AllGather(ctx->d_rank_tot, ctx->d_gathered, PMAX, ncclDouble,
@@ -880,7 +885,7 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   ok = ok && cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   ctx->max_dyn_smem) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sizeof(Plan)) == cudaSuccess;
+                                  (int)KPASS_SMEM) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_control, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sizeof(Plan)) == cudaSuccess;
   if (ok) {

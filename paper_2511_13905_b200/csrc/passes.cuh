@@ -136,7 +136,63 @@ struct PassCtx {
   int8_t* it_row;
   int* n_items;        // shared scalar
   int* timed_out;      // global flag: a streamed input chunk never arrived
+  double* stage;       // shared [NEWTON_STAGE] staging area (null if the launch has none)
 };
+
+// 16-byte vector access is used when every array of a pass is 16-byte
+// aligned (torch / cudaMalloc buffers are; an offset user pointer may not be).
+__device__ __forceinline__ bool al16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
+// ---- Row-pair streaming -------------------------------------------------------
+// Passes that read several element-aligned rows (rho, A rows, x, g, ...) for
+// every element load them as 16-byte pairs: each thread takes element pairs
+// (2q, 2q+1), q = i0, i0 + stride, ..., with every row's pair load issued
+// before any arithmetic (nr x 16 bytes in flight per thread).  Measured on
+// the B200 (tools/streambench.cu, 8 rows of 8.4M doubles, 1 CTA of 512
+// threads per SM): 5.5 TB/s, ahead of a 3-stage cp.async.bulk (TMA) +
+// mbarrier pipeline through shared memory at 4.3 TB/s, so the passes use
+// this.  Misaligned rows or an odd count fall back to one element at a time.
+constexpr int RP_MAXR = 9;
+struct StreamRows {
+  const double* row[RP_MAXR];
+  int nr;
+};
+
+// f(i, v): element i with v[r] = row r at i (r < nr; v[r] = 0 beyond).
+// Per thread the elements come in a fixed order (deterministic sums).
+template <int NR, typename F>
+__device__ __forceinline__ void rows_pairs(const PassCtx& c, const StreamRows& R, int64_t n,
+                                           F&& f) {
+  const int nr = R.nr;
+  const int64_t st = c.stride;
+  bool vec = (n & 1) == 0;
+  for (int r = 0; r < nr; ++r) vec = vec && al16(R.row[r]);
+  if (vec) {
+    const int64_t n2 = n >> 1;
+    for (int64_t q = c.i0; q < n2; q += st) {
+      double2 v2[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        v2[r] = r < nr ? reinterpret_cast<const double2*>(R.row[r])[q] : make_double2(0.0, 0.0);
+      double v[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) v[r] = v2[r].x;
+      f(2 * q, v);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) v[r] = v2[r].y;
+      f(2 * q + 1, v);
+    }
+    return;
+  }
+  for (int64_t i = c.i0; i < n; i += st) {
+    double v[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) v[r] = r < nr ? R.row[r][i] : 0.0;
+    f(i, v);
+  }
+}
 
 // Fill each warp's active list with all of its grid-stride elements (this
 // CTA owns i = blockIdx*BLOCK + tid + k*stride) and clear the fixed sums.
@@ -198,12 +254,6 @@ __device__ __forceinline__ ChunkRange chunk_range(const Problem& P, int k) {
   if (P.chunk <= 0) return {0, P.n};
   const int64_t lo = (int64_t)k * P.chunk;
   return {lo, lo + P.chunk < P.n ? lo + P.chunk : P.n};
-}
-
-// 16-byte vector access is used when every array of a pass is 16-byte
-// aligned (torch / cudaMalloc buffers are; an offset user pointer may not be).
-__device__ __forceinline__ bool al16(const void* p) {
-  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
 }
 
 // ---- PH_STEP_REDUCE: BB / PR+ sums --------------------
@@ -301,6 +351,59 @@ __device__ __forceinline__ void prep_elem(PrepAcc& A, double a, double r, double
   }
 }
 
+// Does an element's exact breakpoint num / a (the rounded quotient) possibly
+// lie below the filter value m (MAX: above it)?  Real arithmetic: num / a < m
+// <=> num < m a (a > 0), num > m a (a < 0).  The product and the quotient are
+// rounded, so the test keeps a 1e-14 relative (+1e-300 absolute) margin in
+// the element's favour, and says "maybe" outside the range it can check.
+template <bool MAX>
+__device__ __forceinline__ bool bp_may_beat(double num, double a, double m) {
+  const double t = m * a;
+  if (!(fabs(t) < 1e300) || !(fabs(num) < 1e300)) return true;
+  const double e = 1e-14 * fabs(t) + 1e-300;
+  const bool flip = (a > 0.0) == MAX;
+  return flip ? (num > t - e) : (num < t + e);
+}
+
+// prep_elem with the breakpoint divisions filtered against (fmin, fmax):
+// exact breakpoint values already seen by this warp (refreshed by the caller
+// with a warp min / max), so that records of one lane stop the divisions of
+// the others.  Elements that cannot beat them cannot be the global extremum
+// (the filter values are themselves element breakpoints).
+__device__ __forceinline__ void prep_elem_w(PrepAcc& A, double a, double r, double gd, bool dot,
+                                            double L, double U, double& fmin, double& fmax) {
+  const double lo = L - r, hi = U - r;
+  if (dot) {
+    const double p = gd * a;
+    A.v[PS_DOT] += p;
+    A.v[PS_DABS] += fabs(p);
+  }
+  const bool b0 = 0.0 < lo, a0 = 0.0 > hi;
+  A.v[PS_S0] += a * (b0 ? lo : (a0 ? hi : 0.0));
+  A.v[PS_SLOPE0] += (b0 || a0) ? 0.0 : a * a;
+  A.v[PS_T] += fabs(a) * dmax_(fabs(lo), fabs(hi));
+  if (fabs(a) >= kGradFloor) {
+    A.v[PS_ANY] += 1.0;
+    const bool pos = a > 0.0;
+    const double nmin = pos ? lo : hi, nmax = pos ? hi : lo;
+    if (bp_may_beat<false>(nmin, a, fmin) || bp_may_beat<true>(nmax, a, fmax)) {
+      const double c1 = lo / a, c2 = hi / a;
+      A.v[PS_BPLO] = dmin_(A.v[PS_BPLO], dmin_(c1, c2));
+      A.v[PS_BPHI] = dmax_(A.v[PS_BPHI], dmax_(c1, c2));
+      fmin = dmin_(fmin, A.v[PS_BPLO]);
+      fmax = dmax_(fmax, A.v[PS_BPHI]);
+    }
+  }
+}
+
+__device__ __forceinline__ void warp_minmax(double& fmin, double& fmax) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    fmin = dmin_(fmin, __shfl_xor_sync(0xffffffffu, fmin, o));
+    fmax = dmax_(fmax, __shfl_xor_sync(0xffffffffu, fmax, o));
+  }
+}
+
 __device__ __noinline__ void pass_prep(const PassCtx& c) {
   const Plan& pl = *c.plan;
   const Problem& P = pl.P;
@@ -383,6 +486,83 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
       }
     }
     block_reduce_store<PREP_SLOTS>(A.v, PREP_SLOTS, PH_PREP, 0, c.out, c.smem);
+    compact_init(c);
+    return;
+  }
+  // no partition, device-resident inputs: the direction pass and one pass
+  // per row over (a_j, rho, d) as 16-byte pairs, same per-element arithmetic
+  if (!owner && P.chunk <= 0) {
+    if (dir) {
+      StreamRows D;
+      D.nr = 3;
+      D.row[0] = g; D.row[1] = use_dp ? dp : g; D.row[2] = x;
+      const bool vo = al16(dout) && al16(rho);
+      if (vo && (n & 1) == 0) {
+        rows_pairs<3>(c, D, n, [&](int64_t i, const double (&v)[3]) {
+          const double d = use_dp ? v[0] + beta * v[1] : v[0];
+          dout[i] = d;
+          rho[i] = v[2] - wa * d;
+        });
+      } else {
+        for (int64_t i = c.i0; i < n; i += st) {
+          const double d = use_dp ? g[i] + beta * dp[i] : g[i];
+          dout[i] = d;
+          rho[i] = x[i] - wa * d;
+        }
+      }
+    }
+    for (int j = 0; j < m; ++j) {
+      PrepAcc A;
+#pragma unroll
+      for (int s2 = 0; s2 < PREP_SLOTS; ++s2) A.v[s2] = 0.0;   // bp_lo = bp_hi = 0 (:58)
+      StreamRows Rj;
+      Rj.nr = 3;
+      Rj.row[0] = P.grad + (int64_t)j * ld; Rj.row[1] = rho;
+      Rj.row[2] = dot ? (dir ? dout : gd_in) : rho;
+      // rho and d of element i were written by this same thread above (same
+      // element-to-thread map), so no barrier is needed between the loops
+      const double* __restrict__ ar = Rj.row[0];
+      const double* __restrict__ gdr = Rj.row[2];
+      if ((n & 1) == 0 && al16(ar) && al16(rho) && al16(gdr)) {
+        // 16-byte pairs, warp-uniform trip count: the breakpoint filter is
+        // refreshed with the warp's min / max every 4 steps
+        const int lane = threadIdx.x & 31;
+        const int64_t n2 = n >> 1;
+        const double2* __restrict__ A2 = reinterpret_cast<const double2*>(ar);
+        const double2* __restrict__ R2 = reinterpret_cast<const double2*>(rho);
+        const double2* __restrict__ D2 = reinterpret_cast<const double2*>(gdr);
+        double fmin = 0.0, fmax = 0.0;
+        constexpr int UP = 4;   // pairs in flight per thread
+        int step = 0;
+        for (int64_t qb = c.i0 - lane; qb < n2; qb += UP * st, ++step) {
+          double2 a2[UP], r2[UP], d2[UP];
+#pragma unroll
+          for (int u = 0; u < UP; ++u) {
+            const int64_t q = qb + u * st + lane;
+            const bool ok = q < n2;
+            a2[u] = ok ? A2[q] : make_double2(0.0, 0.0);
+            r2[u] = ok ? R2[q] : make_double2(0.0, 0.0);
+            d2[u] = (ok && dot) ? D2[q] : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int u = 0; u < UP; ++u) {
+            if (qb + u * st + lane < n2) {
+              const double g0 = dot ? (dir ? wa * d2[u].x : d2[u].x) : 0.0;
+              const double g1 = dot ? (dir ? wa * d2[u].y : d2[u].y) : 0.0;
+              prep_elem_w(A, a2[u].x, r2[u].x, g0, dot, L, U_, fmin, fmax);
+              prep_elem_w(A, a2[u].y, r2[u].y, g1, dot, L, U_, fmin, fmax);
+            }
+          }
+          warp_minmax(fmin, fmax);
+        }
+      } else {
+        rows_pairs<3>(c, Rj, n, [&](int64_t, const double (&v)[3]) {
+          const double gdv = dot ? (dir ? wa * v[2] : v[2]) : 0.0;
+          prep_elem(A, v[0], v[1], gdv, dot, L, U_);
+        });
+      }
+      block_reduce_store<PREP_SLOTS>(A.v, PREP_SLOTS, PH_PREP, j * PREP_SLOTS, c.out, c.smem);
+    }
     compact_init(c);
     return;
   }
@@ -503,6 +683,7 @@ constexpr int SQ_CAP = 64;   // NWARP * 2 * SQ_CAP doubles fit the reduction scr
 template <int KC>
 struct SweepAcc {
   double C[KC], S[KC];
+  double Sall;   // slopes of elements free at every candidate (p1 = 0, p2 = cnt)
   double* qa;    // this warp's queue (shared memory, SQ_CAP entries)
   double* qr;
   int qn;
@@ -513,6 +694,7 @@ struct SweepAcc {
                                        double L_, double U_) {
 #pragma unroll
     for (int k = 0; k < KC; ++k) { C[k] = 0.0; S[k] = 0.0; }
+    Sall = 0.0;
     qa = qa_; qr = qr_; qn = 0; y = y_; cnt = cnt_; L = L_; U = U_;
   }
   // all 32 lanes call push together (valid = this lane holds an element)
@@ -535,6 +717,11 @@ struct SweepAcc {
         const double cl = a * (pos ? lo : hi), ch = a * (pos ? hi : lo);
 #pragma unroll
         for (int k = 0; k < KC; ++k) C[k] += (k < p1) ? cl : ch;
+      } else if (p1 == 0 && p2 == cnt) {
+        // free at every candidate (a small |a| makes the window wide): its
+        // term is y_k a^2 for all k -- one slope sum, added to every S_k at
+        // the end (no clipped constant)
+        Sall += a * a;
       } else {
         need = true;
       }
@@ -559,6 +746,9 @@ struct SweepAcc {
     if (lane < qn) sweep_elem<KC>(qa[lane], qr[lane], y, cnt, L, U, C, S);
     qn = 0;
     __syncwarp();
+#pragma unroll
+    for (int k = 0; k < KC; ++k) S[k] += Sall;
+    Sall = 0.0;
   }
 };
 
@@ -583,6 +773,26 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
   SweepAcc<KC> acc;
   acc.init(c.smem + warp * 2 * SQ_CAP, c.smem + warp * 2 * SQ_CAP + SQ_CAP, c.cmd->cand_y + b,
            cnt, P.lower, P.upper);
+  StreamRows R;
+  R.nr = 2;
+  R.row[0] = ar;
+  R.row[1] = rho;
+  if (!owner && (n & 1) == 0 && al16(ar) && al16(rho)) {
+    // 16-byte pairs; the trip count is warp-uniform (push is warp-collective)
+    const int64_t n2 = n >> 1;
+    const double2* __restrict__ A2 = reinterpret_cast<const double2*>(ar);
+    const double2* __restrict__ R2 = reinterpret_cast<const double2*>(rho);
+    for (int64_t q0 = c.i0 - lane; q0 < n2; q0 += 2 * st) {
+      const int64_t qa = q0 + lane, qb = q0 + st + lane;
+      const bool oa = qa < n2, ob = qb < n2;
+      const double2 a0 = oa ? A2[qa] : make_double2(0.0, 0.0), r0 = oa ? R2[qa] : make_double2(0.0, 0.0);
+      const double2 a1 = ob ? A2[qb] : make_double2(0.0, 0.0), r1 = ob ? R2[qb] : make_double2(0.0, 0.0);
+      acc.push(oa, a0.x, r0.x);
+      acc.push(oa, a0.y, r0.y);
+      acc.push(ob, a1.x, r1.x);
+      acc.push(ob, a1.y, r1.y);
+    }
+  } else {
   constexpr int UL = 4;   // elements' loads in flight per lane
   for (int64_t i0 = c.i0 - lane; i0 < n; i0 += UL * st) {   // warp-uniform trip count
     double av[UL], rv[UL];
@@ -596,6 +806,7 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
     }
 #pragma unroll
     for (int u = 0; u < UL; ++u) acc.push(ok[u], av[u], rv[u]);
+  }
   }
   acc.flush();
   __syncthreads();   // queues (in c.smem) drained before the reduction reuses it
@@ -1043,6 +1254,58 @@ __device__ void local_sweep(const PassCtx& c, double* tot) {
 }
 
 // ---- PH_FEAS: stage-1 dots a_k . clip(y_j a_j) (projection.cpp:320-333) ---
+// Streamed: up to FEAS_GROUP candidates per pass over (rho, A), their m dots
+// each accumulated per thread in the reference's row order.
+constexpr int FEAS_GROUP = 4;
+__device__ __noinline__ void pass_feas_streamed(const PassCtx& c) {
+  constexpr int M = 8;
+  const Plan& pl = *c.plan;
+  const Problem& P = pl.P;
+  const Cmd& cmd = *c.cmd;
+  const double L = P.lower, U = P.upper;
+  const int m = P.m;
+  const int64_t n = P.n, ld = P.ld;
+  StreamRows R;
+  R.nr = m + 1;
+  R.row[0] = P.rho;
+  for (int k = 0; k < m && k + 1 < RP_MAXR; ++k) R.row[1 + k] = P.grad + (int64_t)k * ld;
+  for (int f0 = 0; f0 < cmd.nfeas; f0 += FEAS_GROUP) {
+    double acc[FEAS_GROUP][M];
+    int rj[FEAS_GROUP];
+    double yj[FEAS_GROUP];
+#pragma unroll
+    for (int g = 0; g < FEAS_GROUP; ++g) {
+      const bool on = f0 + g < cmd.nfeas;
+      rj[g] = on ? cmd.feas_row[f0 + g] : -1;
+      yj[g] = on ? cmd.feas_y[f0 + g] : 0.0;
+#pragma unroll
+      for (int k = 0; k < M; ++k) acc[g][k] = 0.0;
+    }
+    rows_pairs<M + 1>(c, R, n, [&](int64_t, const double (&v)[M + 1]) {
+      const double r = v[0];
+      const double lo = L - r, hi = U - r;
+#pragma unroll
+      for (int g = 0; g < FEAS_GROUP; ++g) {
+        double z = 0.0;
+        if (rj[g] >= 0 && yj[g] != 0.0) {
+          double arj = 0.0;
+#pragma unroll
+          for (int k = 0; k < M; ++k)
+            if (k == rj[g]) arj = v[1 + k];
+          z = 0.0 + yj[g] * arj;
+        }
+        const double dl = clipd(z, lo, hi);
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          if (k < m) acc[g][k] += v[1 + k] * dl;
+      }
+    });
+#pragma unroll
+    for (int g = 0; g < FEAS_GROUP; ++g)
+      if (f0 + g < cmd.nfeas) block_reduce_store<M>(acc[g], m, PH_FEAS, (f0 + g) * m, c.out, c.smem);
+  }
+}
+
 __device__ __noinline__ void pass_feas(const PassCtx& c) {
   const Plan& pl = *c.plan;
   const Problem& P = pl.P;
@@ -1052,6 +1315,10 @@ __device__ __noinline__ void pass_feas(const PassCtx& c) {
   const int64_t n = P.n, st = c.stride, ld = P.ld;
   const double* __restrict__ rho = P.rho;
   const double* __restrict__ grad = P.grad;
+  if (m <= 8) {   // 16-byte pairs, FEAS_GROUP candidates per pass
+    pass_feas_streamed(c);
+    return;
+  }
   for (int f = 0; f < cmd.nfeas; ++f) {
     const int rj = cmd.feas_row[f];
     const double yj = cmd.feas_y[f];
@@ -1074,6 +1341,107 @@ __device__ __noinline__ void pass_feas(const PassCtx& c) {
 
 // ---- PH_NEWTON: delta(y), h-dots and the free-set Gram A D A^T ------------
 // (eval_phi projection.cpp:279-298 and J_h projection.cpp:359-376)
+//
+// m <= 8: each warp takes 32 consecutive elements per step (one per lane,
+// the next step's loads already in flight), computes z, delta and the h-dots
+// per lane, and stages the free elements' columns a_.i in shared memory; lane
+// q then owns Gram entry q (and q + 32) of the packed upper triangle and
+// accumulates it over the 32 columns with FMA.  A thread thus holds 2 Gram
+// accumulators instead of m(m+1)/2 = 28 (m = 7), which kept the register
+// version spilling.  Column stride 9 doubles: the lanes' 8 writes of a column
+// and the 8 distinct row reads of an entry step are conflict-free broadcasts.
+constexpr int NW_ROWS = 8;
+constexpr int NW_STRIDE = 9;
+constexpr int NEWTON_STAGE = NWARP * 32 * NW_STRIDE;   // doubles
+__device__ __noinline__ void pass_newton_warp(const PassCtx& c, double* __restrict__ stage) {
+  const Plan& pl = *c.plan;
+  const Problem& P = pl.P;
+  const Cmd& cmd = *c.cmd;
+  const double L = P.lower, U = P.upper;
+  const int m = P.m;
+  const int64_t n = P.n, st = c.stride, ld = P.ld;
+  const double* __restrict__ rho = P.rho;
+  const double* __restrict__ grad = P.grad;
+  const bool want_gram = cmd.want_gram;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* __restrict__ sb = stage + warp * 32 * NW_STRIDE;
+  const int NG = m * (m + 1) / 2;
+  int j0 = 0, k0 = 0, j1 = 0, k1 = 0;
+  {
+    int q = 0;
+    for (int j = 0; j < m; ++j)
+      for (int k = j; k < m; ++k, ++q) {
+        if (q == lane) { j0 = j; k0 = k; }
+        if (q == lane + 32) { j1 = j; k1 = k; }
+      }
+  }
+  const bool e0 = lane < NG, e1 = lane + 32 < NG;
+  double G0 = 0.0, G1 = 0.0;
+  double h[NW_ROWS], y[NW_ROWS];
+#pragma unroll
+  for (int k = 0; k < NW_ROWS; ++k) { h[k] = 0.0; y[k] = (k < m) ? cmd.y[k] : 0.0; }
+  double na[NW_ROWS], nr = 0.0;
+  int64_t i = c.i0;
+#pragma unroll
+  for (int k = 0; k < NW_ROWS; ++k) na[k] = (i < n && k < m) ? grad[(int64_t)k * ld + i] : 0.0;
+  if (i < n) nr = rho[i];
+  for (int64_t ib = c.i0 - lane; ib < n; ib += st, i += st) {   // warp-uniform trip count
+    const bool ok = i < n;
+    double a[NW_ROWS];
+#pragma unroll
+    for (int k = 0; k < NW_ROWS; ++k) a[k] = na[k];
+    const double r = nr;
+    const int64_t inx = i + st;
+    const bool okn = inx < n;
+#pragma unroll
+    for (int k = 0; k < NW_ROWS; ++k) na[k] = (okn && k < m) ? grad[(int64_t)k * ld + inx] : 0.0;
+    nr = okn ? rho[inx] : 0.0;
+    const double lo = L - r, hi = U - r;
+    double z = 0.0;
+#pragma unroll
+    for (int k = 0; k < NW_ROWS; ++k)
+      if (k < m && y[k] != 0.0) z += y[k] * a[k];
+    const bool clipped = (z < lo) || (z > hi);
+    const double dl = clipd(z, lo, hi);
+    if (ok) {
+#pragma unroll
+      for (int k = 0; k < NW_ROWS; ++k) h[k] += a[k] * dl;
+    }
+    if (want_gram) {
+      const bool fr = ok && !clipped;
+#pragma unroll
+      for (int k = 0; k < NW_ROWS; ++k) sb[lane * NW_STRIDE + k] = fr ? a[k] : 0.0;
+      __syncwarp();
+#pragma unroll 8
+      for (int e = 0; e < 32; ++e) {
+        const double* col = sb + e * NW_STRIDE;
+        G0 = __fma_rn(col[j0], col[k0], G0);
+        G1 = __fma_rn(col[j1], col[k1], G1);
+      }
+      __syncwarp();
+    }
+  }
+  // pack: slots [0, m) h ; [m, m + NG) the Gram entries (one lane per entry
+  // and warp holds a value, the others add exact zeros)
+  constexpr int NS = NW_ROWS + NW_ROWS * (NW_ROWS + 1) / 2;
+  double v[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) v[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < NW_ROWS; ++k) if (k < m) v[k] = h[k];
+#pragma unroll
+  for (int q = 0; q < NS - NW_ROWS; ++q) {
+    if (e0 && q == lane) v[m + q] = G0;
+    if (e1 && q == lane + 32) v[m + q] = G1;
+  }
+  block_reduce_store<NS>(v, m + NG, PH_NEWTON, 0, c.out, c.smem);
+}
+
+// ---- PH_NEWTON: delta(y), h-dots and the free-set Gram A D A^T ------------
+// (eval_phi projection.cpp:279-298 and J_h projection.cpp:359-376)
+// Register version: per thread the h-dots and the packed Gram triangle (M
+// exact for m = 7: 28 accumulators); the rows come as 16-byte pairs
+// (rows_pairs), two elements' loads in flight per thread.
 template <int M>
 __device__ __noinline__ void pass_newton_m(const PassCtx& c) {
   const Plan& pl = *c.plan;
@@ -1091,11 +1459,7 @@ __device__ __noinline__ void pass_newton_m(const PassCtx& c) {
   for (int k = 0; k < M; ++k) { h[k] = 0.0; y[k] = (k < m) ? cmd.y[k] : 0.0; }
 #pragma unroll
   for (int k = 0; k < NG; ++k) G[k] = 0.0;
-  for (int64_t i = c.i0; i < n; i += st) {
-    double a[M];
-#pragma unroll
-    for (int k = 0; k < M; ++k) a[k] = (k < m) ? grad[(int64_t)k * ld + i] : 0.0;
-    const double r = rho[i];
+  auto elem = [&](const double (&a)[M], double r) {
     const double lo = L - r, hi = U - r;
     double z = 0.0;
 #pragma unroll
@@ -1110,7 +1474,26 @@ __device__ __noinline__ void pass_newton_m(const PassCtx& c) {
 #pragma unroll
       for (int j = 0; j < M; ++j)
 #pragma unroll
-        for (int k = j; k < M; ++k) G[q++] += a[j] * a[k];
+        for (int k = j; k < M; ++k) { G[q] = __fma_rn(a[j], a[k], G[q]); ++q; }
+    }
+  };
+  if (m + 1 <= RP_MAXR && M + 1 <= RP_MAXR) {
+    StreamRows R;
+    R.nr = m + 1;
+    R.row[0] = rho;
+    for (int k = 0; k < m; ++k) R.row[1 + k] = grad + (int64_t)k * ld;
+    rows_pairs<(M + 1 <= RP_MAXR ? M + 1 : RP_MAXR)>(c, R, n, [&](int64_t, const auto& v) {
+      double a[M];
+#pragma unroll
+      for (int k = 0; k < M; ++k) a[k] = (k < m && k + 1 < RP_MAXR) ? v[1 + k] : 0.0;
+      elem(a, v[0]);
+    });
+  } else {
+    for (int64_t i = c.i0; i < n; i += st) {
+      double a[M];
+#pragma unroll
+      for (int k = 0; k < M; ++k) a[k] = (k < m) ? grad[(int64_t)k * ld + i] : 0.0;
+      elem(a, rho[i]);
     }
   }
   // pack: slots [0, m) h ; [m, m + m(m+1)/2) upper-triangle of the m x m Gram
@@ -1150,6 +1533,34 @@ __device__ __noinline__ void pass_final_m(const PassCtx& c) {
   double yv[M], acc[M];
 #pragma unroll
   for (int k = 0; k < M; ++k) { yv[k] = (k < m) ? cmd.y[k] : 0.0; acc[k] = 0.0; }
+  if (!OWN && M <= 8) {   // streamed: rho and the rows staged by the TMA engine
+    StreamRows R;
+    R.nr = m + 1;
+    R.row[0] = rho;
+    for (int k = 0; k < m && k + 1 < RP_MAXR; ++k) R.row[1 + k] = grad + (int64_t)k * ld;
+    if (m + 1 <= RP_MAXR) {
+      rows_pairs<(M + 1 <= RP_MAXR ? M + 1 : RP_MAXR)>(c, R, n, [&](int64_t i, const auto& v) {
+        const double r = v[0];
+        double z = 0.0;
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          if (k < m && k + 1 < RP_MAXR && yv[k] != 0.0) z += yv[k] * v[1 + k];
+        const double lo = L - r, hi = Up - r;
+        const bool below = z < lo, above = z > hi;
+        const double dl = below ? lo : (above ? hi : z);
+        if (dout) dout[i] = dl;
+        if (xout) xout[i] = r + dl;
+        if (mout) mout[i] = below ? 1 : (above ? 2 : 0);
+        if (resid) {
+#pragma unroll
+          for (int k = 0; k < M; ++k)
+            if (k < m && k + 1 < RP_MAXR) acc[k] += v[1 + k] * dl;
+        }
+      });
+      if (resid) block_reduce_store<M>(acc, m, PH_FINAL, 0, c.out, c.smem);
+      return;
+    }
+  }
   for (int64_t i = c.i0; i < n; i += st) {
     const double r = rho[i];
     double z = 0.0;
@@ -1193,6 +1604,7 @@ __device__ __noinline__ void pass_final_m(const PassCtx& c) {
 __device__ void pass_final(const PassCtx& c) {
   const int m = c.plan->P.m;
   const bool own = c.plan->P.owner != nullptr;
+  if (!own && m == 7) { pass_final_m<7, false>(c); return; }
   if (own) {
     if (m <= 4) pass_final_m<4, true>(c);
     else if (m <= 8) pass_final_m<8, true>(c);
@@ -1208,6 +1620,13 @@ __device__ void pass_final(const PassCtx& c) {
 
 __device__ void pass_newton(const PassCtx& c) {
   const int m = c.plan->P.m;
+#ifdef TOPT_NEWTON_WARP
+  if (m <= NW_ROWS && c.stage) {
+    pass_newton_warp(c, c.stage);
+    return;
+  }
+#endif
+  if (m == 7) { pass_newton_m<7>(c); return; }
   if (m <= 1) pass_newton_m<1>(c);
   else if (m <= 2) pass_newton_m<2>(c);
   else if (m <= 4) pass_newton_m<4>(c);

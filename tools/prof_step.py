@@ -54,6 +54,7 @@ def trace(config="C2", seed=2):
     t, mk = allt[:64], allt[64:]
     t0 = t[0, 0]
     names = {0: "STEP", 1: "PREP", 2: "SWEEP", 3: "FEAS", 4: "NEWTON", 5: "FINAL", 7: "GATHER"}
+    print(p.name, "n", p.n, "m", p.m)
     for k in range(64):
         if t[k, 0] == 0:
             break
@@ -69,6 +70,8 @@ def trace(config="C2", seed=2):
 if __name__ == "__main__":
     if "--trace" in sys.argv:
         sys.argv.remove("--trace")
-        trace()
+        cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
+        seed = int(sys.argv[2]) if len(sys.argv) > 2 else {"C1": 1, "C2": 2, "C3": 3}.get(cfg, 4)
+        trace(cfg, seed)
     else:
         main()
