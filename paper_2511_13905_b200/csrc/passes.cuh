@@ -1533,30 +1533,54 @@ __device__ __noinline__ void pass_final_m(const PassCtx& c) {
   double yv[M], acc[M];
 #pragma unroll
   for (int k = 0; k < M; ++k) { yv[k] = (k < m) ? cmd.y[k] : 0.0; acc[k] = 0.0; }
-  if (!OWN && M <= 8) {   // streamed: rho and the rows staged by the TMA engine
-    StreamRows R;
-    R.nr = m + 1;
-    R.row[0] = rho;
-    for (int k = 0; k < m && k + 1 < RP_MAXR; ++k) R.row[1 + k] = grad + (int64_t)k * ld;
-    if (m + 1 <= RP_MAXR) {
-      rows_pairs<(M + 1 <= RP_MAXR ? M + 1 : RP_MAXR)>(c, R, n, [&](int64_t i, const auto& v) {
-        const double r = v[0];
+  if (!OWN && M + 1 <= RP_MAXR && (n & 1) == 0) {
+    // 16-byte pairs in and out (x_{t+1} / delta as double2, the mask as 2 bytes)
+    bool vec = al16(rho) && (!dout || al16(dout)) && (!xout || al16(xout)) &&
+               (!mout || (reinterpret_cast<uintptr_t>(mout) & 1u) == 0);
+    const double* rows[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      rows[k] = (k < m) ? grad + (int64_t)k * ld : rho;
+      vec = vec && al16(rows[k]);
+    }
+    if (vec) {
+      const int64_t n2 = n >> 1;
+      auto one = [&](double r, const double (&a)[M], bool& below, bool& above) {
         double z = 0.0;
 #pragma unroll
         for (int k = 0; k < M; ++k)
-          if (k < m && k + 1 < RP_MAXR && yv[k] != 0.0) z += yv[k] * v[1 + k];
+          if (k < m && yv[k] != 0.0) z += yv[k] * a[k];
         const double lo = L - r, hi = Up - r;
-        const bool below = z < lo, above = z > hi;
+        below = z < lo; above = z > hi;
         const double dl = below ? lo : (above ? hi : z);
-        if (dout) dout[i] = dl;
-        if (xout) xout[i] = r + dl;
-        if (mout) mout[i] = below ? 1 : (above ? 2 : 0);
         if (resid) {
 #pragma unroll
           for (int k = 0; k < M; ++k)
-            if (k < m && k + 1 < RP_MAXR) acc[k] += v[1 + k] * dl;
+            if (k < m) acc[k] += a[k] * dl;
         }
-      });
+        return dl;
+      };
+      for (int64_t q = c.i0; q < n2; q += st) {
+        const double2 r2 = reinterpret_cast<const double2*>(rho)[q];
+        double2 a2[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          a2[k] = (k < m) ? reinterpret_cast<const double2*>(rows[k])[q] : make_double2(0.0, 0.0);
+        double ax[M], ay[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) { ax[k] = a2[k].x; ay[k] = a2[k].y; }
+        bool b0, u0, b1, u1;
+        const double d0 = one(r2.x, ax, b0, u0);
+        const double d1 = one(r2.y, ay, b1, u1);
+        if (dout) reinterpret_cast<double2*>(dout)[q] = make_double2(d0, d1);
+        if (xout) reinterpret_cast<double2*>(xout)[q] = make_double2(r2.x + d0, r2.y + d1);
+        if (mout) {
+          uchar2 mk;
+          mk.x = b0 ? 1 : (u0 ? 2 : 0);
+          mk.y = b1 ? 1 : (u1 ? 2 : 0);
+          reinterpret_cast<uchar2*>(mout)[q] = mk;
+        }
+      }
       if (resid) block_reduce_store<M>(acc, m, PH_FINAL, 0, c.out, c.smem);
       return;
     }
