@@ -110,6 +110,22 @@ def make_problem(config, seed, world=1):
     raise SystemExit(f"--gpus > 1 is not supported for {config}")
 
 
+def progress(msg):
+    """Stage marks on stderr (the JSON line stays alone on stdout)."""
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
+def cpu_sample_problem(config, seed):
+    """The CPU baseline's bounded sample: the config itself, except C5, where
+    one reference step takes tens of minutes (Newton on 268M elements,
+    measured 461 s for a 1/16 slab) -- there the sample is the same generator
+    on a 1024 x 512 x 8 slab (n = 4.2M, 1/64 of C5)."""
+    from paper_2511_13905_b200 import synth
+    if config == "C5":
+        return synth.com_constrained(1024, 512, 8, seed)
+    return make_problem(config, seed)
+
+
 def cpu_reference_sample(p, budget_s=12.0, max_reps=50):
     """The reference's CPU path on this host: spec step (oracle.c) + the
     reference's own build+project (oracle/_ref), 1 thread, a bounded sample."""
@@ -137,7 +153,7 @@ def cpu_reference_sample(p, budget_s=12.0, max_reps=50):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    p = make_problem(args.config, args.seed)
+    p = cpu_sample_problem(args.config, args.seed)
     # each "step" is the bounded sample of one full reference step
     for _ in range(args.warmup):
         cpu_reference_sample(p, budget_s=0.0, max_reps=1)
@@ -169,6 +185,7 @@ def run_ours(args, rank, world):
 
     dev = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
+    progress("problem")
     gp = make_problem(args.config, args.seed, world)
     # contiguous element slab of this rank (z-slabs for the 3-D grids)
     lo, hi = rank * gp.n // world, (rank + 1) * gp.n // world
@@ -201,6 +218,7 @@ def run_ours(args, rank, world):
     def step():
         return prepared.run()
 
+    progress("warm-up")
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -238,6 +256,7 @@ def run_ours(args, rank, world):
         ms = float(t.item())
     clk = clocks.stop()
 
+    progress("e2e")
     # ---- e2e: pinned host inputs -> H2D -> step -> D2H x_new, d --------------
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
     H = {k: pin(getattr(gp, k)[lo:hi]) for k in ("x", "x_prev", "g", "g_prev", "d_prev")}
@@ -282,6 +301,7 @@ def run_ours(args, rank, world):
     h2d = 8 * n * (5 + m)
     d2h = 8 * n * 2
     # dominant kernel timing (all ranks take part: the passes are collective)
+    progress("kernel stats")
     kern = kernel_pass_stats(ctx, step, min(args.steps, 10), flush)
 
     if rank != 0:
@@ -295,7 +315,9 @@ def run_ours(args, rank, world):
     avg_launch_ms = kern.get("avg_ms")
     achieved = (per_launch_bytes / (avg_launch_ms * 1e-3) / 1e9) if avg_launch_ms else \
         (b_alg / (ms * 1e-3) / 1e9)
-    cpu = (cpu_reference_sample(make_problem(args.config, args.seed), budget_s=args.cpu_budget)
+    progress("cpu baseline")
+    cpu = (cpu_reference_sample(cpu_sample_problem(args.config, args.seed),
+                                budget_s=args.cpu_budget)
            if world == 1 else None)   # reported at N = 1 only
     line = {
         "metric": METRIC, "value": value, "unit": "design vars/s", "n_gpus": world,
@@ -367,11 +389,14 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--seed", type=int, default=2)
+    ap.add_argument("--seed", type=int, default=None,
+                    help="default: the config's own number (C1 -> 1, ..., C5 -> 5)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.seed is None:
+        args.seed = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C4p": 4, "C5": 5}.get(args.config, 1)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if world > 1:

@@ -1,0 +1,111 @@
+"""Full-size GPU checks of the Newton-path configs (C4, C4', C5).
+
+C4 (n = 8,388,608, m = 7) runs against the oracle on the same inputs.  The
+reference's Newton loop stops when its own sequentially summed ||Phi||_inf
+drops below tol_n = 1e-6 (projection.cpp:356); at this size that sum's
+rounding noise is itself ~1e-6 (its iterate-4 value 2.4e-6 is noise: the
+exactly summed value at that point is ~1e-8), so the reference takes 6
+iterations where ours -- tree-summed, ~1e-9 noise -- takes 4.  The test
+therefore asserts, besides path, duals, x (normwise 1e-12) and identical
+active masks: that our stopping point is converged in exact arithmetic
+(||Phi(y)||_inf <= tol_n with the h-dots summed in 80-bit extended precision)
+and that we never take MORE Newton iterations than the reference.
+
+C5 (n = 268,435,456) is beyond what the CPU reference can run in a test (one
+reference step takes tens of minutes); it is checked through size-independent
+properties: x_{t+1} and rho_tilde equal their defining elementwise formulas
+bit for bit (recomputed in numpy, the reference's operation order), bounds,
+determinism of two runs, and for the Newton path exact-arithmetic convergence.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2511_13905_b200 import api, synth
+
+pytestmark = pytest.mark.gpu
+
+TOL_N = 1e-6
+C_REG = 1e12
+
+
+def _z(y, grad):
+    """z = sum_{j: y_j != 0} y_j a_j in ascending j from 0.0 (projection.cpp:199-205)."""
+    z = np.zeros(grad.shape[1])
+    for j in range(grad.shape[0]):
+        if y[j] != 0.0:
+            z = z + y[j] * grad[j]
+    return z
+
+
+def _masks(y, grad, rho, lower=0.0, upper=1.0):
+    z = _z(y, grad)
+    return np.where(z < lower - rho, 1, np.where(z > upper - rho, 2, 0)).astype(np.uint8)
+
+
+def _phi_exact(y, grad, rho, ghat, is_eq, lower=0.0, upper=1.0):
+    """||Phi(y)||_inf (projection.cpp:279-296) with each h-dot summed in
+    80-bit extended precision (pairwise): error ~1e-10, far below tol_n."""
+    z = _z(y, grad)
+    delta = np.clip(z, lower - rho, upper - rho)
+    phi = []
+    for j in range(grad.shape[0]):
+        dot = float(np.sum((grad[j] * delta).astype(np.longdouble)))
+        h = dot + y[j] / C_REG - ghat[j]
+        phi.append(h if is_eq[j] else min(-y[j], -h))
+    return float(np.max(np.abs(phi)))
+
+
+def test_full_c4_newton_vs_oracle():
+    p = synth.CONFIGS["C4"](4)
+    ref = O.pgd_step(p)
+    rt, gd = ref["rho_tilde"], ref["gd_step"]
+    lin = api.ConstraintLinearization.build(p.m, p.n, p.grad, p.g_values, p.bounds_g, gd,
+                                            p.is_eq, p.partition)
+    res = api.project(rt, lin, p.lower, p.upper)
+    orc = O.project(rt, p.grad, p.g_values, p.bounds_g, gd, p.is_eq, p.partition, p.lower,
+                    p.upper)
+    assert res.path.name == orc["path"] == "newton"
+    assert res.converged and orc["converged"]
+    assert res.newton_iters <= orc["newton_iters"]
+    np.testing.assert_allclose(res.y, orc["y"], rtol=1e-9, atol=1e-9)
+    x_g, x_o = rt + res.delta, rt + orc["delta"]
+    assert np.max(np.abs(x_g - x_o)) <= 1e-12 * np.max(np.abs(x_o))
+    assert np.array_equal(_masks(res.y, p.grad, rt), _masks(orc["y"], p.grad, rt))
+    # both stopping points are converged in exact arithmetic
+    assert _phi_exact(res.y, p.grad, rt, lin.g_hat, p.is_eq) <= TOL_N
+    assert _phi_exact(orc["y"], p.grad, rt, lin.g_hat, p.is_eq) <= TOL_N
+
+
+def test_full_c5_properties():
+    torch = pytest.importorskip("torch")
+    p = synth.CONFIGS["C5"](5)
+    cu = lambda v: torch.from_numpy(np.ascontiguousarray(v)).cuda()  # noqa: E731
+    X = [cu(getattr(p, k)) for k in ("x", "x_prev", "g", "g_prev", "d_prev")]
+    A = cu(p.grad.reshape(-1))
+    out = {k: torch.empty(p.n, dtype=torch.float64, device="cuda")
+           for k in ("x_new", "d", "rho_tilde")}
+    r1 = api.pgd_step(*X, A, p.g_values, p.bounds_g, p.is_eq, None, t=p.t, out=out)
+    x1 = out["x_new"].cpu().numpy()
+    r2 = api.pgd_step(*X, A, p.g_values, p.bounds_g, p.is_eq, None, t=p.t, out=out)
+    x2 = out["x_new"].cpu().numpy()
+    assert np.array_equal(x1, x2) and np.array_equal(r1.y, r2.y)      # deterministic
+    d = out["d"].cpu().numpy()
+    rt = out["rho_tilde"].cpu().numpy()
+    del X, A, out
+    torch.cuda.empty_cache()
+    # the step's elementwise formulas, bit for bit
+    d_ref = p.g + r1.beta * p.d_prev if r1.beta != 0.0 else p.g.copy()
+    assert np.array_equal(d, d_ref)
+    assert np.array_equal(rt, p.x - r1.alpha * d_ref)       # omega = 1
+    z = _z(r1.y, p.grad)
+    delta = np.where(z < p.lower - rt, p.lower - rt, np.where(z > p.upper - rt, p.upper - rt, z))
+    assert np.array_equal(x1, rt + delta)
+    assert np.all(x1 >= p.lower - 1e-15) and np.all(x1 <= p.upper + 1e-15)
+    if r1.projection.path.name == "newton":
+        assert r1.projection.converged
+        assert _phi_exact(r1.y, p.grad, rt, r1.g_hat, p.is_eq) <= TOL_N
+    else:   # an accepted stage-1 row: every constraint within tol_n (projection.cpp:324-331)
+        for k in range(p.m):
+            v = float(np.sum((p.grad[k] * delta).astype(np.longdouble))) - r1.g_hat[k]
+            assert v <= TOL_N * 1.0001, (k, v)
