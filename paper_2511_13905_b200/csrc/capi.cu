@@ -215,6 +215,9 @@ struct PlanBlob {
   int w[PLAN_WORDS];
 };
 
+#ifdef TOPT_ICACHE_EXPERIMENT
+__device__ Plan g_plan_scratch[160];
+#endif
 __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
                                                    unsigned long long* trace, GatherBufs gb,
                                                    const __grid_constant__ PlanBlob blob) {
@@ -265,11 +268,6 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     c.stage = reinterpret_cast<double*>(s_work);   // lists / items / Newton staging
     if (sp.cmd.phase == PH_SWEEP && sp.cmd.local) {   // CTA-local sweep: no barrier
       local_sweep(c, s_tot);
-#ifdef TOPT_ICACHE_EXPERIMENT
-      if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[7] = gtimer();
-      __syncthreads();
-      local_sweep(c, s_tot);
-#endif
       if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
         tr[1] = tr[6] = tr[2] = tr[3] = gtimer();
         g_ctl_marks = trace + 512 + pass * 8;
@@ -294,6 +292,20 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
       tr[3] = gtimer();
       g_ctl_marks = trace + 512 + pass * 8;
     }
+#ifdef TOPT_ICACHE_EXPERIMENT
+    {  // controller twice on the same state: cold (first) vs warm (second) code
+      int* gp = reinterpret_cast<int*>(g_plan_scratch + blockIdx.x);
+      int* spi = reinterpret_cast<int*>(&sp);
+      for (int k = threadIdx.x; k < (int)(sizeof(Plan) / 4); k += BLOCK) gp[k] = spi[k];
+      __syncthreads();
+      if (threadIdx.x < 32) plan_consume_warp(sp, s_tot);
+      __syncthreads();
+      if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[7] = gtimer();
+      for (int k = threadIdx.x; k < (int)(sizeof(Plan) / 4); k += BLOCK) spi[k] = gp[k];
+      __syncthreads();
+      if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[3] = gtimer();
+    }
+#endif
     if (threadIdx.x < 32) plan_consume_warp(sp, s_tot);
     __syncthreads();
     if (sp.cmd.load_fused) {   // fused gather: the items were published by the sweep
@@ -427,6 +439,10 @@ struct topt_b200_ctx {
   uint32_t epoch = 0;
   int stream_inputs = 1;           // TOPT_B200_STREAM=0 disables
   Plan* hp_pin = nullptr;          // pinned staging of the plan (upload / results)
+  // contiguous-range partition detected by the last owner map built here
+  const int8_t* rng_owner = nullptr;
+  int rng_m = 0;
+  int64_t rng_lo[MAX_M] = {}, rng_hi[MAX_M] = {};
 };
 
 // ---- NCCL, resolved at run time (the process may already hold torch's copy)
@@ -810,8 +826,38 @@ int upload(topt_b200_ctx* ctx, int slot, const void* src, size_t bytes, void** d
   return TOPT_OK;
 }
 
+// Is every set of the partition one contiguous ascending index range?  (Host
+// scan of the index arrays; remembered with the owner map it belongs to.)
+void detect_ranges(topt_b200_ctx* ctx, int32_t m, const int64_t* off, const int32_t* idx,
+                   const int8_t* owner_dev) {
+  ctx->rng_owner = nullptr;
+  if (m < 1 || m > MAX_M) return;
+  for (int j = 0; j < m; ++j) {
+    const int64_t b = off[j], e = off[j + 1];
+    if (e <= b) return;
+    for (int64_t k = b + 1; k < e; ++k)
+      if (idx[k] != idx[k - 1] + 1) return;
+    ctx->rng_lo[j] = idx[b];
+    ctx->rng_hi[j] = (int64_t)idx[e - 1] + 1;
+  }
+  ctx->rng_m = m;
+  ctx->rng_owner = owner_dev;
+}
+
+void apply_ranges(const topt_b200_ctx* ctx, Problem& P) {
+  P.part_ranges = 0;
+  if (!P.owner || P.owner != ctx->rng_owner || P.m != ctx->rng_m) return;
+  for (int j = 0; j < P.m; ++j) {
+    if (ctx->rng_lo[j] < 0 || ctx->rng_hi[j] > P.n) return;
+    P.row_lo[j] = ctx->rng_lo[j];
+    P.row_hi[j] = ctx->rng_hi[j];
+  }
+  P.part_ranges = 1;
+}
+
 int owner_map_impl(topt_b200_ctx* ctx, int64_t n, int32_t m, const int64_t* off,
                    const int32_t* idx, int8_t* owner_dev) {
+  detect_ranges(ctx, m, off, idx, owner_dev);
   int32_t* o32 = (int32_t*)buf(ctx, B_OWNER32, sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1));
   if (!o32) return fail(ctx, TOPT_ERR_CUDA, "cudaMalloc failed");
   const int64_t total = off[m];
@@ -1068,6 +1114,7 @@ static int stage_lin(topt_b200_ctx* ctx, Plan& hp, const topt_linearization* lin
     if (rc) return rc;
     hp.P.owner = own;
     hp.P.has_part = 1;
+    apply_ranges(ctx, hp.P);
   }
   return TOPT_OK;
 }
@@ -1227,6 +1274,7 @@ int topt_b200_project_dev(topt_b200_ctx* ctx, int which, const double* rho_tilde
   hp.P.gd_step = lin->gd_step;
   const bool use_part = lin->owner && which != W_SINGLE && which != W_NEWTON && m > 1;
   hp.P.owner = use_part ? lin->owner : nullptr;
+  apply_ranges(ctx, hp.P);
   hp.P.has_part = use_part ? 1 : 0;
   hp.P.rho = const_cast<double*>(rho_tilde);
   hp.P.delta_out = delta_out;
@@ -1302,6 +1350,7 @@ int topt_b200_pgd_step_dev(topt_b200_ctx* ctx, const topt_step_problem* prob,
   P.x = prob->x; P.x_prev = prob->x_prev; P.g = prob->g; P.g_prev = prob->g_prev;
   P.d_prev = prob->d_prev; P.grad = prob->grad;
   P.owner = (prob->owner && prob->m > 1) ? prob->owner : nullptr;
+  apply_ranges(ctx, P);
   P.has_part = P.owner ? 1 : 0;
   P.rho = out->rho_tilde; P.d_out = out->d; P.x_out = out->x_new; P.delta_out = out->delta;
   P.mask_out = out->mask;
@@ -1348,6 +1397,7 @@ int topt_b200_pgd_step(topt_b200_ctx* ctx, const topt_step_problem* prob,
     if ((rc = owner_map_impl(ctx, n, m, prob->part_offsets, prob->part_indices, own))) return rc;
     P.owner = own;
     P.has_part = 1;
+    apply_ranges(ctx, P);
   }
   P.rho = (double*)buf(ctx, B_RHO, nb);
   P.d_out = (double*)buf(ctx, B_D, nb);

@@ -489,9 +489,11 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
     compact_init(c);
     return;
   }
-  // no partition, device-resident inputs: the direction pass and one pass
-  // per row over (a_j, rho, d) as 16-byte pairs, same per-element arithmetic
-  if (!owner && P.chunk <= 0) {
+  // device-resident inputs, no partition or a partition of contiguous index
+  // ranges: the direction pass and one pass per row over (a_j, rho, d) as
+  // 16-byte pairs (a range row only over its own range; outside it only a_j
+  // is read, for the validation count), same per-element arithmetic
+  if ((!owner || P.part_ranges) && P.chunk <= 0) {
     if (dir) {
       StreamRows D;
       D.nr = 3;
@@ -523,18 +525,40 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
       // element-to-thread map), so no barrier is needed between the loops
       const double* __restrict__ ar = Rj.row[0];
       const double* __restrict__ gdr = Rj.row[2];
-      if ((n & 1) == 0 && al16(ar) && al16(rho) && al16(gdr)) {
+      const int64_t rlo = owner ? P.row_lo[j] : 0, rhi = owner ? P.row_hi[j] : n;
+      if (owner) {   // validation (projection.cpp:173-180): a_j must vanish outside its set
+        int nz = 0;
+        auto scan = [&](int64_t b, int64_t e) {   // count a_ji != 0 for i in [b, e)
+          if (((b | e) & 1) == 0 && al16(ar)) {
+            const double2* __restrict__ A2 = reinterpret_cast<const double2*>(ar);
+            const int64_t e2 = e >> 1;
+            for (int64_t q = (b >> 1) + c.i0; q < e2; q += 4 * st) {
+              double2 v[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                v[u] = q + u * st < e2 ? A2[q + u * st] : make_double2(0.0, 0.0);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) nz += (v[u].x != 0.0) + (v[u].y != 0.0);
+            }
+          } else {
+            for (int64_t i = b + c.i0; i < e; i += st) nz += ar[i] != 0.0;
+          }
+        };
+        scan(0, rlo);
+        scan(rhi, n);
+        A.v[PS_NZOUT] = (double)nz;
+      }
+      if (((rlo | rhi) & 1) == 0 && al16(ar) && al16(rho) && al16(gdr)) {
         // 16-byte pairs, warp-uniform trip count: the breakpoint filter is
-        // refreshed with the warp's min / max every 4 steps
+        // refreshed with the warp's min / max every step
         const int lane = threadIdx.x & 31;
-        const int64_t n2 = n >> 1;
+        const int64_t q0 = rlo >> 1, n2 = rhi >> 1;
         const double2* __restrict__ A2 = reinterpret_cast<const double2*>(ar);
         const double2* __restrict__ R2 = reinterpret_cast<const double2*>(rho);
         const double2* __restrict__ D2 = reinterpret_cast<const double2*>(gdr);
         double fmin = 0.0, fmax = 0.0;
         constexpr int UP = 4;   // pairs in flight per thread
-        int step = 0;
-        for (int64_t qb = c.i0 - lane; qb < n2; qb += UP * st, ++step) {
+        for (int64_t qb = q0 + c.i0 - lane; qb < n2; qb += UP * st) {
           double2 a2[UP], r2[UP], d2[UP];
 #pragma unroll
           for (int u = 0; u < UP; ++u) {
@@ -556,10 +580,10 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
           warp_minmax(fmin, fmax);
         }
       } else {
-        rows_pairs<3>(c, Rj, n, [&](int64_t, const double (&v)[3]) {
-          const double gdv = dot ? (dir ? wa * v[2] : v[2]) : 0.0;
-          prep_elem(A, v[0], v[1], gdv, dot, L, U_);
-        });
+        for (int64_t i = rlo + c.i0; i < rhi; i += st) {
+          const double gdv = dot ? (dir ? wa * gdr[i] : gdr[i]) : 0.0;
+          prep_elem(A, ar[i], rho[i], gdv, dot, L, U_);
+        }
       }
       block_reduce_store<PREP_SLOTS>(A.v, PREP_SLOTS, PH_PREP, j * PREP_SLOTS, c.out, c.smem);
     }
@@ -777,12 +801,14 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
   R.nr = 2;
   R.row[0] = ar;
   R.row[1] = rho;
-  if (!owner && (n & 1) == 0 && al16(ar) && al16(rho)) {
-    // 16-byte pairs; the trip count is warp-uniform (push is warp-collective)
-    const int64_t n2 = n >> 1;
+  const int64_t rlo = owner ? P.row_lo[j] : 0, rhi = owner ? P.row_hi[j] : n;
+  if ((!owner || P.part_ranges) && ((rlo | rhi) & 1) == 0 && al16(ar) && al16(rho)) {
+    // 16-byte pairs over the row's elements (its own range for a range
+    // partition); the trip count is warp-uniform (push is warp-collective)
+    const int64_t n2 = rhi >> 1;
     const double2* __restrict__ A2 = reinterpret_cast<const double2*>(ar);
     const double2* __restrict__ R2 = reinterpret_cast<const double2*>(rho);
-    for (int64_t q0 = c.i0 - lane; q0 < n2; q0 += 2 * st) {
+    for (int64_t q0 = (rlo >> 1) + c.i0 - lane; q0 < n2; q0 += 2 * st) {
       const int64_t qa = q0 + lane, qb = q0 + st + lane;
       const bool oa = qa < n2, ob = qb < n2;
       const double2 a0 = oa ? A2[qa] : make_double2(0.0, 0.0), r0 = oa ? R2[qa] : make_double2(0.0, 0.0);

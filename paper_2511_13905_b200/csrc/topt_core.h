@@ -181,6 +181,12 @@ struct Problem {
   int64_t chunk;                // 0: inputs already resident
   uint32_t epoch;
   int32_t nchunk;
+  // Partition whose every set is a contiguous ascending index range (e.g.
+  // the channel-major material blocks of C3): set j = [row_lo[j], row_hi[j]).
+  // The passes then visit each row's own range instead of all n elements.
+  int32_t part_ranges;
+  int32_t pad1_;
+  int64_t row_lo[MAX_M], row_hi[MAX_M];
 };
 
 // Controller-visible result.

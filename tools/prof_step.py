@@ -62,7 +62,7 @@ def trace(config="C2", seed=2):
               f"b0-end {1e-3*(t[k,1]-t[k,0]):7.2f} last-end {1e-3*(t[k,6]-t[k,0]):7.2f} "
               f"fin-start {1e-3*(t[k,2]-t[k,0]):7.2f} reduce {1e-3*(t[k,3]-t[k,2]):6.2f} "
               f"control {1e-3*(t[k,4]-t[k,3]):6.2f}" +
-              (f" t7 {1e-3*(t[k,7]-t[k,0]):7.2f}" if t[k, 7] else "") +
+              (f" cold-ctl {1e-3*(t[k,7]-t[k,2]):6.2f}" if t[k, 7] else "") +
               (" | marks " + " ".join(f"{k2}:{1e-3*(mk[k,k2]-t[k,3]):6.2f}" for k2 in range(8) if mk[k,k2])
                if mk[k].any() else ""))
 
