@@ -432,11 +432,12 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
     const bool vec = al16(g) && al16(x) && al16(ar) && al16(dout) && al16(rho) &&
                      (!use_dp || al16(dp));
     // d = g + beta d_prev ; gd = (omega alpha) d ; rho = x - gd
+    double fmin = 0.0, fmax = 0.0;   // warp-shared breakpoint filter (prep_elem_w)
     auto elem = [&](double gv, double dv, double xv, double av, double& d, double& r) {
       d = use_dp ? gv + beta * dv : gv;
       const double gd = wa * d;
       r = xv - gd;
-      prep_elem(A, av, r, gd, dot, L, U_);
+      prep_elem_w(A, av, r, gd, dot, L, U_, fmin, fmax);
     };
     for (int k = 0; k < nch; ++k) {
       if (P.chunk > 0) wait_chunk(P.in_flags + P.nchunk + k, P.epoch, c.timed_out);
@@ -449,25 +450,31 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
         double2* __restrict__ DO = reinterpret_cast<double2*>(dout);
         double2* __restrict__ RO = reinterpret_cast<double2*>(rho);
         const int64_t q1 = cr.hi >> 1;
-        for (int64_t q = (cr.lo >> 1) + c.i0; q < q1; q += 2 * st) {
-          const bool ok1 = q + st < q1;
+        const int lane = threadIdx.x & 31;
+        // warp-uniform trip count (the filter refresh is a warp shuffle)
+        for (int64_t qb = (cr.lo >> 1) + c.i0 - lane; qb < q1; qb += 2 * st) {
+          const int64_t q = qb + lane;
+          const bool ok0 = q < q1, ok1 = q + st < q1;
           const double2 z2 = make_double2(0.0, 0.0);
-          const double2 g0 = G2[q], x0 = X2[q], a0 = A2[q];
-          const double2 d0 = use_dp ? D2[q] : z2;
+          const double2 g0 = ok0 ? G2[q] : z2, x0 = ok0 ? X2[q] : z2, a0 = ok0 ? A2[q] : z2;
+          const double2 d0 = (ok0 && use_dp) ? D2[q] : z2;
           const double2 g1 = ok1 ? G2[q + st] : z2, x1 = ok1 ? X2[q + st] : z2;
           const double2 a1 = ok1 ? A2[q + st] : z2;
           const double2 d1 = (ok1 && use_dp) ? D2[q + st] : z2;
           double2 dd, rr;
-          elem(g0.x, d0.x, x0.x, a0.x, dd.x, rr.x);
-          elem(g0.y, d0.y, x0.y, a0.y, dd.y, rr.y);
-          DO[q] = dd;
-          RO[q] = rr;
+          if (ok0) {
+            elem(g0.x, d0.x, x0.x, a0.x, dd.x, rr.x);
+            elem(g0.y, d0.y, x0.y, a0.y, dd.y, rr.y);
+            DO[q] = dd;
+            RO[q] = rr;
+          }
           if (ok1) {
             elem(g1.x, d1.x, x1.x, a1.x, dd.x, rr.x);
             elem(g1.y, d1.y, x1.y, a1.y, dd.y, rr.y);
             DO[q + st] = dd;
             RO[q + st] = rr;
           }
+          warp_minmax(fmin, fmax);
         }
         if ((cr.hi & 1) && c.i0 == 0) {   // odd tail element
           const int64_t i = cr.hi - 1;
