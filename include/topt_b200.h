@@ -166,6 +166,28 @@ int64_t topt_b200_kernel_launches(const topt_b200_ctx* ctx);
 void* topt_b200_get_stream(const topt_b200_ctx* ctx);
 int topt_b200_set_stream(topt_b200_ctx* ctx, void* stream);
 
+/* Structured constraint rows (extension beyond the reference interface;
+ * SURVEY.md §8(f) rank 1).  Rows the caller can describe instead of storing:
+ *   TOPT_ROW_DENSE     row k of prob->grad (as usual)
+ *   TOPT_ROW_CONST     a_i = value                      (volume rows)
+ *   TOPT_ROW_CENTROID  a_i = sign * ((c_axis(i) + 0.5) - center) / scale
+ * where c_axis(i) is the integer coordinate of global element
+ * i + index_offset on the x-fastest grid[0] x grid[1] x grid[2]
+ * (grid.hpp:29-33; the centre-of-mass rows of SPEC.md:405).  The values are
+ * bit-identical to the dense rows the same formulas produce, and the passes
+ * then never read them from memory.  Applies to the following
+ * topt_b200_pgd_step_dev / topt_b200_pgd_step_ranks calls on this context
+ * (2 <= m <= 8, no partition, even n); rows = NULL clears it. */
+enum { TOPT_ROW_DENSE = 0, TOPT_ROW_CONST = 1, TOPT_ROW_CENTROID = 2 };
+typedef struct {
+  int32_t kind;
+  int32_t axis;                    /* CENTROID: 0 x, 1 y, 2 z */
+  double value;                    /* CONST */
+  double center, scale, sign;      /* CENTROID */
+} topt_row_desc;
+int topt_b200_set_structured_rows(topt_b200_ctx* ctx, int32_t m, const topt_row_desc* rows,
+                                  const int64_t* grid, int64_t index_offset);
+
 /* Per-launch device timing of the pass kernel (CUDA events on the launching
  * stream).  When enabled, every pass launch is bracketed by events; the
  * accumulated device time and launch count are returned (and reset). */

@@ -78,6 +78,7 @@ EXPORTS = [
     "topt_b200_set_profiling", "topt_b200_kernel_time", "topt_b200_step_time",
     "topt_b200_debug_trace",
     "topt_b200_nccl_unique_id", "topt_b200_ctx_create_ranks", "topt_b200_pgd_step_ranks",
+    "topt_b200_set_structured_rows",
 ]
 
 _lib = None
@@ -123,6 +124,7 @@ def load():
         "topt_b200_ctx_create_ranks": [C.c_int, C.c_int, C.c_int, vp, C.POINTER(C.c_void_p)],
         "topt_b200_pgd_step_ranks": [vp, vp, i64, vp, vp, vp, vp, vp],
         "topt_b200_default_options": [vp],
+        "topt_b200_set_structured_rows": [vp, i32, vp, vp, i64],
         "topt_b200_default_settings": [vp],
     }
     for name, args in sig.items():
@@ -149,6 +151,13 @@ def nccl_unique_id() -> bytes:
     if rc != OK:
         raise RuntimeError(f"topt_b200_nccl_unique_id failed ({rc}): NCCL not loadable")
     return bytes(buf)
+
+
+class RowDesc(C.Structure):
+    """topt_row_desc: DENSE (0), CONST (1, a_i = value) or CENTROID
+    (2, a_i = sign * ((coord_axis(i) + 0.5) - center) / scale)."""
+    _fields_ = [("kind", C.c_int32), ("axis", C.c_int32), ("value", C.c_double),
+                ("center", C.c_double), ("scale", C.c_double), ("sign", C.c_double)]
 
 
 class Context:
@@ -197,6 +206,18 @@ class Context:
 
     def set_stream(self, stream_ptr: int):
         self.lib.topt_b200_set_stream(self.h, C.c_void_p(stream_ptr))
+
+    def set_structured_rows(self, rows, grid=None, index_offset: int = 0):
+        """Structured constraint rows for the following device steps (None
+        clears): a list of RowDesc, one per constraint row."""
+        if not rows:
+            self.lib.topt_b200_set_structured_rows(self.h, 0, None, None, 0)
+            return
+        arr = (RowDesc * len(rows))(*rows)
+        g = (C.c_int64 * 3)(*[int(v) for v in grid])
+        rc = self.lib.topt_b200_set_structured_rows(self.h, len(rows), arr, g, int(index_offset))
+        if rc != OK:
+            raise RuntimeError(self.last_error())
 
     def set_profiling(self, on: bool):
         self.lib.topt_b200_set_profiling(self.h, 1 if on else 0)

@@ -396,12 +396,19 @@ class PreparedStep:
     loop, the benchmark) pay only the library call.  `run()` executes the
     step; `result()` wraps the last outputs like pgd_step's return value."""
 
-    def __init__(self, ctx, fn, args, keep, m, outs):
+    def __init__(self, ctx, fn, args, keep, m, outs, rows=None):
         self.ctx, self._fn, self._args, self._keep, self.m = ctx, fn, args, keep, m
         self._outs = outs
+        self._rows = rows   # (RowDesc list, grid, index_offset) or None
 
     def run(self):
-        _check(self.ctx, self._fn(*self._args))
+        if self._rows is not None:
+            self.ctx.set_structured_rows(*self._rows)
+        try:
+            _check(self.ctx, self._fn(*self._args))
+        finally:
+            if self._rows is not None:
+                self.ctx.set_structured_rows(None)
         return self
 
     def result(self) -> StepResult:
@@ -438,10 +445,16 @@ def prepare_pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_
                      settings: PgdSettings = None, device: int = 0, want_delta=False,
                      want_mask=False, out=None,
                      host_outputs=("x_new", "d", "rho_tilde"), ctx: L.Context = None,
-                     n_global: int = None, row_counts=None) -> PreparedStep:
+                     n_global: int = None, row_counts=None, rows=None, grid=None,
+                     index_offset: int = 0) -> PreparedStep:
     """pgd_step's argument handling without the call: returns a PreparedStep
     whose run() executes the step on these buffers (the arrays are referenced,
-    not copied, so updating them in place between runs is allowed)."""
+    not copied, so updating them in place between runs is allowed).
+
+    rows / grid / index_offset (device tensors only): structured constraint
+    rows (a list of dicts {kind: "dense"|"const"|"centroid", value, axis,
+    center, scale, sign}); generated rows are never read from `grad`, which
+    may then be None."""
     settings = settings or PgdSettings()
     ctx = ctx or L.context(device)
     dev = _is_torch_cuda(x)
@@ -478,7 +491,7 @@ def prepare_pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_
                                                     _ptr(idx), C.c_void_p(owner.data_ptr())))
         for f, a in (("x", x), ("x_prev", x_prev), ("g", g), ("g_prev", g_prev),
                      ("d_prev", d_prev), ("grad", grad)):
-            setattr(pr, f, a.data_ptr())
+            setattr(pr, f, a.data_ptr() if a is not None else None)
         pr.g_values, pr.bounds_g = _ptr(gv), _ptr(bg)
         pr.is_equality = _ptr(ie)
         pr.part_offsets, pr.part_indices = _ptr(off), _ptr(idx)
@@ -523,5 +536,14 @@ def prepare_pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_
         keep = [arrs]
     keep += [pr, sc, opts, o, meta, gv, bg, ie, off, idx]
     outs = dict(meta=meta, delta=delta, y=y, sl=sl, gh=gh, mask=mask, x_new=x_new, d=d, rt=rt)
-    return PreparedStep(ctx, fn, args, keep, m, outs)
+    srows = None
+    if rows is not None:
+        if not dev:
+            raise ValueError("structured rows need device (torch CUDA) inputs")
+        kinds = {"dense": 0, "const": 1, "centroid": 2}
+        descs = [L.RowDesc(kinds[r["kind"]], int(r.get("axis", 0)), float(r.get("value", 0.0)),
+                           float(r.get("center", 0.0)), float(r.get("scale", 1.0)),
+                           float(r.get("sign", 1.0))) for r in rows]
+        srows = (descs, grid, index_offset)
+    return PreparedStep(ctx, fn, args, keep, m, outs, srows)
 

@@ -141,6 +141,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass(Plan* plan, double* partials,
   c.list_cap = 0;
   c.timed_out = nullptr;   // never streamed
   c.stage = reinterpret_cast<double*>(reinterpret_cast<char*>(s_dyn) + PLAN_SMEM);
+  double* s_rtab = c.stage + NEWTON_STAGE;
+  c.rtab = s_rtab;
+  build_row_tables(plan->P, s_rtab);
+  __syncthreads();
   run_pass(c);
   __threadfence();
   __syncthreads();
@@ -236,6 +240,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     int* spi = reinterpret_cast<int*>(&sp);
     for (int k = threadIdx.x; k < (int)PLAN_WORDS; k += BLOCK) spi[k] = blob.w[k];
   }
+  // structured rows: centroid tables after the staging area of the work region
+  double* s_rtab = reinterpret_cast<double*>(s_work) + NEWTON_STAGE;
+  __syncthreads();
+  build_row_tables(sp.P, s_rtab);
   __syncthreads();
   if (threadIdx.x == 0) g_ctl_marks = nullptr;
   for (int pass = 0; pass < 8192; ++pass) {
@@ -266,6 +274,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     c.n_items = &s_nitems;
     c.timed_out = gb.timed_out;
     c.stage = reinterpret_cast<double*>(s_work);   // lists / items / Newton staging
+    c.rtab = s_rtab;
     if (sp.cmd.phase == PH_SWEEP && sp.cmd.local) {   // CTA-local sweep: no barrier
       local_sweep(c, s_tot);
       if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -439,6 +448,11 @@ struct topt_b200_ctx {
   uint32_t epoch = 0;
   int stream_inputs = 1;           // TOPT_B200_STREAM=0 disables
   Plan* hp_pin = nullptr;          // pinned staging of the plan (upload / results)
+  // structured rows for the following *_dev / *_ranks steps (topt_b200_set_structured_rows)
+  int srows_m = 0;
+  topt_row_desc srows[MAX_M] = {};
+  int64_t sgrid[3] = {0, 0, 0};
+  int64_t sidx_off = 0;
   // contiguous-range partition detected by the last owner map built here
   const int8_t* rng_owner = nullptr;
   int rng_m = 0;
@@ -632,8 +646,10 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
       dyn_smem = PLAN_SMEM + bytes;
     }
   }
-  // the work area also stages the Newton pass's Gram columns
-  dyn_smem = std::max(dyn_smem, PLAN_SMEM + sizeof(double) * (size_t)NEWTON_STAGE);
+  // the work area also stages the Newton pass's Gram columns, then the
+  // centroid tables of structured rows (no active lists in that case)
+  dyn_smem = std::max(dyn_smem, PLAN_SMEM + sizeof(double) * ((size_t)NEWTON_STAGE +
+                                                              (size_t)hp.P.n_tab));
   plan_start(hp);
   int phase = hp.cmd.phase;
   if (persistent && phase != PH_DONE) {
@@ -679,7 +695,7 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
   if (int rc = plan_upload(ctx, hp)) return rc;
   for (int it = 0; phase != PH_DONE && it < 4096; ++it) {
     if (ctx->profile) cudaEventRecord(ctx->ev0, ctx->stream);
-    k_pass<<<ctx->grid, BLOCK, KPASS_SMEM, ctx->stream>>>(ctx->d_plan, ctx->d_part,
+    k_pass<<<ctx->grid, BLOCK, KPASS_SMEM + sizeof(double) * (size_t)hp.P.n_tab, ctx->stream>>>(ctx->d_plan, ctx->d_part,
                                                             ctx->d_counter, nullptr);
     ctx->launches++;
     CUDA_TRY(ctx, cudaGetLastError());
@@ -721,7 +737,7 @@ int run_plan_ranks(topt_b200_ctx* ctx, Plan& hp) {
   NcclApi& api = nccl();
   for (int it = 0; phase != PH_DONE && it < 4096; ++it) {
     if (ctx->profile) cudaEventRecord(ctx->ev0, ctx->stream);
-    k_pass<<<grid, BLOCK, KPASS_SMEM, ctx->stream>>>(ctx->d_plan, ctx->d_part, ctx->d_counter,
+    k_pass<<<grid, BLOCK, KPASS_SMEM + sizeof(double) * (size_t)hp.P.n_tab, ctx->stream>>>(ctx->d_plan, ctx->d_part, ctx->d_counter,
                                                        ctx->d_rank_tot);
     CUDA_TRY(ctx, cudaGetLastError());
     const ncclResult_t nr = api.AllGather(ctx->d_rank_tot, ctx->d_gathered, PMAX, ncclDouble,
@@ -844,6 +860,70 @@ void detect_ranges(topt_b200_ctx* ctx, int32_t m, const int64_t* off, const int3
   ctx->rng_owner = owner_dev;
 }
 
+// Structured rows set on the context -> the Problem (device entries only).
+int apply_structured(topt_b200_ctx* ctx, Problem& P) {
+  P.structured = 0;
+  P.n_tab = 0;
+  if (ctx->srows_m == 0) return TOPT_OK;
+  if (ctx->srows_m != P.m)
+    return fail(ctx, TOPT_ERR_DOMAIN, "structured rows: row count differs from the problem's m");
+  if (P.m < 2 || P.m > 8 || P.owner || (P.n & 1))
+    return fail(ctx, TOPT_ERR_UNSUPPORTED,
+                "structured rows: need 2 <= m <= 8, no partition and an even element count");
+  int ntab = 0;
+  for (int k = 0; k < P.m; ++k) {
+    const topt_row_desc& d = ctx->srows[k];
+    P.row_kind[k] = d.kind;
+    P.row_axis[k] = d.axis;
+    P.row_c[k] = d.kind == RK_CONST ? d.value : d.center;
+    P.row_scale[k] = d.scale;
+    P.row_sign[k] = d.sign < 0.0 ? -1.0 : 1.0;
+    P.row_tab[k] = -1;
+    if (d.kind == RK_DENSE) {
+      if (!P.grad) return fail(ctx, TOPT_ERR_DOMAIN, "structured rows: a dense row needs grad");
+      continue;
+    }
+    if (d.kind == RK_CONST) {   // one table entry holding the value
+      P.row_tab[k] = ntab++;
+      continue;
+    }
+    if (d.kind != RK_CENTROID || d.axis < 0 || d.axis > 2)
+      return fail(ctx, TOPT_ERR_DOMAIN, "structured rows: unknown row kind / axis");
+    for (int j = 0; j < k && P.row_tab[k] < 0; ++j)   // share an identical centroid row's table
+      if (P.row_kind[j] == RK_CENTROID && P.row_axis[j] == d.axis &&
+          P.row_c[j] == d.center && P.row_scale[j] == d.scale)
+        P.row_tab[k] = P.row_tab[j];
+    if (P.row_tab[k] < 0) {
+      P.row_tab[k] = ntab;
+      ntab += (int)ctx->sgrid[d.axis];
+    }
+  }
+  if (ctx->sgrid[0] <= 0 || ctx->sgrid[1] <= 0 || ctx->sgrid[2] <= 0 || ntab > MAX_TAB)
+    return fail(ctx, TOPT_ERR_UNSUPPORTED, "structured rows: grid missing or tables too large");
+  for (int a = 0; a < 3; ++a) P.grid_n[a] = ctx->sgrid[a];
+  P.idx_off = ctx->sidx_off;
+  // one table per axis (the centre-of-mass pattern): the passes then fetch
+  // three values per element and take every row as +-value / constant
+  P.axis_fast = 1;
+  for (int a = 0; a < 3; ++a) P.axis_tab[a] = -1;
+  P.const_tab = -1;
+  int kc = -1;   // first constant row
+  for (int k = 0; k < P.m; ++k) {
+    if (P.row_kind[k] == RK_CONST) {
+      if (kc < 0) { kc = k; P.const_tab = P.row_tab[k]; }
+      else if (!(P.row_c[k] == P.row_c[kc])) P.axis_fast = 0;
+      continue;
+    }
+    if (P.row_kind[k] != RK_CENTROID) continue;
+    const int a = P.row_axis[k];
+    if (P.axis_tab[a] < 0) P.axis_tab[a] = P.row_tab[k];
+    else if (P.axis_tab[a] != P.row_tab[k]) P.axis_fast = 0;
+  }
+  P.n_tab = ntab;
+  P.structured = 1;
+  return TOPT_OK;
+}
+
 void apply_ranges(const topt_b200_ctx* ctx, Problem& P) {
   P.part_ranges = 0;
   if (!P.owner || P.owner != ctx->rng_owner || P.m != ctx->rng_m) return;
@@ -931,7 +1011,7 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   ok = ok && cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   ctx->max_dyn_smem) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)KPASS_SMEM) == cudaSuccess;
+                                  (int)(KPASS_SMEM + sizeof(double) * MAX_TAB)) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_control, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sizeof(Plan)) == cudaSuccess;
   if (ok) {
@@ -999,6 +1079,18 @@ void topt_b200_ctx_destroy(topt_b200_ctx* ctx) {
 const char* topt_b200_last_error(const topt_b200_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
 int64_t topt_b200_kernel_launches(const topt_b200_ctx* ctx) { return ctx ? ctx->launches : 0; }
 void* topt_b200_get_stream(const topt_b200_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+int topt_b200_set_structured_rows(topt_b200_ctx* ctx, int32_t m, const topt_row_desc* rows,
+                                  const int64_t* grid, int64_t index_offset) {
+  if (!ctx) return TOPT_ERR_INTERNAL;
+  if (!rows || m <= 0) { ctx->srows_m = 0; return TOPT_OK; }
+  if (m > MAX_M || !grid) return fail(ctx, TOPT_ERR_DOMAIN, "structured rows: bad arguments");
+  for (int k = 0; k < m; ++k) ctx->srows[k] = rows[k];
+  for (int a = 0; a < 3; ++a) ctx->sgrid[a] = grid[a];
+  ctx->sidx_off = index_offset;
+  ctx->srows_m = m;
+  return TOPT_OK;
+}
+
 int topt_b200_set_stream(topt_b200_ctx* ctx, void* stream) {
   if (!ctx) return TOPT_ERR_INTERNAL;
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1351,6 +1443,7 @@ int topt_b200_pgd_step_dev(topt_b200_ctx* ctx, const topt_step_problem* prob,
   P.d_prev = prob->d_prev; P.grad = prob->grad;
   P.owner = (prob->owner && prob->m > 1) ? prob->owner : nullptr;
   apply_ranges(ctx, P);
+  if ((rc = apply_structured(ctx, P))) return rc;
   P.has_part = P.owner ? 1 : 0;
   P.rho = out->rho_tilde; P.d_out = out->d; P.x_out = out->x_new; P.delta_out = out->delta;
   P.mask_out = out->mask;

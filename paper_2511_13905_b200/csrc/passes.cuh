@@ -137,7 +137,106 @@ struct PassCtx {
   int* n_items;        // shared scalar
   int* timed_out;      // global flag: a streamed input chunk never arrived
   double* stage;       // shared [NEWTON_STAGE] staging area (null if the launch has none)
+  const double* rtab;  // shared centroid tables of structured rows (P.n_tab entries)
 };
+
+// ---- Structured constraint rows ------------------------------------------------
+// Rows the caller describes instead of storing:
+// constant rows (the volume row, a_i = 1) and centroid rows
+// a_i = sign * ((coord_axis(i) + 0.5) - center) / scale (the centre-of-mass
+// rows, grid.hpp:29-33).  A pass then reads rho (and d) only.
+// The centroid values come from a per-launch shared-memory table built with
+// the same IEEE operations as the dense rows, so results are bit-identical.
+struct GridIx {
+  int64_t nx, ny, off;
+  int sx, sy;          // log2 of nx / ny when powers of two, else -1
+};
+__device__ __forceinline__ GridIx grid_ix(const Problem& P) {
+  GridIx G;
+  G.nx = P.grid_n[0]; G.ny = P.grid_n[1]; G.off = P.idx_off;
+  G.sx = (G.nx > 0 && (G.nx & (G.nx - 1)) == 0) ? __ffsll(G.nx) - 1 : -1;
+  G.sy = (G.ny > 0 && (G.ny & (G.ny - 1)) == 0) ? __ffsll(G.ny) - 1 : -1;
+  return G;
+}
+// x-fastest coordinates of global element gi
+__device__ __forceinline__ void grid_coords(const GridIx& G, int64_t gi, int64_t (&co)[3]) {
+  if (G.sx >= 0 && G.sy >= 0) {
+    co[0] = gi & (G.nx - 1);
+    const int64_t q = gi >> G.sx;
+    co[1] = q & (G.ny - 1);
+    co[2] = q >> G.sy;
+  } else if (gi >= 0 && gi < (int64_t)0xffffffffLL) {
+    const uint32_t g = (uint32_t)gi, nx = (uint32_t)G.nx, ny = (uint32_t)G.ny;
+    const uint32_t q = g / nx;
+    co[0] = g - q * nx;
+    co[2] = q / ny;
+    co[1] = q - (uint32_t)co[2] * ny;
+  } else {
+    const int64_t q = gi / G.nx;
+    co[0] = gi - q * G.nx;
+    co[2] = q / G.ny;
+    co[1] = q - co[2] * G.ny;
+  }
+}
+// Structured row k as one packed int, hoisted out of the element loops:
+// table offset | table axis << 24 (3: constant row, entry 0) | negate << 27.
+__device__ __forceinline__ int srow_code(const Problem& P, int k) {
+  const int ax = P.row_kind[k] == RK_CONST ? 3 : P.row_axis[k];
+  return P.row_tab[k] | (ax << 24) | ((P.row_sign[k] < 0.0 ? 1 : 0) << 27);
+}
+__device__ __forceinline__ double srow_fetch(const double* tab, int code, const int64_t (&co)[3]) {
+  const int ax = (code >> 24) & 7;
+  const int64_t ci = ax == 0 ? co[0] : (ax == 1 ? co[1] : (ax == 2 ? co[2] : 0));
+  const double v = tab[(code & 0xffffff) + ci];
+  return ((code >> 27) & 1) ? -v : v;
+}
+
+// The centre-of-mass pattern (P.axis_fast): per element four values --
+// tv[a] = tab[axis_tab[a] + c_a] for the three axes and tv[3] = the constant
+// row's entry -- and every structured row is +-tv[code & 3] (code: one int).
+struct AxisRows {
+  int tab[4];
+  __device__ __forceinline__ void init(const Problem& P) {
+    for (int a = 0; a < 3; ++a) tab[a] = P.axis_tab[a];
+    tab[3] = P.const_tab;
+  }
+  __device__ __forceinline__ void values(const double* t, const int64_t (&co)[3],
+                                         double (&tv)[4]) const {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) tv[a] = tab[a] >= 0 ? t[tab[a] + co[a]] : 0.0;
+    tv[3] = tab[3] >= 0 ? t[tab[3]] : 0.0;
+  }
+};
+__device__ __forceinline__ int row_pick_code(const Problem& P, int k) {
+  const int ax = P.row_kind[k] == RK_CONST ? 3 : P.row_axis[k];
+  return ax | ((P.row_sign[k] < 0.0 && P.row_kind[k] != RK_CONST) ? 4 : 0);
+}
+__device__ __forceinline__ double row_pick(int code, const double (&tv)[4]) {
+  const int ax = code & 3;
+  const double v = ax == 0 ? tv[0] : (ax == 1 ? tv[1] : (ax == 2 ? tv[2] : tv[3]));
+  return (code & 4) ? -v : v;
+}
+
+// Build the row tables (every CTA, at the start of a launch): one entry per
+// constant row, one per grid coordinate for each distinct centroid row.
+__device__ __forceinline__ void build_row_tables(const Problem& P, double* tab) {
+  if (!P.structured) return;
+  for (int k = 0; k < P.m; ++k) {
+    if (P.row_kind[k] == RK_CONST) {
+      if (threadIdx.x == 0) tab[P.row_tab[k]] = P.row_c[k];
+      continue;
+    }
+    if (P.row_kind[k] != RK_CENTROID) continue;
+    bool first = true;   // rows sharing (axis, center, scale) share one table
+    for (int j = 0; j < k; ++j)
+      if (P.row_kind[j] == RK_CENTROID && P.row_tab[j] == P.row_tab[k]) first = false;
+    if (!first) continue;
+    const int64_t len = P.grid_n[P.row_axis[k]];
+    const double ctr = P.row_c[k], sc = P.row_scale[k];
+    for (int64_t t = threadIdx.x; t < len; t += blockDim.x)
+      tab[P.row_tab[k] + t] = (((double)t + 0.5) - ctr) / sc;
+  }
+}
 
 // 16-byte vector access is used when every array of a pass is 16-byte
 // aligned (torch / cudaMalloc buffers are; an offset user pointer may not be).
@@ -158,7 +257,24 @@ constexpr int RP_MAXR = 9;
 struct StreamRows {
   const double* row[RP_MAXR];
   int nr;
+  // structured rows: gen[r] >= 0 -> row r is structured row gen[r] of *P
+  const Problem* P = nullptr;
+  const double* tab = nullptr;
+  int gen[RP_MAXR] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
 };
+
+// Row r of a pass = A row k: dense pointer or, for a structured row, generated.
+__device__ __forceinline__ void set_arow(StreamRows& R, int r, const PassCtx& c, const Problem& P,
+                                         int k) {
+  if (P.structured && P.row_kind[k] != RK_DENSE) {
+    R.P = &P;
+    R.tab = c.rtab;
+    R.gen[r] = k;
+    R.row[r] = nullptr;
+  } else {
+    R.row[r] = P.grad + (int64_t)k * P.ld;
+  }
+}
 
 // f(i, v): element i with v[r] = row r at i (r < nr; v[r] = 0 beyond).
 // Per thread the elements come in a fixed order (deterministic sums).
@@ -168,7 +284,71 @@ __device__ __forceinline__ void rows_pairs(const PassCtx& c, const StreamRows& R
   const int nr = R.nr;
   const int64_t st = c.stride;
   bool vec = (n & 1) == 0;
-  for (int r = 0; r < nr; ++r) vec = vec && al16(R.row[r]);
+  for (int r = 0; r < nr; ++r) vec = vec && (R.gen[r] >= 0 || al16(R.row[r]));
+  if (vec && R.P && R.P->axis_fast) {   // structured rows, centre-of-mass pattern
+    const GridIx G = grid_ix(*R.P);
+    const int64_t n2 = n >> 1;
+    AxisRows AX;
+    AX.init(*R.P);
+    int pk[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) pk[r] = (r < nr && R.gen[r] >= 0) ? row_pick_code(*R.P, R.gen[r]) : 0;
+    const double* __restrict__ tab = R.tab;
+    for (int64_t q = c.i0; q < n2; q += st) {
+      double2 v2[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        v2[r] = (r < nr && R.gen[r] < 0) ? reinterpret_cast<const double2*>(R.row[r])[q]
+                                         : make_double2(0.0, 0.0);
+      int64_t c0[3], c1[3];
+      grid_coords(G, 2 * q + G.off, c0);
+      grid_coords(G, 2 * q + 1 + G.off, c1);
+      double t0[4], t1[4];
+      AX.values(tab, c0, t0);
+      AX.values(tab, c1, t1);
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        if (r < nr && R.gen[r] >= 0) v2[r] = make_double2(row_pick(pk[r], t0), row_pick(pk[r], t1));
+      double v[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) v[r] = v2[r].x;
+      f(2 * q, v);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) v[r] = v2[r].y;
+      f(2 * q + 1, v);
+    }
+    return;
+  }
+  if (vec && R.P) {   // some rows are generated (structured rows)
+    const GridIx G = grid_ix(*R.P);
+    const int64_t n2 = n >> 1;
+    int code[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) code[r] = (r < nr && R.gen[r] >= 0) ? srow_code(*R.P, R.gen[r]) : 0;
+    const double* __restrict__ tab = R.tab;
+    for (int64_t q = c.i0; q < n2; q += st) {
+      double2 v2[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        v2[r] = (r < nr && R.gen[r] < 0) ? reinterpret_cast<const double2*>(R.row[r])[q]
+                                         : make_double2(0.0, 0.0);
+      int64_t c0[3], c1[3];
+      grid_coords(G, 2 * q + G.off, c0);
+      grid_coords(G, 2 * q + 1 + G.off, c1);
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        if (r < nr && R.gen[r] >= 0)
+          v2[r] = make_double2(srow_fetch(tab, code[r], c0), srow_fetch(tab, code[r], c1));
+      double v[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) v[r] = v2[r].x;
+      f(2 * q, v);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) v[r] = v2[r].y;
+      f(2 * q + 1, v);
+    }
+    return;
+  }
   if (vec) {
     const int64_t n2 = n >> 1;
     for (int64_t q = c.i0; q < n2; q += st) {
@@ -530,9 +710,12 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
       Rj.row[2] = dot ? (dir ? dout : gd_in) : rho;
       // rho and d of element i were written by this same thread above (same
       // element-to-thread map), so no barrier is needed between the loops
-      const double* __restrict__ ar = Rj.row[0];
+      const bool gen = P.structured && P.row_kind[j] != RK_DENSE;
+      const int gcode = gen ? srow_code(P, j) : 0;
+      const double* __restrict__ ar = gen ? rho : Rj.row[0];   // (not read when generated)
       const double* __restrict__ gdr = Rj.row[2];
       const int64_t rlo = owner ? P.row_lo[j] : 0, rhi = owner ? P.row_hi[j] : n;
+      const GridIx G = grid_ix(P);
       if (owner) {   // validation (projection.cpp:173-180): a_j must vanish outside its set
         int nz = 0;
         auto scan = [&](int64_t b, int64_t e) {   // count a_ji != 0 for i in [b, e)
@@ -571,9 +754,15 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
           for (int u = 0; u < UP; ++u) {
             const int64_t q = qb + u * st + lane;
             const bool ok = q < n2;
-            a2[u] = ok ? A2[q] : make_double2(0.0, 0.0);
+            a2[u] = (ok && !gen) ? A2[q] : make_double2(0.0, 0.0);
             r2[u] = ok ? R2[q] : make_double2(0.0, 0.0);
             d2[u] = (ok && dot) ? D2[q] : make_double2(0.0, 0.0);
+            if (ok && gen) {
+              int64_t c0[3], c1[3];
+              grid_coords(G, 2 * q + G.off, c0);
+              grid_coords(G, 2 * q + 1 + G.off, c1);
+              a2[u] = make_double2(srow_fetch(c.rtab, gcode, c0), srow_fetch(c.rtab, gcode, c1));
+            }
           }
 #pragma unroll
           for (int u = 0; u < UP; ++u) {
@@ -809,7 +998,10 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
   R.row[0] = ar;
   R.row[1] = rho;
   const int64_t rlo = owner ? P.row_lo[j] : 0, rhi = owner ? P.row_hi[j] : n;
-  if ((!owner || P.part_ranges) && ((rlo | rhi) & 1) == 0 && al16(ar) && al16(rho)) {
+  const bool gen = P.structured && P.row_kind[j] != RK_DENSE;
+  const int gcode = gen ? srow_code(P, j) : 0;
+  const GridIx G = grid_ix(P);
+  if ((!owner || P.part_ranges) && ((rlo | rhi) & 1) == 0 && (gen || al16(ar)) && al16(rho)) {
     // 16-byte pairs over the row's elements (its own range for a range
     // partition); the trip count is warp-uniform (push is warp-collective)
     const int64_t n2 = rhi >> 1;
@@ -818,8 +1010,22 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
     for (int64_t q0 = (rlo >> 1) + c.i0 - lane; q0 < n2; q0 += 2 * st) {
       const int64_t qa = q0 + lane, qb = q0 + st + lane;
       const bool oa = qa < n2, ob = qb < n2;
-      const double2 a0 = oa ? A2[qa] : make_double2(0.0, 0.0), r0 = oa ? R2[qa] : make_double2(0.0, 0.0);
-      const double2 a1 = ob ? A2[qb] : make_double2(0.0, 0.0), r1 = ob ? R2[qb] : make_double2(0.0, 0.0);
+      double2 a0 = (oa && !gen) ? A2[qa] : make_double2(0.0, 0.0);
+      double2 a1 = (ob && !gen) ? A2[qb] : make_double2(0.0, 0.0);
+      const double2 r0 = oa ? R2[qa] : make_double2(0.0, 0.0), r1 = ob ? R2[qb] : make_double2(0.0, 0.0);
+      if (gen) {   // structured row: generated from the element coordinates
+        int64_t c0[3], c1[3];
+        if (oa) {
+          grid_coords(G, 2 * qa + G.off, c0);
+          grid_coords(G, 2 * qa + 1 + G.off, c1);
+          a0 = make_double2(srow_fetch(c.rtab, gcode, c0), srow_fetch(c.rtab, gcode, c1));
+        }
+        if (ob) {
+          grid_coords(G, 2 * qb + G.off, c0);
+          grid_coords(G, 2 * qb + 1 + G.off, c1);
+          a1 = make_double2(srow_fetch(c.rtab, gcode, c0), srow_fetch(c.rtab, gcode, c1));
+        }
+      }
       acc.push(oa, a0.x, r0.x);
       acc.push(oa, a0.y, r0.y);
       acc.push(ob, a1.x, r1.x);
@@ -1301,7 +1507,7 @@ __device__ __noinline__ void pass_feas_streamed(const PassCtx& c) {
   StreamRows R;
   R.nr = m + 1;
   R.row[0] = P.rho;
-  for (int k = 0; k < m && k + 1 < RP_MAXR; ++k) R.row[1 + k] = P.grad + (int64_t)k * ld;
+  for (int k = 0; k < m && k + 1 < RP_MAXR; ++k) set_arow(R, 1 + k, c, P, k);
   for (int f0 = 0; f0 < cmd.nfeas; f0 += FEAS_GROUP) {
     double acc[FEAS_GROUP][M];
     int rj[FEAS_GROUP];
@@ -1514,7 +1720,7 @@ __device__ __noinline__ void pass_newton_m(const PassCtx& c) {
     StreamRows R;
     R.nr = m + 1;
     R.row[0] = rho;
-    for (int k = 0; k < m; ++k) R.row[1 + k] = grad + (int64_t)k * ld;
+    for (int k = 0; k < m; ++k) set_arow(R, 1 + k, c, P, k);
     rows_pairs<(M + 1 <= RP_MAXR ? M + 1 : RP_MAXR)>(c, R, n, [&](int64_t, const auto& v) {
       double a[M];
 #pragma unroll
@@ -1573,7 +1779,8 @@ __device__ __noinline__ void pass_final_m(const PassCtx& c) {
     const double* rows[M];
 #pragma unroll
     for (int k = 0; k < M; ++k) {
-      rows[k] = (k < m) ? grad + (int64_t)k * ld : rho;
+      const bool gen = k < m && P.structured && P.row_kind[k] != RK_DENSE;
+      rows[k] = (k < m && !gen) ? grad + (int64_t)k * ld : rho;
       vec = vec && al16(rows[k]);
     }
     if (vec) {
@@ -1593,12 +1800,27 @@ __device__ __noinline__ void pass_final_m(const PassCtx& c) {
         }
         return dl;
       };
+      const bool sr = P.structured;
+      const GridIx G = grid_ix(P);
+      int scode[M];
+#pragma unroll
+      for (int k = 0; k < M; ++k) scode[k] = (sr && k < m && P.row_kind[k] != RK_DENSE) ? srow_code(P, k) : -1;
       for (int64_t q = c.i0; q < n2; q += st) {
         const double2 r2 = reinterpret_cast<const double2*>(rho)[q];
         double2 a2[M];
 #pragma unroll
         for (int k = 0; k < M; ++k)
-          a2[k] = (k < m) ? reinterpret_cast<const double2*>(rows[k])[q] : make_double2(0.0, 0.0);
+          a2[k] = (k < m && scode[k] < 0)
+                      ? reinterpret_cast<const double2*>(rows[k])[q] : make_double2(0.0, 0.0);
+        if (sr) {   // structured rows: generated from the element coordinates
+          int64_t c0[3], c1[3];
+          grid_coords(G, 2 * q + G.off, c0);
+          grid_coords(G, 2 * q + 1 + G.off, c1);
+#pragma unroll
+          for (int k = 0; k < M; ++k)
+            if (scode[k] >= 0)
+              a2[k] = make_double2(srow_fetch(c.rtab, scode[k], c0), srow_fetch(c.rtab, scode[k], c1));
+        }
         double ax[M], ay[M];
 #pragma unroll
         for (int k = 0; k < M; ++k) { ax[k] = a2[k].x; ay[k] = a2[k].y; }

@@ -185,9 +185,29 @@ struct Problem {
   // the channel-major material blocks of C3): set j = [row_lo[j], row_hi[j]).
   // The passes then visit each row's own range instead of all n elements.
   int32_t part_ranges;
-  int32_t pad1_;
+  int32_t structured;           // some rows are generated (row_kind != RK_DENSE)
   int64_t row_lo[MAX_M], row_hi[MAX_M];
+  // Structured constraint rows: a row is dense
+  // (grad + k*ld), a constant (volume rows: a_i = row_c[k]) or a centroid
+  // row a_i = sign * ((coord_axis(i) + 0.5) - center) / scale of an
+  // x-fastest grid (grid.hpp:29-33), read from a per-launch shared-memory
+  // table tab[row_tab[k] + coord] built with the same IEEE operations.
+  int32_t row_kind[MAX_M];
+  int32_t row_axis[MAX_M];
+  int32_t row_tab[MAX_M];       // table offset (doubles) of a centroid row
+  int32_t n_tab;                // table entries in all
+  double row_c[MAX_M];          // constant value / center
+  double row_scale[MAX_M];
+  double row_sign[MAX_M];
+  int64_t grid_n[3];            // nx, ny, nz
+  int64_t idx_off;              // global index of local element 0 (slabs)
+  int32_t axis_tab[3];          // the one table of each axis (-1: none / several)
+  int32_t axis_fast;            // every centroid row uses its axis' one table,
+  int32_t const_tab;            // ... and the constant rows share one value (entry)
+  int32_t pad2_;
 };
+enum RowKind { RK_DENSE = 0, RK_CONST = 1, RK_CENTROID = 2 };
+constexpr int MAX_TAB = 8192;   // centroid table entries (shared memory, 64 KB)
 
 // Controller-visible result.
 struct Result {

@@ -46,6 +46,7 @@ class StepProblem:
     t: int = 1
     violation: float = 0.0
     grid: tuple = ()
+    rows: Optional[list] = None       # structured description of the rows (C4/C5)
 
     @property
     def part_offsets(self):
@@ -139,6 +140,8 @@ def com_constrained(nx=256, ny=256, nz=128, seed=4, volfrac=0.3, band=0.01,
     grad[0] = 1.0
     gv[0] = S
     G[0] = volfrac * n
+    # the same rows, described (structured-row extension, api rows=...)
+    rows = [dict(kind="const", value=1.0)]
     for a, (c, L) in enumerate(((cx, nx), (cy, ny), (cz, nz))):
         R = float(c @ x0) / S
         target = L / 2.0 + (com_offset_x if a == 0 else 0.0)
@@ -149,10 +152,12 @@ def com_constrained(nx=256, ny=256, nz=128, seed=4, volfrac=0.3, band=0.01,
         gv[2 + 2 * a] = -(R - target)
         G[1 + 2 * a] = band
         G[2 + 2 * a] = band
+        rows.append(dict(kind="centroid", axis=a, center=R, scale=S, sign=1.0))
+        rows.append(dict(kind="centroid", axis=a, center=R, scale=S, sign=-1.0))
     return StepProblem(
         name=f"C4_com_{nx}x{ny}x{nz}" + (f"_off{com_offset_x}" if com_offset_x else ""),
         n=n, m=7, x=x0, x_prev=xp, g=g, g_prev=gp, d_prev=gp.copy(), grad=grad, g_values=gv,
-        bounds_g=G, is_eq=np.zeros(7, np.uint8), grid=(nx, ny, nz))
+        bounds_g=G, is_eq=np.zeros(7, np.uint8), grid=(nx, ny, nz), rows=rows)
 
 
 # Full-size configs, BASELINE.json order (C1..C5), and CI-sized variants.

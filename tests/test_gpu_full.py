@@ -109,3 +109,23 @@ def test_full_c5_properties():
         for k in range(p.m):
             v = float(np.sum((p.grad[k] * delta).astype(np.longdouble))) - r1.g_hat[k]
             assert v <= TOL_N * 1.0001, (k, v)
+
+
+@pytest.mark.parametrize("name,size", [("C4", "small"), ("C4p", "small"), ("C4", "full")])
+def test_structured_rows_bit_identical(name, size):
+    """Structured rows (volume = const 1, COM rows generated from the element
+    coordinates) give the same step, bit for bit, as the dense rows."""
+    torch = pytest.importorskip("torch")
+    p = (synth.SMALL if size == "small" else synth.CONFIGS)[name](4)
+    cu = lambda v: torch.from_numpy(np.ascontiguousarray(v)).cuda()  # noqa: E731
+    X = [cu(getattr(p, k)) for k in ("x", "x_prev", "g", "g_prev", "d_prev")]
+    A = cu(p.grad.reshape(-1))
+    dense = api.pgd_step(*X, A, p.g_values, p.bounds_g, p.is_eq, None, t=p.t)
+    grid = (p.grid[0], p.grid[1], p.grid[2])
+    st = api.prepare_pgd_step(*X, None, p.g_values, p.bounds_g, p.is_eq, None, t=p.t,
+                              rows=p.rows, grid=grid).run().result()
+    assert st.projection.path == dense.projection.path
+    assert st.projection.newton_iters == dense.projection.newton_iters
+    assert np.array_equal(st.y, dense.y)
+    assert np.array_equal(st.x_new.cpu().numpy(), dense.x_new.cpu().numpy())
+    assert np.array_equal(st.g_hat, dense.g_hat)

@@ -18,9 +18,18 @@ A = cu(p.grad.reshape(-1))
 out = {k: torch.empty(p.n, dtype=torch.float64, device="cuda") for k in ("x_new", "d", "rho_tilde")}
 torch.cuda.synchronize()
 log("on device")
+structured = "--structured" in sys.argv
+if structured:
+    del A
+    A = None
+    prep = api.prepare_pgd_step(*X, None, p.g_values, p.bounds_g, p.is_eq, None, t=p.t, out=out,
+                                rows=p.rows, grid=p.grid)
+    log("structured rows")
+step = (lambda: prep.run().result()) if structured else \
+    (lambda: api.pgd_step(*X, A, p.g_values, p.bounds_g, p.is_eq, p.partition, t=p.t, out=out))
 for it in range(3):
     t = time.time()
-    r = api.pgd_step(*X, A, p.g_values, p.bounds_g, p.is_eq, p.partition, t=p.t, out=out)
+    r = step()
     torch.cuda.synchronize()
     log(f"step {it}: {1e3*(time.time()-t):.1f} ms path {r.projection.path.name} passes {r.projection.passes} "
         f"sweeps {r.projection.sweeps} newton {r.projection.newton_iters} y {r.y}")
@@ -28,7 +37,7 @@ if "--trace" in sys.argv:
     import ctypes as C
     ctx = _lib.context(0)
     ctx.lib.topt_b200_debug_trace(ctx.h, 1, None)
-    api.pgd_step(*X, A, p.g_values, p.bounds_g, p.is_eq, p.partition, t=p.t, out=out)
+    step()
     buf = (C.c_ulonglong * 1024)()
     ctx.lib.topt_b200_debug_trace(ctx.h, 0, buf)
     allt = np.array(buf, dtype=np.float64).reshape(128, 8)

@@ -33,7 +33,7 @@ def main():
 
 
 
-def trace(config="C2", seed=2):
+def trace(config="C2", seed=2, structured=False):
     """Per-pass device timeline of one persistent step (us)."""
     import ctypes as C
     from paper_2511_13905_b200 import _lib
@@ -44,10 +44,19 @@ def trace(config="C2", seed=2):
     out = {k: torch.empty(p.n, dtype=torch.float64, device="cuda")
            for k in ("x_new", "d", "rho_tilde")}
     ctx = _lib.context(0)
+    if structured:
+        del A
+        st = api.prepare_pgd_step(*X, None, p.g_values, p.bounds_g, p.is_eq, None, t=p.t, out=out,
+                                  rows=p.rows, grid=p.grid)
+        run = lambda: st.run()  # noqa: E731
+        print("structured rows")
+    else:
+        run = lambda: api.pgd_step(*X, A, p.g_values, p.bounds_g, p.is_eq, p.partition,  # noqa
+                                   t=p.t, out=out)
     for _ in range(2):
-        api.pgd_step(*X, A, p.g_values, p.bounds_g, p.is_eq, p.partition, t=p.t, out=out)
+        run()
     ctx.lib.topt_b200_debug_trace(ctx.h, 1, None)
-    api.pgd_step(*X, A, p.g_values, p.bounds_g, p.is_eq, p.partition, t=p.t, out=out)
+    run()
     buf = (C.c_ulonglong * 1024)()
     ctx.lib.topt_b200_debug_trace(ctx.h, 0, buf)
     allt = np.array(buf, dtype=np.float64).reshape(128, 8)
@@ -70,8 +79,11 @@ def trace(config="C2", seed=2):
 if __name__ == "__main__":
     if "--trace" in sys.argv:
         sys.argv.remove("--trace")
+        structured = "--structured" in sys.argv
+        if structured:
+            sys.argv.remove("--structured")
         cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
         seed = int(sys.argv[2]) if len(sys.argv) > 2 else {"C1": 1, "C2": 2, "C3": 3}.get(cfg, 4)
-        trace(cfg, seed)
+        trace(cfg, seed, structured)
     else:
         main()
