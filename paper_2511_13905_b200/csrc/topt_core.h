@@ -30,7 +30,10 @@
 namespace topt_b200 {
 
 constexpr int MAX_M = 16;      // constraint rows
-constexpr int MAX_K = 16;      // bisection candidates per row per sweep
+#ifndef TOPT_MAX_K
+#define TOPT_MAX_K 16
+#endif
+constexpr int MAX_K = TOPT_MAX_K;   // bisection candidates per row per sweep
 constexpr int MAX_CAND = 64;   // candidates per sweep over all rows
 constexpr int MAX_FEAS = MAX_M + 1;
 constexpr int PMAX = 512;      // partial-sum slots per pass
