@@ -1809,8 +1809,8 @@ __device__ __noinline__ void pass_final_m(const PassCtx& c) {
         const double2 r2 = reinterpret_cast<const double2*>(rho)[q];
         double2 a2[M];
 #pragma unroll
-        for (int k = 0; k < M; ++k)
-          a2[k] = (k < m && scode[k] < 0)
+        for (int k = 0; k < M; ++k)   // rows with y_k = 0 are not read unless their dot is wanted
+          a2[k] = (k < m && scode[k] < 0 && (resid || yv[k] != 0.0))
                       ? reinterpret_cast<const double2*>(rows[k])[q] : make_double2(0.0, 0.0);
         if (sr) {   // structured rows: generated from the element coordinates
           int64_t c0[3], c1[3];
