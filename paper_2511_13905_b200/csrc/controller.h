@@ -605,7 +605,10 @@ TOPT_NOINLINE bool schedule_sweep(Plan& pl) {
 
 TOPT_NOINLINE void after_walks(Plan& pl);
 
-TOPT_NOINLINE void finish_newton_or_loop(Plan& pl) {
+// finish_newton_or_loop in two halves around the m x m solve, so that the
+// device can run the solve on a whole warp: _pre builds J_Phi (sc.jp) and
+// returns 1 when a solve J_Phi step = Phi is pending; _post consumes it.
+TOPT_NOINLINE int finish_newton_pre(Plan& pl) {
   Newton& nt = pl.nt;
   const Problem& P = pl.P;
   const int m = P.m;
@@ -640,18 +643,7 @@ TOPT_NOINLINE void finish_newton_or_loop(Plan& pl) {
       }
       if (curv > 0.9 * nt.prev_phi_sq) nt.curv_viol++;
     }
-    if (!fullpiv_solve(m, jp, nt.phi, nt.step)) { set_error(pl, ST_NUMERICAL); return; }
-    for (int j = 0; j < m; ++j)
-      if (!isfinite(nt.step[j])) { set_error(pl, ST_NUMERICAL); return; }
-    double sq = 0.0;
-    for (int j = 0; j < m; ++j) sq = sq + nt.phi[j] * nt.phi[j];
-    nt.phi_sq = sq;
-    nt.merit0 = nt.merit;
-    nt.gamma = 1.0;
-    for (int j = 0; j < m; ++j) nt.ty[j] = nt.y[j] - nt.gamma * nt.step[j];
-    nt.in_linesearch = 1;
-    cmd_newton(pl);
-    return;
+    return 1;
   }
   Result& r = pl.res;
   r.path = PATH_NEWTON;
@@ -666,9 +658,29 @@ TOPT_NOINLINE void finish_newton_or_loop(Plan& pl) {
     r.h[j] = nt.h[j];
   }
   cmd_final(pl, nt.y, 0);
+  return 0;
 }
 
-TOPT_NOINLINE void consume_newton(Plan& pl, const double* t) {
+TOPT_NOINLINE void finish_newton_post(Plan& pl, bool solved) {
+  Newton& nt = pl.nt;
+  const int m = pl.P.m;
+  if (!solved) { set_error(pl, ST_NUMERICAL); return; }
+  for (int j = 0; j < m; ++j)
+    if (!isfinite(nt.step[j])) { set_error(pl, ST_NUMERICAL); return; }
+  double sq = 0.0;
+  for (int j = 0; j < m; ++j) sq = sq + nt.phi[j] * nt.phi[j];
+  nt.phi_sq = sq;
+  nt.merit0 = nt.merit;
+  nt.gamma = 1.0;
+  for (int j = 0; j < m; ++j) nt.ty[j] = nt.y[j] - nt.gamma * nt.step[j];
+  nt.in_linesearch = 1;
+  cmd_newton(pl);
+}
+
+
+
+// consume_newton up to the pending solve (returns finish_newton_pre's flag).
+TOPT_NOINLINE int consume_newton_core(Plan& pl, const double* t) {
   Newton& nt = pl.nt;
   const Problem& P = pl.P;
   const int m = P.m;
@@ -685,8 +697,7 @@ TOPT_NOINLINE void consume_newton(Plan& pl, const double* t) {
     for (int j = 0; j < m; ++j) { nt.y[j] = nt.ty[j]; nt.h[j] = th[j]; nt.phi[j] = tphi[j]; }
     for (int k = 0; k < ng; ++k) nt.gram[k] = t[m + k];
     nt.merit = tmerit;
-    finish_newton_or_loop(pl);
-    return;
+    return finish_newton_pre(pl);
   }
   const double c1 = 1e-4;                 // projection.cpp:415-422
   if (tmerit <= nt.merit0 - c1 * nt.gamma * nt.phi_sq || nt.gamma < 1e-16) {
@@ -702,13 +713,20 @@ TOPT_NOINLINE void consume_newton(Plan& pl, const double* t) {
     for (int k = 0; k < ng; ++k) nt.gram[k] = t[m + k];
     nt.iters++;
     nt.in_linesearch = 0;
-    finish_newton_or_loop(pl);
-    return;
+    return finish_newton_pre(pl);
   }
   nt.gamma = nt.gamma * 0.5;
   for (int j = 0; j < m; ++j) nt.ty[j] = nt.y[j] - nt.gamma * nt.step[j];
   cmd_newton(pl);
+  return 0;
 }
+
+TOPT_NOINLINE void consume_newton(Plan& pl, const double* t) {
+  if (consume_newton_core(pl, t))
+    finish_newton_post(pl, fullpiv_solve(pl.P.m, pl.sc.jp, pl.nt.phi, pl.nt.step));
+}
+
+
 
 // Stage-1 feasibility (projection.cpp:320-342) over every row whose bisection
 // succeeded, evaluated in one pass; first feasible row by index wins.
@@ -1013,6 +1031,110 @@ TOPT_NOINLINE void plan_consume(Plan& pl, const double* t) {
 }
 
 #if defined(__CUDACC__)
+// Warp-parallel full-pivot LU + solve, the same algorithm and arithmetic as
+// fullpiv_solve (Eigen::FullPivLU as used at projection.cpp:401-407): lane l
+// holds the column-major entries l and l + 32 of the m x m matrix (m <= 8);
+// the pivot search is a warp arg-max with the scalar scan's tie rule (first
+// in column-major order, NaN never chosen), row / column swaps and the
+// elimination read their operands with shuffles, and every entry gets the
+// scalar code's operations in the scalar code's order.  The triangular solves
+// (O(m^2), sequential) run on lane 0 from the factors written back.  All 32
+// lanes call it; returns false if the matrix is not invertible.
+__device__ __noinline__ bool fullpiv_solve_warp(int m, double* a, const double* b, double* x) {
+  const int lane = threadIdx.x & 31;
+  const unsigned F = 0xffffffffu;
+  if (m > 8) {
+    int ok = 0;
+    if (lane == 0) ok = fullpiv_solve(m, a, b, x) ? 1 : 0;
+    return __shfl_sync(F, ok, 0) != 0;
+  }
+  const int mm = m * m;
+  const int x0 = lane, x1 = lane + 32;
+  double e0 = x0 < mm ? a[x0] : 0.0, e1 = x1 < mm ? a[x1] : 0.0;
+  const int r0 = x0 % m, c0 = x0 / m, r1 = x1 % m, c1 = x1 / m;
+  auto fetch = [&](int idx) -> double {   // entry idx (lane-dependent) from its owner
+    const double v0 = __shfl_sync(F, e0, idx & 31), v1 = __shfl_sync(F, e1, idx & 31);
+    return idx < 32 ? v0 : v1;
+  };
+  unsigned rowperm = 0, colperm = 0;   // 4 bits per index
+  for (int i = 0; i < m; ++i) { rowperm |= (unsigned)i << (4 * i); colperm |= (unsigned)i << (4 * i); }
+  auto pswap = [](unsigned p, int u, int v) {
+    const unsigned pu = (p >> (4 * u)) & 15u, pv = (p >> (4 * v)) & 15u;
+    p &= ~((15u << (4 * u)) | (15u << (4 * v)));
+    return p | (pv << (4 * u)) | (pu << (4 * v));
+  };
+  int nz = m;
+  double maxpivot = 0.0;
+  for (int k = 0; k < m; ++k) {
+    double bv = -1.0;
+    int bi = k * m + k;
+    // this lane's candidates in scan order (x0 < x1), first strict max kept
+    if (x0 < mm && r0 >= k && c0 >= k) { const double v = fabs(e0); if (v > bv) { bv = v; bi = x0; } }
+    if (x1 < mm && r1 >= k && c1 >= k) { const double v = fabs(e1); if (v > bv) { bv = v; bi = x1; } }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(F, bv, o);
+      const int oi = __shfl_xor_sync(F, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (bv == 0.0) { nz = k; break; }
+    if (bv > maxpivot) maxpivot = bv;
+    const int br = bi % m, bc = bi / m;
+    if (br != k) {   // swap rows k, br (all columns)
+      const int s0 = c0 * m + (r0 == k ? br : (r0 == br ? k : r0));
+      const int s1 = c1 * m + (r1 == k ? br : (r1 == br ? k : r1));
+      const double n0 = fetch(s0 < mm ? s0 : 0), n1 = fetch(s1 < mm ? s1 : 0);
+      if (x0 < mm) e0 = n0;
+      if (x1 < mm) e1 = n1;
+      rowperm = pswap(rowperm, k, br);
+    }
+    if (bc != k) {   // swap columns k, bc (all rows)
+      const int s0 = (c0 == k ? bc : (c0 == bc ? k : c0)) * m + r0;
+      const int s1 = (c1 == k ? bc : (c1 == bc ? k : c1)) * m + r1;
+      const double n0 = fetch(s0 < mm ? s0 : 0), n1 = fetch(s1 < mm ? s1 : 0);
+      if (x0 < mm) e0 = n0;
+      if (x1 < mm) e1 = n1;
+      colperm = pswap(colperm, k, bc);
+    }
+    const double piv = fetch(k * m + k);
+    if (x0 < mm && c0 == k && r0 > k) e0 = e0 / piv;
+    if (x1 < mm && c1 == k && r1 > k) e1 = e1 / piv;
+    {   // A(i,j) = A(i,j) - A(i,k) * A(k,j) for i, j > k
+      const double l0 = fetch(x0 < mm ? k * m + r0 : 0), u0 = fetch(x0 < mm ? c0 * m + k : 0);
+      const double l1 = fetch(x1 < mm ? k * m + r1 : 0), u1 = fetch(x1 < mm ? c1 * m + k : 0);
+      if (x0 < mm && r0 > k && c0 > k) e0 = e0 - l0 * u0;
+      if (x1 < mm && r1 > k && c1 > k) e1 = e1 - l1 * u1;
+    }
+  }
+  const double thr = fabs(maxpivot) * 2.220446049250313e-16 * (double)m;
+  const bool d0 = x0 < mm && r0 == c0 && r0 < nz && fabs(e0) > thr;
+  const bool d1 = x1 < mm && r1 == c1 && r1 < nz && fabs(e1) > thr;
+  const int rank = __popc(__ballot_sync(F, d0)) + __popc(__ballot_sync(F, d1));
+  if (rank != m) return false;
+  if (x0 < mm) a[x0] = e0;
+  if (x1 < mm) a[x1] = e1;
+  __syncwarp();
+  if (lane == 0) {
+#define A_(i, j) a[(j) * m + (i)]
+    double cv[8];
+    for (int i = 0; i < m; ++i) cv[i] = b[(rowperm >> (4 * i)) & 15u];
+    for (int i = 0; i < m; ++i) {
+      double s2 = cv[i];
+      for (int k = 0; k < i; ++k) s2 = s2 - A_(i, k) * cv[k];
+      cv[i] = s2;
+    }
+    for (int i = nz - 1; i >= 0; --i) {
+      double s2 = cv[i];
+      for (int k = i + 1; k < nz; ++k) s2 = s2 - A_(i, k) * cv[k];
+      cv[i] = s2 / A_(i, i);
+    }
+    for (int i = 0; i < m; ++i) x[(colperm >> (4 * i)) & 15u] = (i < nz) ? cv[i] : 0.0;
+#undef A_
+  }
+  __syncwarp();
+  return true;
+}
+
 // Warp-parallel candidate choice (same set as walk_candidates).  Lane 0
 // walks the predicted path -- a bisection toward the estimate, where a level
 // certified by (yL, yH) is skipped, a near-certain level only updates the
@@ -1386,6 +1508,21 @@ __device__ void plan_consume_warp(Plan& pl, const double* t) {
       if (lane == 0 && !more) after_walks(pl);
     }
     if (lane == 0) ctl_mark(7);
+    __syncwarp();
+    return;
+  }
+  if (ph == PH_NEWTON) {   // the m x m solve on the whole warp
+    __shared__ int s_pend;
+    if (lane == 0) {
+      pl.res.passes++;
+      s_pend = consume_newton_core(pl, t);
+    }
+    __syncwarp();
+    if (s_pend) {
+      const bool ok = fullpiv_solve_warp(pl.P.m, pl.sc.jp, pl.nt.phi, pl.nt.step);
+      if (lane == 0) finish_newton_post(pl, ok);
+    }
+    if (lane == 0 && pl.res.passes > 4096 && pl.cmd.phase != PH_DONE) set_error(pl, ST_INTERNAL);
     __syncwarp();
     return;
   }

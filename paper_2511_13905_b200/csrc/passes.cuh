@@ -1503,7 +1503,7 @@ __device__ __noinline__ void pass_feas_streamed(const PassCtx& c) {
   const Cmd& cmd = *c.cmd;
   const double L = P.lower, U = P.upper;
   const int m = P.m;
-  const int64_t n = P.n, ld = P.ld;
+  const int64_t n = P.n;
   StreamRows R;
   R.nr = m + 1;
   R.row[0] = P.rho;
