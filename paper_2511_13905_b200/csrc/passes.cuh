@@ -1880,9 +1880,80 @@ __device__ __noinline__ void pass_final_m(const PassCtx& c) {
   if (resid) block_reduce_store<M>(acc, m, PH_FINAL, 0, c.out, c.smem);
 }
 
+// FINAL for a contiguous-range partition: row j's range as 16-byte pairs
+// (z = 0.0 + y_j a_j, the OWN path's expression), then the elements in no
+// set (owner -1, z = 0) if the ranges do not cover the slab.
+__device__ __noinline__ void pass_final_ranges(const PassCtx& c) {
+  const Problem& P = c.plan->P;
+  const Cmd& cmd = *c.cmd;
+  const double L = P.lower, Up = P.upper;
+  const int m = P.m;
+  const int64_t n = P.n, st = c.stride, ld = P.ld;
+  const double* __restrict__ rho = P.rho;
+  double* __restrict__ dout = cmd.write_delta ? P.delta_out : nullptr;
+  double* __restrict__ xout = cmd.write_x ? P.x_out : nullptr;
+  uint8_t* __restrict__ mout = cmd.write_mask ? P.mask_out : nullptr;
+  const bool resid = cmd.resid_rows;
+  double acc[MAX_M];
+#pragma unroll
+  for (int k = 0; k < MAX_M; ++k) acc[k] = 0.0;
+  auto one = [&](int64_t i, double r, double a, double yj, double& accj) {
+    const double z = (yj != 0.0) ? 0.0 + yj * a : 0.0;
+    const double lo = L - r, hi = Up - r;
+    const bool below = z < lo, above = z > hi;
+    const double dl = below ? lo : (above ? hi : z);
+    if (dout) dout[i] = dl;
+    if (xout) xout[i] = r + dl;
+    if (mout) mout[i] = below ? 1 : (above ? 2 : 0);
+    if (resid) accj += a * dl;
+  };
+  int64_t covered = 0;
+  for (int j = 0; j < m; ++j) {
+    const int64_t b = P.row_lo[j], e = P.row_hi[j];
+    covered += e - b;
+    const double yj = cmd.y[j];
+    const double* __restrict__ a = P.grad + (int64_t)j * ld;
+    double accj = 0.0;
+    const bool need_a = resid || yj != 0.0;
+    if (((b | e) & 1) == 0 && al16(rho) && al16(a) && (!dout || al16(dout)) &&
+        (!xout || al16(xout)) && !mout) {
+      const double2* __restrict__ R2 = reinterpret_cast<const double2*>(rho);
+      const double2* __restrict__ A2 = reinterpret_cast<const double2*>(a);
+      for (int64_t q = (b >> 1) + c.i0; q < (e >> 1); q += st) {
+        const double2 r2 = R2[q];
+        const double2 a2 = need_a ? A2[q] : make_double2(0.0, 0.0);
+        double d[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double r = h ? r2.y : r2.x, av = h ? a2.y : a2.x;
+          const double z = (yj != 0.0) ? 0.0 + yj * av : 0.0;
+          const double lo = L - r, hi = Up - r;
+          d[h] = z < lo ? lo : (z > hi ? hi : z);
+          if (resid) accj += av * d[h];
+        }
+        if (dout) reinterpret_cast<double2*>(dout)[q] = make_double2(d[0], d[1]);
+        if (xout) reinterpret_cast<double2*>(xout)[q] = make_double2(r2.x + d[0], r2.y + d[1]);
+      }
+    } else {
+      for (int64_t i = b + c.i0; i < e; i += st) one(i, rho[i], need_a ? a[i] : 0.0, yj, accj);
+    }
+#pragma unroll
+    for (int k = 0; k < MAX_M; ++k)
+      if (k == j) acc[k] = accj;
+  }
+  if (covered < n) {   // elements in no set: delta = clip(0, lo, hi)
+    const int8_t* __restrict__ owner = P.owner;
+    double dummy = 0.0;
+    for (int64_t i = c.i0; i < n; i += st)
+      if (owner[i] < 0) one(i, rho[i], 0.0, 0.0, dummy);
+  }
+  if (resid) block_reduce_store<MAX_M>(acc, m, PH_FINAL, 0, c.out, c.smem);
+}
+
 __device__ void pass_final(const PassCtx& c) {
   const int m = c.plan->P.m;
   const bool own = c.plan->P.owner != nullptr;
+  if (own && c.plan->P.part_ranges) { pass_final_ranges(c); return; }
   if (!own && m == 7) { pass_final_m<7, false>(c); return; }
   if (own) {
     if (m <= 4) pass_final_m<4, true>(c);
