@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass(Plan* plan, double* partials,
   c.stride = (int64_t)gridDim.x * BLOCK;
   c.list = nullptr;
   c.list_cnt = nullptr;
+  c.seg = nullptr;
   c.fixC = c.fixS = nullptr;
   c.list_cap = 0;
   c.timed_out = nullptr;   // never streamed
@@ -229,6 +230,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
   __shared__ double s_tot[PMAX];
   __shared__ double s_fixC[MAX_M], s_fixS[MAX_M];
   __shared__ int s_lcnt[NWARP];
+  __shared__ int s_seg[NWARP * MAX_M * 2];
   __shared__ int s_nitems;
   extern __shared__ int4 s_dyn[];
   Plan& sp = *reinterpret_cast<Plan*>(s_dyn);
@@ -260,6 +262,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     c.stride = (int64_t)nb * BLOCK;
     c.list = sp.P.compact_cap > 0 ? s_list : nullptr;
     c.list_cnt = s_lcnt;
+    c.seg = s_seg;
     c.fixC = s_fixC;
     c.fixS = s_fixS;
     c.list_cap = sp.P.compact_cap;

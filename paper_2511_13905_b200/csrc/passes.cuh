@@ -122,6 +122,7 @@ struct PassCtx {
   // and per-CTA fixed sums of the compacted bisection sweeps.
   uint32_t* list;      // [NWARP][list_cap]
   int* list_cnt;       // [NWARP]
+  int* seg;            // [NWARP][MAX_M][2] range partitions: row j's (start, count) in a warp list
   double* fixC;        // [MAX_M]
   double* fixS;        // [MAX_M]
   int list_cap;
@@ -392,6 +393,25 @@ __device__ void compact_init(const PassCtx& c) {
     cnt += __popc(ok);
   }
   if (lane == 0) c.list_cnt[warp] = cnt;
+  const Problem& P = c.plan->P;
+  if (P.part_ranges && c.seg) {
+    // the list is ascending and every set a contiguous range: row j's items
+    // are one segment [lower_bound(lo_j), lower_bound(hi_j)); lane j finds it
+    __syncwarp();
+    if (lane < P.m) {
+      auto lb = [&](int64_t v) {
+        int lo = 0, hi = cnt;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if ((int64_t)L[mid] < v) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+      };
+      const int s0 = lb(P.row_lo[lane]), s1 = lb(P.row_hi[lane]);
+      c.seg[(warp * MAX_M + lane) * 2] = s0;
+      c.seg[(warp * MAX_M + lane) * 2 + 1] = s1 - s0;
+    }
+  }
   if (threadIdx.x < MAX_M) { c.fixC[threadIdx.x] = 0.0; c.fixS[threadIdx.x] = 0.0; }
   __syncthreads();
 }
@@ -1068,13 +1088,17 @@ __device__ __noinline__ void pass_sweep_row_compact(const PassCtx& c, int j, int
   const Cmd& cmd = *c.cmd;
   const double* __restrict__ rho = P.rho;
   const double* __restrict__ ar = P.grad + (int64_t)j * P.ld;
-  const int8_t* __restrict__ owner = P.owner;
+  const int8_t* owner = P.owner;
   const double L = P.lower, U_ = P.upper;
   const double wlo = cmd.wlo[j], whi = cmd.whi[j];
   const double* y = cmd.cand_y + b;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* Lst = c.list + (size_t)warp * c.list_cap;
-  const int n_items = c.list_cnt[warp];
+  // range partition: row j's own segment of the warp list (no owner tests)
+  const bool segs = P.part_ranges && c.seg;
+  int* sg = segs ? c.seg + (warp * MAX_M + j) * 2 : nullptr;
+  uint32_t* Lst = c.list + (size_t)warp * c.list_cap + (segs ? sg[0] : 0);
+  const int n_items = segs ? sg[1] : c.list_cnt[warp];
+  if (segs) owner = nullptr;
   double R[KC], S[KC];
 #pragma unroll
   for (int k = 0; k < KC; ++k) { R[k] = 0.0; S[k] = 0.0; }
@@ -1131,7 +1155,9 @@ __device__ __noinline__ void pass_sweep_row_compact(const PassCtx& c, int j, int
     sweep_elem<KC>(ar[i], rho[i], y, cnt, L, U_, R, S);
   }
   __syncwarp();
-  if (lane == 0) c.list_cnt[warp] = kept;
+  if (lane == 0) {
+    if (segs) sg[1] = kept; else c.list_cnt[warp] = kept;
+  }
   sweep_finish<KC>(y, cnt, R, S);
   // CTA totals of this sweep's active sums and newly fixed sums
   double v[2 * KC + 2];
@@ -1180,6 +1206,29 @@ __device__ void pass_sweep(const PassCtx& c) {
   }
   if (cmd.compact && c.list) {   // active elements left in this CTA
     __shared__ int s_woff[NWARP + 1];
+    if (c.plan->P.part_ranges && c.seg) {
+      // close the gaps the per-row compactions left: segments back to back in
+      // row order (every move goes to a lower address, in increasing order)
+      __syncthreads();
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      uint32_t* Lw = c.list + (size_t)warp * c.list_cap;
+      int off = 0;
+      for (int j = 0; j < m; ++j) {
+        int* sg = c.seg + (warp * MAX_M + j) * 2;
+        const int s0 = sg[0], n0 = sg[1];
+        for (int k0 = 0; k0 < n0; k0 += 32) {
+          const int k = k0 + lane;
+          const uint32_t v = k < n0 ? Lw[s0 + k] : 0u;
+          __syncwarp();
+          if (k < n0) Lw[off + k] = v;
+          __syncwarp();
+        }
+        __syncwarp();
+        if (lane == 0) sg[0] = off;
+        off += n0;
+      }
+      if (lane == 0) c.list_cnt[warp] = off;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
       int tot = 0;
