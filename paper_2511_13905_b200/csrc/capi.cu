@@ -30,7 +30,7 @@ namespace {
 
 constexpr int RED_SCRATCH = NWARP * 160;   // doubles (max NS = 16 + 136)
 constexpr size_t PLAN_SMEM = (sizeof(Plan) + 255) & ~size_t(255);
-constexpr size_t KPASS_SMEM = PLAN_SMEM + sizeof(double) * (size_t)NEWTON_STAGE;
+constexpr size_t KPASS_SMEM = PLAN_SMEM;   // + the structured-row tables
 
 // Combine all CTAs' partial slots in a fixed order into totals[].  Group g
 // sums CTAs g, g+G, g+2G, ... sequentially (loads batched 8 deep, the
@@ -141,8 +141,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass(Plan* plan, double* partials,
   c.fixC = c.fixS = nullptr;
   c.list_cap = 0;
   c.timed_out = nullptr;   // never streamed
-  c.stage = reinterpret_cast<double*>(reinterpret_cast<char*>(s_dyn) + PLAN_SMEM);
-  double* s_rtab = c.stage + NEWTON_STAGE;
+  double* s_rtab = reinterpret_cast<double*>(reinterpret_cast<char*>(s_dyn) + PLAN_SMEM);
   c.rtab = s_rtab;
   build_row_tables(plan->P, s_rtab);
   __syncthreads();
@@ -223,6 +222,10 @@ struct PlanBlob {
 #ifdef TOPT_ICACHE_EXPERIMENT
 __device__ Plan g_plan_scratch[160];
 #endif
+// MULTI: the CTA-level controller (rows spread over warps, m > 1); the
+// single-row instantiation keeps the one-warp controller and its smaller
+// shared-memory and register footprint.
+template <bool MULTI>
 __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
                                                    unsigned long long* trace, GatherBufs gb,
                                                    const __grid_constant__ PlanBlob blob) {
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     for (int k = threadIdx.x; k < (int)PLAN_WORDS; k += BLOCK) spi[k] = blob.w[k];
   }
   // structured rows: centroid tables after the staging area of the work region
-  double* s_rtab = reinterpret_cast<double*>(s_work) + NEWTON_STAGE;
+  double* s_rtab = reinterpret_cast<double*>(s_work);   // no active lists when rows are structured
   __syncthreads();
   build_row_tables(sp.P, s_rtab);
   __syncthreads();
@@ -276,7 +279,6 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     c.it_row = reinterpret_cast<int8_t*>(c.it_r + GATHER_CAP);
     c.n_items = &s_nitems;
     c.timed_out = gb.timed_out;
-    c.stage = reinterpret_cast<double*>(s_work);   // lists / items / Newton staging
     c.rtab = s_rtab;
     if (sp.cmd.phase == PH_SWEEP && sp.cmd.local) {   // CTA-local sweep: no barrier
       local_sweep(c, s_tot);
@@ -284,8 +286,12 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
         tr[1] = tr[6] = tr[2] = tr[3] = gtimer();
         g_ctl_marks = trace + 512 + pass * 8;
       }
-      if (threadIdx.x < 32) plan_consume_warp(sp, s_tot);
-      __syncthreads();
+      if constexpr (MULTI) {
+        plan_consume_cta(sp, s_tot);
+      } else {
+        if (threadIdx.x < 32) plan_consume_warp(sp, s_tot);
+        __syncthreads();
+      }
       if (tr && blockIdx.x == 0 && threadIdx.x == 0) { tr[4] = gtimer(); g_ctl_marks = nullptr; }
       continue;
     }
@@ -310,16 +316,19 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
       int* spi = reinterpret_cast<int*>(&sp);
       for (int k = threadIdx.x; k < (int)(sizeof(Plan) / 4); k += BLOCK) gp[k] = spi[k];
       __syncthreads();
-      if (threadIdx.x < 32) plan_consume_warp(sp, s_tot);
-      __syncthreads();
+      plan_consume_cta(sp, s_tot);
       if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[7] = gtimer();
       for (int k = threadIdx.x; k < (int)(sizeof(Plan) / 4); k += BLOCK) spi[k] = gp[k];
       __syncthreads();
       if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[3] = gtimer();
     }
 #endif
-    if (threadIdx.x < 32) plan_consume_warp(sp, s_tot);
-    __syncthreads();
+    if constexpr (MULTI) {
+      plan_consume_cta(sp, s_tot);
+    } else {
+      if (threadIdx.x < 32) plan_consume_warp(sp, s_tot);
+      __syncthreads();
+    }
     if (sp.cmd.load_fused) {   // fused gather: the items were published by the sweep
       gather_load_fused(c, nb);
       if (threadIdx.x == 0) sp.cmd.load_fused = 0;
@@ -639,7 +648,9 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
   hp.P.ours_len = 2.0 * (double)per_thread + (double)grid + 64.0;
   size_t dyn_smem = sizeof(Plan);
   hp.P.compact_cap = 0;
-  if (persistent && ctx->compact) {
+  // active lists only where compacted sweeps run (one row, or a partition);
+  // otherwise the work area is free (structured rows keep their tables there)
+  if (persistent && ctx->compact && (hp.P.m == 1 || hp.P.has_part)) {
     const int64_t cap = 32 * per_thread;
     size_t bytes = (size_t)NWARP * (size_t)cap * sizeof(uint32_t);
     const size_t item_bytes = (size_t)GATHER_CAP * (2 * sizeof(double) + 1);
@@ -649,10 +660,9 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
       dyn_smem = PLAN_SMEM + bytes;
     }
   }
-  // the work area also stages the Newton pass's Gram columns, then the
-  // centroid tables of structured rows (no active lists in that case)
-  dyn_smem = std::max(dyn_smem, PLAN_SMEM + sizeof(double) * ((size_t)NEWTON_STAGE +
-                                                              (size_t)hp.P.n_tab));
+  // the work area holds the structured rows' tables instead (no active
+  // lists in that case)
+  dyn_smem = std::max(dyn_smem, PLAN_SMEM + sizeof(double) * (size_t)hp.P.n_tab);
   plan_start(hp);
   int phase = hp.cmd.phase;
   if (persistent && phase != PH_DONE) {
@@ -666,7 +676,8 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
     void* args[] = {&ctx->d_plan, &ctx->d_part, &tr, &gb, blob};
     if (si) CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_timed_out, 0, sizeof(int), ctx->stream));
     if (ctx->profile) cudaEventRecord(ctx->ev0, ctx->stream);
-    CUDA_TRY(ctx, cudaLaunchCooperativeKernel((void*)k_step, grid, BLOCK, args, dyn_smem,
+    const void* kfn = hp.P.m > 1 ? (const void*)k_step<true> : (const void*)k_step<false>;
+    CUDA_TRY(ctx, cudaLaunchCooperativeKernel(kfn, grid, BLOCK, args, dyn_smem,
                                               ctx->stream));
     ctx->launches++;
     if (ctx->profile) cudaEventRecord(ctx->ev1, ctx->stream);
@@ -1011,7 +1022,9 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   ok = ok && cudaMalloc(&ctx->d_grow, sizeof(int) * gcap) == cudaSuccess;
   ok = ok && cudaMalloc(&ctx->d_gfix, sizeof(double) * 2 * MAX_M * ctx->grid) == cudaSuccess;
   ctx->max_dyn_smem = 160 * 1024;
-  ok = ok && cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  ok = ok && cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  ctx->max_dyn_smem) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   ctx->max_dyn_smem) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(KPASS_SMEM + sizeof(double) * MAX_TAB)) == cudaSuccess;
@@ -1020,7 +1033,10 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   if (ok) {
     int per_sm = 0, coop = 0;
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step, BLOCK, (int)sizeof(Plan));
+    int per_sm2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step<false>, BLOCK, (int)sizeof(Plan));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_step<true>, BLOCK, (int)sizeof(Plan));
+    per_sm = std::min(per_sm, per_sm2);
     ctx->coop_grid = coop ? per_sm * ctx->nsm : 0;
     if (ctx->coop_grid > ctx->grid) ctx->coop_grid = ctx->grid;
     if (const char* e = getenv("TOPT_B200_PERSISTENT")) ctx->persistent = atoi(e);

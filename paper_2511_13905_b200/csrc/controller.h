@@ -1296,50 +1296,63 @@ __device__ __noinline__ int walk_candidates_warp(const Walk& w, const ProjOption
 }
 
 // Warp version of schedule_sweep (same command layout).
+// Candidates of row j, ascending (rank sort, ties by index), into out[];
+// returns their count.  One warp.
+__device__ __noinline__ int schedule_row_warp(Plan& pl, int j, int per, double* out,
+                                              WarpPath& wp) {
+  const int lane = threadIdx.x & 31;
+  const Walk& w = pl.w[j];   // shared memory (a copy would live in local memory)
+  const int nc = walk_candidates_warp(w, pl.P.opt, per, out, wp);
+  const double v = lane < nc ? out[lane] : 0.0;
+  int rk = 0;
+  for (int q = 0; q < nc; ++q) {
+    const double u = __shfl_sync(0xffffffffu, v, q);
+    rk += (u < v || (u == v && q < lane)) ? 1 : 0;
+  }
+  __syncwarp();
+  if (lane < nc) out[rk] = v;
+  __syncwarp();
+  if (lane == 0) ctl_mark(11);
+  return nc;
+}
+
+TOPT_HDN inline int schedule_per(const Plan& pl, int need) {
+  int per = MAX_CAND / need;
+  return per > MAX_K ? MAX_K : per;
+}
+
+// The sweep command around the candidates already in cmd.cand_y (lane 0).
+TOPT_HDN inline void schedule_finish(Plan& pl, int tot) {
+  Cmd& c = pl.cmd;
+  const int m = pl.P.m;
+  c.phase = PH_SWEEP;
+  for (int j = m; j <= MAX_M; ++j) c.row_start[j] = tot;
+  // the first global sweep of a job classifies nothing away (its window is
+  // the whole bracket): it runs the plain full sweep with the queued fast
+  // path; the active lists start with the second
+  c.compact = (pl.P.compact_cap > 0 && (m == 1 || pl.P.has_part) &&
+               (c.local || pl.res.sweeps > 0)) ? 1 : 0;
+  for (int j = 0; j < m; ++j) walk_window(pl.w[j], &c.wlo[j], &c.whi[j]);
+  c.ncand = tot;
+  c.nslots = 2 * tot + ((c.compact && !c.local) ? 2 : 0);
+  if (c.local) pl.res.local_sweeps++; else pl.res.sweeps++;
+}
+
 __device__ __noinline__ bool schedule_sweep_warp(Plan& pl, WarpPath& wp) {
   const int lane = threadIdx.x & 31;
   const int m = pl.P.m;
   int need = 0;
   for (int j = 0; j < m; ++j) need += (pl.w[j].status == WK_NEED);
   if (!need) return false;
-  int per = MAX_CAND / need;
-  if (per > MAX_K) per = MAX_K;
+  const int per = schedule_per(pl, need);
   Cmd& c = pl.cmd;
   int tot = 0;
   for (int j = 0; j < m; ++j) {
     if (lane == 0) c.row_start[j] = tot;
-    if (pl.w[j].status == WK_NEED) {
-      const Walk& w = pl.w[j];   // shared memory (a copy would live in local memory)
-      const int nc = walk_candidates_warp(w, pl.P.opt, per, c.cand_y + tot, wp);
-      // ascending order for the sweeps (rank sort, ties by index)
-      double* cy = c.cand_y + tot;
-      const double v = lane < nc ? cy[lane] : 0.0;
-      int rk = 0;
-      for (int q = 0; q < nc; ++q) {
-        const double u = __shfl_sync(0xffffffffu, v, q);
-        rk += (u < v || (u == v && q < lane)) ? 1 : 0;
-      }
-      __syncwarp();
-      if (lane < nc) cy[rk] = v;
-      __syncwarp();
-      if (lane == 0) ctl_mark(11);
-      tot += nc;
-    }
+    if (pl.w[j].status == WK_NEED) tot += schedule_row_warp(pl, j, per, c.cand_y + tot, wp);
   }
   __syncwarp();
-  if (lane == 0) {
-    c.phase = PH_SWEEP;
-    for (int j = m; j <= MAX_M; ++j) c.row_start[j] = tot;
-    // the first global sweep of a job classifies nothing away (its window is
-    // the whole bracket): it runs the plain full sweep with the queued
-    // fast path; the active lists start with the second
-    c.compact = (pl.P.compact_cap > 0 && (m == 1 || pl.P.has_part) &&
-                 (c.local || pl.res.sweeps > 0)) ? 1 : 0;
-    for (int j = 0; j < m; ++j) walk_window(pl.w[j], &c.wlo[j], &c.whi[j]);
-    c.ncand = tot;
-    c.nslots = 2 * tot + ((c.compact && !c.local) ? 2 : 0);
-    if (c.local) pl.res.local_sweeps++; else pl.res.sweeps++;
-  }
+  if (lane == 0) schedule_finish(pl, tot);
   __syncwarp();
   return true;
 }
@@ -1348,14 +1361,15 @@ __device__ __noinline__ bool schedule_sweep_warp(Plan& pl, WarpPath& wp) {
 // holds candidate k; bracket updates are warp arg-reductions and each
 // replayed midpoint is matched with one ballot.  Same decisions as the
 // scalar consume_sweep (candidates are distinct duals).
-__device__ __noinline__ void consume_sweep_warp(Plan& pl, const double* t) {
+// Ingest + replay of row j's evaluations (one warp): lane k holds candidate
+// k; bracket updates are warp arg-reductions and each replayed midpoint is
+// matched with one ballot.
+__device__ __noinline__ void consume_sweep_row_warp(Plan& pl, const double* t, int j) {
   const int lane = threadIdx.x & 31;
-  const int m = pl.P.m;
   Cmd& c = pl.cmd;
-  const bool was_global_compact = c.compact && !c.local;
-  for (int j = 0; j < m; ++j) {
+  {
     const int b = c.row_start[j], e = c.row_start[j + 1], nc = e - b;
-    if (nc <= 0) continue;
+    if (nc <= 0) return;
     Walk w = pl.w[j];
     // lane k holds candidate k; the row's candidates are ascending, so the
     // nearest qualifying point below (above) is the highest (lowest) lane
@@ -1444,6 +1458,14 @@ __device__ __noinline__ void consume_sweep_warp(Plan& pl, const double* t) {
     if (lane == 0) pl.w[j] = w;
     __syncwarp();
   }
+}
+
+__device__ __noinline__ void consume_sweep_warp(Plan& pl, const double* t) {
+  const int lane = threadIdx.x & 31;
+  const int m = pl.P.m;
+  Cmd& c = pl.cmd;
+  const bool was_global_compact = c.compact && !c.local;
+  for (int j = 0; j < m; ++j) consume_sweep_row_warp(pl, t, j);
   __shared__ WarpPath s_wp;
   __shared__ int s_act;
   if (lane == 0) {
@@ -1528,6 +1550,93 @@ __device__ void plan_consume_warp(Plan& pl, const double* t) {
   }
   if (lane == 0) plan_consume(pl, t);
   __syncwarp();
+}
+
+// CTA-level controller step (all threads of the CTA call it).  With several
+// rows (stage-1 walks, independent partitions), the per-row work of a sweep
+// step -- ingest + replay, then candidate choice -- runs on warp j for row j;
+// warp 0 does the bookkeeping in between and concatenates the rows'
+// candidates in row order, so the command is the same as the one-warp
+// controller's.  Everything else is plan_consume_warp on warp 0.
+__device__ __noinline__ void plan_consume_cta(Plan& pl, const double* t) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int m = pl.P.m;
+  const int ph = pl.cmd.phase;
+  const bool multi = m > 1 && m <= (int)(blockDim.x >> 5) && (ph == PH_SWEEP || ph == PH_PREP);
+  if (!multi) {
+    if (warp == 0) plan_consume_warp(pl, t);
+    __syncthreads();
+    return;
+  }
+  __shared__ int s_sched;
+  __shared__ int s_nc[MAX_M];
+  __shared__ double s_cand[MAX_M * MAX_K];
+  __shared__ WarpPath s_wpr[MAX_M];
+  Cmd& c = pl.cmd;
+  if (ph == PH_SWEEP) {
+    const bool was_global_compact = c.compact && !c.local;
+    if (warp < m) consume_sweep_row_warp(pl, t, warp);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ctl_mark(1);
+      if (was_global_compact) pl.res.active = t[2 * c.ncand];
+      pl.res.passes++;
+      int need = 0;
+      for (int j = 0; j < m; ++j) need += (pl.w[j].status == WK_NEED);
+      s_sched = 1;
+      if (need && was_global_compact && pl.res.active <= (double)GATHER_TRIGGER) {
+        if (t[2 * c.ncand + 1] == 0.0) {   // fused gather
+          c.local = 1;
+          c.load_fused = 1;
+          pl.res.gathered = 1;
+        } else {
+          c.phase = PH_GATHER;
+          c.nslots = 0;
+          s_sched = 0;
+        }
+      }
+    }
+  } else {   // PH_PREP
+    if (threadIdx.x == 0) {
+      pl.res.passes++;
+      ctl_mark(0);
+      consume_prep_core(pl, t);
+      ctl_mark(1);
+      s_sched = (pl.cmd.phase == PH_SWEEP && pl.cmd.nslots == -1) ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  if (s_sched) {
+    int need = 0;
+    for (int j = 0; j < m; ++j) need += (pl.w[j].status == WK_NEED);
+    if (need) {
+      const int per = schedule_per(pl, need);
+      if (warp < m) {
+        const int nc = pl.w[warp].status == WK_NEED
+                           ? schedule_row_warp(pl, warp, per, s_cand + warp * MAX_K, s_wpr[warp])
+                           : 0;
+        if (lane == 0) s_nc[warp] = nc;
+      }
+      __syncthreads();
+      if (warp == 0) {   // concatenate in row order (the one-warp layout)
+        int tot = 0;
+        for (int j = 0; j < m; ++j) {
+          if (lane == 0) c.row_start[j] = tot;
+          if (lane < s_nc[j]) c.cand_y[tot + lane] = s_cand[j * MAX_K + lane];
+          tot += s_nc[j];
+        }
+        __syncwarp();
+        if (lane == 0) schedule_finish(pl, tot);
+      }
+    } else if (threadIdx.x == 0) {
+      after_walks(pl);
+    }
+  }
+  if (threadIdx.x == 0) {
+    ctl_mark(7);
+    if (pl.res.passes > 4096 && pl.cmd.phase != PH_DONE) set_error(pl, ST_INTERNAL);
+  }
+  __syncthreads();
 }
 #endif
 

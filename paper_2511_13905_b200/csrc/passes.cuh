@@ -137,7 +137,6 @@ struct PassCtx {
   int8_t* it_row;
   int* n_items;        // shared scalar
   int* timed_out;      // global flag: a streamed input chunk never arrived
-  double* stage;       // shared [NEWTON_STAGE] staging area (null if the launch has none)
   const double* rtab;  // shared centroid tables of structured rows (P.n_tab entries)
 };
 
@@ -1630,103 +1629,6 @@ __device__ __noinline__ void pass_feas(const PassCtx& c) {
 // ---- PH_NEWTON: delta(y), h-dots and the free-set Gram A D A^T ------------
 // (eval_phi projection.cpp:279-298 and J_h projection.cpp:359-376)
 //
-// m <= 8: each warp takes 32 consecutive elements per step (one per lane,
-// the next step's loads already in flight), computes z, delta and the h-dots
-// per lane, and stages the free elements' columns a_.i in shared memory; lane
-// q then owns Gram entry q (and q + 32) of the packed upper triangle and
-// accumulates it over the 32 columns with FMA.  A thread thus holds 2 Gram
-// accumulators instead of m(m+1)/2 = 28 (m = 7), which kept the register
-// version spilling.  Column stride 9 doubles: the lanes' 8 writes of a column
-// and the 8 distinct row reads of an entry step are conflict-free broadcasts.
-constexpr int NW_ROWS = 8;
-constexpr int NW_STRIDE = 9;
-constexpr int NEWTON_STAGE = NWARP * 32 * NW_STRIDE;   // doubles
-__device__ __noinline__ void pass_newton_warp(const PassCtx& c, double* __restrict__ stage) {
-  const Plan& pl = *c.plan;
-  const Problem& P = pl.P;
-  const Cmd& cmd = *c.cmd;
-  const double L = P.lower, U = P.upper;
-  const int m = P.m;
-  const int64_t n = P.n, st = c.stride, ld = P.ld;
-  const double* __restrict__ rho = P.rho;
-  const double* __restrict__ grad = P.grad;
-  const bool want_gram = cmd.want_gram;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* __restrict__ sb = stage + warp * 32 * NW_STRIDE;
-  const int NG = m * (m + 1) / 2;
-  int j0 = 0, k0 = 0, j1 = 0, k1 = 0;
-  {
-    int q = 0;
-    for (int j = 0; j < m; ++j)
-      for (int k = j; k < m; ++k, ++q) {
-        if (q == lane) { j0 = j; k0 = k; }
-        if (q == lane + 32) { j1 = j; k1 = k; }
-      }
-  }
-  const bool e0 = lane < NG, e1 = lane + 32 < NG;
-  double G0 = 0.0, G1 = 0.0;
-  double h[NW_ROWS], y[NW_ROWS];
-#pragma unroll
-  for (int k = 0; k < NW_ROWS; ++k) { h[k] = 0.0; y[k] = (k < m) ? cmd.y[k] : 0.0; }
-  double na[NW_ROWS], nr = 0.0;
-  int64_t i = c.i0;
-#pragma unroll
-  for (int k = 0; k < NW_ROWS; ++k) na[k] = (i < n && k < m) ? grad[(int64_t)k * ld + i] : 0.0;
-  if (i < n) nr = rho[i];
-  for (int64_t ib = c.i0 - lane; ib < n; ib += st, i += st) {   // warp-uniform trip count
-    const bool ok = i < n;
-    double a[NW_ROWS];
-#pragma unroll
-    for (int k = 0; k < NW_ROWS; ++k) a[k] = na[k];
-    const double r = nr;
-    const int64_t inx = i + st;
-    const bool okn = inx < n;
-#pragma unroll
-    for (int k = 0; k < NW_ROWS; ++k) na[k] = (okn && k < m) ? grad[(int64_t)k * ld + inx] : 0.0;
-    nr = okn ? rho[inx] : 0.0;
-    const double lo = L - r, hi = U - r;
-    double z = 0.0;
-#pragma unroll
-    for (int k = 0; k < NW_ROWS; ++k)
-      if (k < m && y[k] != 0.0) z += y[k] * a[k];
-    const bool clipped = (z < lo) || (z > hi);
-    const double dl = clipd(z, lo, hi);
-    if (ok) {
-#pragma unroll
-      for (int k = 0; k < NW_ROWS; ++k) h[k] += a[k] * dl;
-    }
-    if (want_gram) {
-      const bool fr = ok && !clipped;
-#pragma unroll
-      for (int k = 0; k < NW_ROWS; ++k) sb[lane * NW_STRIDE + k] = fr ? a[k] : 0.0;
-      __syncwarp();
-#pragma unroll 8
-      for (int e = 0; e < 32; ++e) {
-        const double* col = sb + e * NW_STRIDE;
-        G0 = __fma_rn(col[j0], col[k0], G0);
-        G1 = __fma_rn(col[j1], col[k1], G1);
-      }
-      __syncwarp();
-    }
-  }
-  // pack: slots [0, m) h ; [m, m + NG) the Gram entries (one lane per entry
-  // and warp holds a value, the others add exact zeros)
-  constexpr int NS = NW_ROWS + NW_ROWS * (NW_ROWS + 1) / 2;
-  double v[NS];
-#pragma unroll
-  for (int k = 0; k < NS; ++k) v[k] = 0.0;
-#pragma unroll
-  for (int k = 0; k < NW_ROWS; ++k) if (k < m) v[k] = h[k];
-#pragma unroll
-  for (int q = 0; q < NS - NW_ROWS; ++q) {
-    if (e0 && q == lane) v[m + q] = G0;
-    if (e1 && q == lane + 32) v[m + q] = G1;
-  }
-  block_reduce_store<NS>(v, m + NG, PH_NEWTON, 0, c.out, c.smem);
-}
-
-// ---- PH_NEWTON: delta(y), h-dots and the free-set Gram A D A^T ------------
-// (eval_phi projection.cpp:279-298 and J_h projection.cpp:359-376)
 // Register version: per thread the h-dots and the packed Gram triangle (M
 // exact for m = 7: 28 accumulators); the rows come as 16-byte pairs
 // (rows_pairs), two elements' loads in flight per thread.
@@ -2019,12 +1921,6 @@ __device__ void pass_final(const PassCtx& c) {
 
 __device__ void pass_newton(const PassCtx& c) {
   const int m = c.plan->P.m;
-#ifdef TOPT_NEWTON_WARP
-  if (m <= NW_ROWS && c.stage) {
-    pass_newton_warp(c, c.stage);
-    return;
-  }
-#endif
   if (m == 7) { pass_newton_m<7>(c); return; }
   if (m <= 1) pass_newton_m<1>(c);
   else if (m <= 2) pass_newton_m<2>(c);

@@ -48,7 +48,7 @@ enum Phase : int32_t {
   PH_DONE = 6,
   PH_GATHER = 7        // copy the (small) active sets to every CTA; later sweeps run CTA-locally
 };
-constexpr int GATHER_CAP = 8192;   // max gathered active elements (all rows)
+constexpr int GATHER_CAP = 1024;   // max gathered active elements (all rows; = the trigger)
 constexpr int GATHER_BLK = 128;    // per-CTA items a compacted sweep publishes (fused gather)
 constexpr int GATHER_TRIGGER = 1024;   // go CTA-local at or below this many active items
 

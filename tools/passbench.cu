@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_sweep(const Plan* plan, double* pa
   c.plan = plan; c.cmd = &s_cmd; c.out = part + blockIdx.x * PMAX; c.smem = s_red;
   c.i0 = (int64_t)blockIdx.x * BLOCK + threadIdx.x; c.stride = (int64_t)gridDim.x * BLOCK;
   c.list = nullptr; c.list_cnt = nullptr; c.fixC = c.fixS = nullptr; c.list_cap = 0;
-  c.stage = nullptr; c.seg = nullptr; c.rtab = nullptr;
+  c.seg = nullptr; c.rtab = nullptr;
 
   if (mode == 0) pass_sweep_row<16>(c, 0, 0, 16);
   if (mode == 1) pass_sweep_row<8>(c, 0, 0, 8);
