@@ -465,10 +465,17 @@ struct topt_b200_ctx {
   topt_row_desc srows[MAX_M] = {};
   int64_t sgrid[3] = {0, 0, 0};
   int64_t sidx_off = 0;
-  // contiguous-range partition detected by the last owner map built here
-  const int8_t* rng_owner = nullptr;
-  int rng_m = 0;
-  int64_t rng_lo[MAX_M] = {}, rng_hi[MAX_M] = {};
+  // contiguous-range partitions detected by the owner maps built here (a
+  // few, keyed by the owner map's device pointer: the host-buffer and the
+  // device-buffer steps of one problem keep different maps)
+  struct RangeEntry {
+    const int8_t* owner = nullptr;
+    int m = 0;
+    int64_t lo[MAX_M] = {}, hi[MAX_M] = {};
+  };
+  static constexpr int N_RANGE = 4;
+  RangeEntry rng[N_RANGE];
+  int rng_next = 0;
 };
 
 // ---- NCCL, resolved at run time (the process may already hold torch's copy)
@@ -860,18 +867,26 @@ int upload(topt_b200_ctx* ctx, int slot, const void* src, size_t bytes, void** d
 // scan of the index arrays; remembered with the owner map it belongs to.)
 void detect_ranges(topt_b200_ctx* ctx, int32_t m, const int64_t* off, const int32_t* idx,
                    const int8_t* owner_dev) {
-  ctx->rng_owner = nullptr;
+  int slot = -1;   // a rebuilt map replaces what was known about its buffer
+  for (int k = 0; k < topt_b200_ctx::N_RANGE; ++k)
+    if (ctx->rng[k].owner == owner_dev) { ctx->rng[k].owner = nullptr; slot = k; }
   if (m < 1 || m > MAX_M) return;
+  topt_b200_ctx::RangeEntry r;
   for (int j = 0; j < m; ++j) {
     const int64_t b = off[j], e = off[j + 1];
     if (e <= b) return;
     for (int64_t k = b + 1; k < e; ++k)
       if (idx[k] != idx[k - 1] + 1) return;
-    ctx->rng_lo[j] = idx[b];
-    ctx->rng_hi[j] = (int64_t)idx[e - 1] + 1;
+    r.lo[j] = idx[b];
+    r.hi[j] = (int64_t)idx[e - 1] + 1;
   }
-  ctx->rng_m = m;
-  ctx->rng_owner = owner_dev;
+  r.m = m;
+  r.owner = owner_dev;
+  if (slot < 0) {
+    slot = ctx->rng_next;
+    ctx->rng_next = (ctx->rng_next + 1) % topt_b200_ctx::N_RANGE;
+  }
+  ctx->rng[slot] = r;
 }
 
 // Structured rows set on the context -> the Problem (device entries only).
@@ -940,13 +955,17 @@ int apply_structured(topt_b200_ctx* ctx, Problem& P) {
 
 void apply_ranges(const topt_b200_ctx* ctx, Problem& P) {
   P.part_ranges = 0;
-  if (!P.owner || P.owner != ctx->rng_owner || P.m != ctx->rng_m) return;
-  for (int j = 0; j < P.m; ++j) {
-    if (ctx->rng_lo[j] < 0 || ctx->rng_hi[j] > P.n) return;
-    P.row_lo[j] = ctx->rng_lo[j];
-    P.row_hi[j] = ctx->rng_hi[j];
+  if (!P.owner) return;
+  for (const auto& e : ctx->rng) {
+    if (e.owner != P.owner || e.m != P.m) continue;
+    for (int j = 0; j < P.m; ++j) {
+      if (e.lo[j] < 0 || e.hi[j] > P.n) return;
+      P.row_lo[j] = e.lo[j];
+      P.row_hi[j] = e.hi[j];
+    }
+    P.part_ranges = 1;
+    return;
   }
-  P.part_ranges = 1;
 }
 
 int owner_map_impl(topt_b200_ctx* ctx, int64_t n, int32_t m, const int64_t* off,
