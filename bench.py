@@ -45,17 +45,55 @@ def measured_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons DURING the timed region.  NVML is polled
+    from a thread every ~0.5 ms (the device-side timed region of a small
+    config lasts a few ms, shorter than nvidia-smi's sampling loop can start);
+    nvidia-smi -lms is the fallback when NVML is unavailable."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index=0):
-        self.index = index
-        self.rows = []
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [s.strip() for s in vis.split(",") if s.strip()]
+        self.index = int(ids[index]) if index < len(ids) and ids[index].isdigit() else index
+        self.rows = []          # (sm_mhz, max_mhz, set of reason names)
         self.proc = None
+        self.nvml = None
+        self.halt = threading.Event()
+        self.t = None
+
+    def _nvml_sample(self):
+        nv, h = self.nvml, self.h
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        masks = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                 nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        self.rows.append((float(sm), float(mx),
+                          {self.NAMES[k] for k in range(4) if bits & masks[k]}))
+
+    def _poll(self):
+        while not self.halt.is_set():
+            try:
+                self._nvml_sample()
+            except Exception:
+                pass
+            time.sleep(0.0005)
 
     def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nvml, self.h = nv, nv.nvmlDeviceGetHandleByIndex(self.index)
+            self._nvml_sample()
+            self.rows.clear()
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -68,29 +106,34 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            parts = [s.strip() for s in line.split(",")]
-            if len(parts) >= 7:
-                self.rows.append(parts)
+            p = [s.strip() for s in line.split(",")]
+            if len(p) >= 7 and p[0].replace(".", "").isdigit():
+                self.rows.append((float(p[0]), float(p[1]) if p[1].replace(".", "").isdigit()
+                                  else float("nan"),
+                                  {self.NAMES[k] for k in range(4) if p[3 + k] == "Active"}))
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
-        rows = self.rows
+        if self.nvml is not None:
+            self.halt.set()
+            self.t.join(timeout=2)
+            src = "nvml"
+        elif self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+            src = "nvidia-smi"
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml and nvidia-smi unavailable"]}
+        rows = list(self.rows)
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "source": src}
+        return {"sm_mhz": statistics.median(r[0] for r in rows),
+                "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": sorted(set().union(*(r[2] for r in rows))),
+                "samples": len(rows), "source": src}
 
 
 def make_problem(config, seed, world=1):

@@ -603,6 +603,108 @@ __device__ __forceinline__ void warp_minmax(double& fmin, double& fmax) {
   }
 }
 
+// PREP row sums of G dense rows j0 .. j0+G-1 in ONE sweep over
+// (a_j0 .. a_j0+G-1, rho, d): rho and d are read once per group instead of
+// once per row (C4/C5, m = 7: 26 -> 16 streamed n-vectors).  FUSE folds the
+// direction pass into the group (g, d_prev, x read; d, rho computed in
+// registers and written).  Pair q is handled by thread q mod stride, in
+// increasing q, exactly like the one-row loop and rows_pairs, so every row's
+// per-thread sums and the stores of rho / d are those of the unfused passes
+// (the warp breakpoint filter only skips divisions that cannot move the
+// min / max).  Needs 16-byte aligned vectors and even n.
+template <int G, bool FUSE>
+__device__ __forceinline__ void prep_group(const PassCtx& c, int j0, int64_t n, bool dot, bool use_dp,
+                                           double beta, double wa, double L, double U_) {
+  const Problem& P = c.plan->P;
+  const int64_t st = c.stride, n2 = n >> 1;
+  const int lane = threadIdx.x & 31;
+  const double2* __restrict__ R2 = reinterpret_cast<const double2*>(P.rho);
+  const double2* __restrict__ D2 = reinterpret_cast<const double2*>(P.d_out);
+  const double2* __restrict__ G2 = reinterpret_cast<const double2*>(P.g);
+  const double2* __restrict__ P2 = reinterpret_cast<const double2*>(use_dp ? P.d_prev : P.g);
+  const double2* __restrict__ X2 = reinterpret_cast<const double2*>(P.x);
+  double2* __restrict__ RO = reinterpret_cast<double2*>(P.rho);
+  double2* __restrict__ DO = reinterpret_cast<double2*>(P.d_out);
+  const double2* __restrict__ A2[G];
+#pragma unroll
+  for (int r = 0; r < G; ++r)
+    A2[r] = reinterpret_cast<const double2*>(P.grad + (int64_t)(j0 + r) * P.ld);
+  PrepAcc A[G];
+  double fmin[G], fmax[G];
+#pragma unroll
+  for (int r = 0; r < G; ++r) {
+#pragma unroll
+    for (int s = 0; s < PREP_SLOTS; ++s) A[r].v[s] = 0.0;   // bp_lo = bp_hi = 0 (:58)
+    fmin[r] = 0.0;
+    fmax[r] = 0.0;
+  }
+  constexpr int UP = 2;   // pairs in flight per thread
+  for (int64_t qb = c.i0 - lane; qb < n2; qb += UP * st) {   // warp-uniform trip count
+    double2 a2[UP][G], r2[UP], d2[UP];
+    const double2 z2 = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      const int64_t q = qb + u * st + lane;
+      const bool ok = q < n2;
+#pragma unroll
+      for (int r = 0; r < G; ++r) a2[u][r] = ok ? A2[r][q] : z2;
+      if (FUSE) {
+        const double2 gv = ok ? G2[q] : z2, pv = (ok && use_dp) ? P2[q] : z2;
+        const double2 xv = ok ? X2[q] : z2;
+        // d = g + beta d_prev ; rho = x - (omega alpha) d
+        d2[u].x = use_dp ? gv.x + beta * pv.x : gv.x;
+        d2[u].y = use_dp ? gv.y + beta * pv.y : gv.y;
+        r2[u].x = xv.x - wa * d2[u].x;
+        r2[u].y = xv.y - wa * d2[u].y;
+        if (ok) {
+          DO[q] = d2[u];
+          RO[q] = r2[u];
+        }
+      } else {
+        r2[u] = ok ? R2[q] : z2;
+        d2[u] = (ok && dot) ? D2[q] : z2;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      if (qb + u * st + lane < n2) {
+        const double g0 = dot ? wa * d2[u].x : 0.0, g1 = dot ? wa * d2[u].y : 0.0;
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+          prep_elem_w(A[r], a2[u][r].x, r2[u].x, g0, dot, L, U_, fmin[r], fmax[r]);
+          prep_elem_w(A[r], a2[u][r].y, r2[u].y, g1, dot, L, U_, fmin[r], fmax[r]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < G; ++r) warp_minmax(fmin[r], fmax[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < G; ++r)
+    block_reduce_store<PREP_SLOTS>(A[r].v, PREP_SLOTS, PH_PREP, (j0 + r) * PREP_SLOTS, c.out, c.smem);
+}
+
+// Dense rows, no partition, device-resident aligned inputs: the direction
+// pass fused with the first row group, then groups of PREP_GROUP rows.
+constexpr int PREP_GROUP = 2;
+__device__ __noinline__ void prep_dense_grouped(const PassCtx& c, int m, int64_t n, bool dir,
+                                                bool dot, bool use_dp, double beta, double wa,
+                                                double L, double U_) {
+  int j = 0;
+  if (dir) {
+    if (m >= PREP_GROUP) {
+      prep_group<PREP_GROUP, true>(c, 0, n, dot, use_dp, beta, wa, L, U_);
+      j = PREP_GROUP;
+    } else {
+      prep_group<1, true>(c, 0, n, dot, use_dp, beta, wa, L, U_);
+      j = 1;
+    }
+  }
+  for (; j + PREP_GROUP <= m; j += PREP_GROUP)
+    prep_group<PREP_GROUP, false>(c, j, n, dot, use_dp, beta, wa, L, U_);
+  for (; j < m; ++j) prep_group<1, false>(c, j, n, dot, use_dp, beta, wa, L, U_);
+}
+
 __device__ __noinline__ void pass_prep(const PassCtx& c) {
   const Plan& pl = *c.plan;
   const Problem& P = pl.P;
@@ -700,6 +802,12 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
   // 16-byte pairs (a range row only over its own range; outside it only a_j
   // is read, for the validation count), same per-element arithmetic
   if ((!owner || P.part_ranges) && P.chunk <= 0) {
+    if (dir && !owner && !P.structured && (n & 1) == 0 && (ld & 1) == 0 && al16(P.grad) &&
+        al16(g) && al16(x) && al16(dout) && al16(rho) && (!use_dp || al16(dp))) {
+      prep_dense_grouped(c, m, n, dir, dot, use_dp, beta, wa, L, U_);
+      compact_init(c);
+      return;
+    }
     if (dir) {
       StreamRows D;
       D.nr = 3;
@@ -1593,6 +1701,67 @@ __device__ __noinline__ void pass_feas_streamed(const PassCtx& c) {
   }
 }
 
+// Dense rows, exact m = M (C4/C5): pass_feas_streamed with one base pointer
+// for the rows and the candidates' (row, dual) re-read from the shared-memory
+// command per element (register-lean: no spills in the loop).  Same element
+// order per thread and the same per-element arithmetic; the zero-padded warp
+// reduction of M and of pass_feas_streamed's 8 slots are the same.
+template <int M>
+__device__ __noinline__ void pass_feas_dense(const PassCtx& c) {
+  const Plan& pl = *c.plan;
+  const Problem& P = pl.P;
+  const Cmd& cmd = *c.cmd;
+  const double L = P.lower, U = P.upper;
+  const int64_t n2 = P.n >> 1, st = c.stride, ld2 = P.ld >> 1;
+  const double2* __restrict__ R2 = reinterpret_cast<const double2*>(P.rho);
+  const double2* __restrict__ A2 = reinterpret_cast<const double2*>(P.grad);
+  const volatile int* frow = cmd.feas_row;
+  const volatile double* fy = cmd.feas_y;
+  for (int f0 = 0; f0 < cmd.nfeas; f0 += FEAS_GROUP) {
+    const int ng = cmd.nfeas - f0 < FEAS_GROUP ? cmd.nfeas - f0 : FEAS_GROUP;
+    double acc[FEAS_GROUP][M];
+#pragma unroll
+    for (int g = 0; g < FEAS_GROUP; ++g)
+#pragma unroll
+      for (int k = 0; k < M; ++k) acc[g][k] = 0.0;
+    auto one = [&](const double (&a)[M], double r) {
+      const double lo = L - r, hi = U - r;
+#pragma unroll
+      for (int g = 0; g < FEAS_GROUP; ++g) {
+        const int rj = g < ng ? frow[f0 + g] : -1;
+        const double yj = g < ng ? fy[f0 + g] : 0.0;
+        double z = 0.0;
+        if (rj >= 0 && yj != 0.0) {
+          double arj = 0.0;
+#pragma unroll
+          for (int k = 0; k < M; ++k)
+            if (k == rj) arj = a[k];
+          z = 0.0 + yj * arj;
+        }
+        const double dl = clipd(z, lo, hi);
+#pragma unroll
+        for (int k = 0; k < M; ++k) acc[g][k] += a[k] * dl;
+      }
+    };
+    for (int64_t q = c.i0; q < n2; q += st) {
+      double2 v2[M + 1];
+      v2[0] = R2[q];
+#pragma unroll
+      for (int k = 0; k < M; ++k) v2[1 + k] = A2[(int64_t)k * ld2 + q];
+      double a[M];
+#pragma unroll
+      for (int k = 0; k < M; ++k) a[k] = v2[1 + k].x;
+      one(a, v2[0].x);
+#pragma unroll
+      for (int k = 0; k < M; ++k) a[k] = v2[1 + k].y;
+      one(a, v2[0].y);
+    }
+#pragma unroll
+    for (int g = 0; g < FEAS_GROUP; ++g)
+      if (g < ng) block_reduce_store<M>(acc[g], M, PH_FEAS, (f0 + g) * M, c.out, c.smem);
+  }
+}
+
 __device__ __noinline__ void pass_feas(const PassCtx& c) {
   const Plan& pl = *c.plan;
   const Problem& P = pl.P;
@@ -1602,6 +1771,10 @@ __device__ __noinline__ void pass_feas(const PassCtx& c) {
   const int64_t n = P.n, st = c.stride, ld = P.ld;
   const double* __restrict__ rho = P.rho;
   const double* __restrict__ grad = P.grad;
+  if (m == 7 && !P.structured && (n & 1) == 0 && (ld & 1) == 0 && al16(rho) && al16(grad)) {
+    pass_feas_dense<7>(c);
+    return;
+  }
   if (m <= 8) {   // 16-byte pairs, FEAS_GROUP candidates per pass
     pass_feas_streamed(c);
     return;
@@ -1632,6 +1805,72 @@ __device__ __noinline__ void pass_feas(const PassCtx& c) {
 // Register version: per thread the h-dots and the packed Gram triangle (M
 // exact for m = 7: 28 accumulators); the rows come as 16-byte pairs
 // (rows_pairs), two elements' loads in flight per thread.
+// Dense rows, exact m = M (C4/C5): a register-lean copy of pass_newton_m's
+// rows_pairs loop -- one base pointer for the rows and the duals re-read
+// from the shared-memory command per element, so the m + m(m+1)/2
+// accumulators and the m + 1 pair loads fit without spilling.  Same elements
+// per thread in the same order and the same per-element arithmetic.
+template <int M>
+__device__ __noinline__ void pass_newton_dense(const PassCtx& c) {
+  const Plan& pl = *c.plan;
+  const Problem& P = pl.P;
+  const Cmd& cmd = *c.cmd;
+  const double L = P.lower, U = P.upper;
+  const int64_t n = P.n, st = c.stride, ld = P.ld;
+  const double* __restrict__ rho = P.rho;
+  const double* __restrict__ grad = P.grad;
+  const bool want_gram = cmd.want_gram;
+  constexpr int NG = M * (M + 1) / 2;
+  double h[M], G[NG];
+#pragma unroll
+  for (int k = 0; k < M; ++k) h[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < NG; ++k) G[k] = 0.0;
+  const volatile double* ys = cmd.y;
+  const double2* __restrict__ R2 = reinterpret_cast<const double2*>(rho);
+  const double2* __restrict__ A2 = reinterpret_cast<const double2*>(grad);
+  const int64_t n2 = n >> 1, ld2 = ld >> 1;
+  auto one = [&](const double (&a)[M], double r) {
+    const double lo = L - r, hi = U - r;
+    double z = 0.0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const double yk = ys[k];
+      if (yk != 0.0) z += yk * a[k];
+    }
+    const bool clipped = (z < lo) || (z > hi);
+    const double dl = clipd(z, lo, hi);
+#pragma unroll
+    for (int k = 0; k < M; ++k) h[k] += a[k] * dl;
+    if (want_gram && !clipped) {
+      int q = 0;
+#pragma unroll
+      for (int j = 0; j < M; ++j)
+#pragma unroll
+        for (int k = j; k < M; ++k) { G[q] = __fma_rn(a[j], a[k], G[q]); ++q; }
+    }
+  };
+  for (int64_t q = c.i0; q < n2; q += st) {
+    double2 v2[M + 1];
+    v2[0] = R2[q];
+#pragma unroll
+    for (int k = 0; k < M; ++k) v2[1 + k] = A2[(int64_t)k * ld2 + q];
+    double a[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) a[k] = v2[1 + k].x;
+    one(a, v2[0].x);
+#pragma unroll
+    for (int k = 0; k < M; ++k) a[k] = v2[1 + k].y;
+    one(a, v2[0].y);
+  }
+  double v[M + NG];
+#pragma unroll
+  for (int k = 0; k < M; ++k) v[k] = h[k];
+#pragma unroll
+  for (int k = 0; k < NG; ++k) v[M + k] = G[k];   // m = M: gram_idx is the packed order
+  block_reduce_store<M + NG>(v, M + NG, PH_NEWTON, 0, c.out, c.smem);
+}
+
 template <int M>
 __device__ __noinline__ void pass_newton_m(const PassCtx& c) {
   const Plan& pl = *c.plan;
@@ -1921,7 +2160,14 @@ __device__ void pass_final(const PassCtx& c) {
 
 __device__ void pass_newton(const PassCtx& c) {
   const int m = c.plan->P.m;
-  if (m == 7) { pass_newton_m<7>(c); return; }
+  if (m == 7) {
+    const Problem& P = c.plan->P;
+    if (!P.structured && (P.n & 1) == 0 && (P.ld & 1) == 0 && al16(P.rho) && al16(P.grad))
+      pass_newton_dense<7>(c);
+    else
+      pass_newton_m<7>(c);
+    return;
+  }
   if (m <= 1) pass_newton_m<1>(c);
   else if (m <= 2) pass_newton_m<2>(c);
   else if (m <= 4) pass_newton_m<4>(c);
