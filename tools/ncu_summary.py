@@ -24,8 +24,11 @@ STALLS = ["long_scoreboard", "wait", "barrier", "short_scoreboard", "math_pipe_t
 
 
 def from_report(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if path.endswith("_raw.csv"):   # `ncu -i <rep> --page raw --csv` exported on the GPU box
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     out = [f"# ncu summary: {path}", ""]
@@ -73,4 +76,5 @@ def from_launches(path):
 
 if __name__ == "__main__":
     p = sys.argv[1]
-    print(from_launches(p) if p.endswith(".csv") else from_report(p))
+    print(from_launches(p) if p.endswith(".csv") and not p.endswith("_raw.csv")
+          else from_report(p))
