@@ -75,3 +75,30 @@ def test_pgd_step_small(name):
     assert st.projection.path.name == ref["path"]
     x_o = ref["x_new"]
     assert np.max(np.abs(st.x_new - x_o)) <= 1e-12 * np.max(np.abs(x_o))
+
+
+@pytest.mark.parametrize("m", [2, 3, 5, 6])
+@pytest.mark.parametrize("half_g", [False, True])
+def test_pgd_step_dense_row_groups(m, half_g):
+    """Dense rows without a partition take the grouped PREP (rows in pairs,
+    the first pair fused with the direction pass; odd m ends on a single
+    row).  half_g: g_prev = g / 2, so beta = 2 > 0 and d_prev is read
+    (beta = 0 otherwise on this data)."""
+    import dataclasses
+    p = synth.SMALL["C4p"](5)
+    p = dataclasses.replace(p, name=f"C4p_m{m}", m=m, grad=np.ascontiguousarray(p.grad[:m]),
+                            g_values=p.g_values[:m].copy(), bounds_g=p.bounds_g[:m].copy(),
+                            is_eq=p.is_eq[:m].copy(), rows=None)
+    if half_g:
+        p = dataclasses.replace(p, g_prev=0.5 * p.g)
+    ref = O.pgd_step(p)
+    st = api.pgd_step(p.x, p.x_prev, p.g, p.g_prev, p.d_prev, p.grad, p.g_values, p.bounds_g,
+                      p.is_eq, p.partition, t=p.t, want_delta=True)
+    assert st.alpha == pytest.approx(ref["alpha"], rel=1e-13)
+    assert st.beta == pytest.approx(ref["beta"], rel=1e-12, abs=1e-300)
+    np.testing.assert_allclose(st.d, ref["d"], rtol=1e-13, atol=0)
+    assert st.projection.path.name == ref["path"]
+    x_o = ref["x_new"]
+    if ref["path"] == "newton":
+        assert st.projection.newton_iters == ref["newton_iters"]
+    assert np.max(np.abs(st.x_new - x_o)) <= 1e-12 * np.max(np.abs(x_o))
