@@ -1033,7 +1033,7 @@ __device__ __forceinline__ void sweep_elem(double a, double r, const double* y, 
   const double cl = a * (pos ? lo : hi), ch = a * (pos ? hi : lo), aa = a * a;
   int p1 = 0, p2 = 0;   // p1 = #{y_k < bl}, p2 = #{y_k <= bh}
 #pragma unroll
-  for (int s = (KC >= 16 ? 16 : KC); s > 0; s >>= 1) {
+  for (int s = (KC >= 16 ? 16 : pow2_at_least(KC)); s > 0; s >>= 1) {
     if (p1 + s <= cnt && y[p1 + s - 1] < bl) p1 += s;
     if (p2 + s <= cnt && y[p2 + s - 1] <= bh) p2 += s;
   }
@@ -1080,7 +1080,7 @@ struct SweepAcc {
       const double bl = pos ? b1 : b2, bh = pos ? b2 : b1;
       int p1 = 0, p2 = 0;
 #pragma unroll
-      for (int s = (KC >= 16 ? 16 : KC); s > 0; s >>= 1) {
+      for (int s = (KC >= 16 ? 16 : pow2_at_least(KC)); s > 0; s >>= 1) {
         if (p1 + s <= cnt && y[p1 + s - 1] < bl) p1 += s;
         if (p2 + s <= cnt && y[p2 + s - 1] <= bh) p2 += s;
       }
@@ -1331,8 +1331,12 @@ __device__ void pass_sweep(const PassCtx& c) {
       else pass_sweep_row_compact<MAX_K>(c, j, b, cnt);
       continue;
     }
+    // (10 / 12: the multi-row stage-1 sweeps, MAX_CAND / rows candidates per
+    // row -- the per-element work is one select + add per template slot)
     if (cnt <= 4) pass_sweep_row<4>(c, j, b, cnt);
     else if (cnt <= 8) pass_sweep_row<8>(c, j, b, cnt);
+    else if (cnt <= 10) pass_sweep_row<10>(c, j, b, cnt);
+    else if (cnt <= 12) pass_sweep_row<12>(c, j, b, cnt);
     else pass_sweep_row<MAX_K>(c, j, b, cnt);
   }
   if (cmd.compact && c.list) {   // active elements left in this CTA
