@@ -574,18 +574,19 @@ __device__ __forceinline__ void prep_elem(PrepAcc& A, double a, double r, double
   }
 }
 
-// Does an element's exact breakpoint num / a (the rounded quotient) possibly
-// lie below the filter value m (MAX: above it)?  Real arithmetic: num / a < m
-// <=> num < m a (a > 0), num > m a (a < 0).  The product and the quotient are
-// rounded, so the test keeps a 1e-14 relative (+1e-300 absolute) margin in
-// the element's favour, and says "maybe" outside the range it can check.
+// Does an element's breakpoint fl(num / a) possibly lie below the filter
+// value m (MAX: above it)?  It is skipped only when a STRICT comparison with
+// the correctly rounded product t = fl(m a) proves it cannot: for a > 0,
+// num > t means num >= succ(t) > m a (round-to-nearest puts m a within half
+// an ulp of t), so num / a > m and, the division rounding monotonically,
+// fl(num / a) >= m -- it cannot be a new minimum.  a < 0 flips the test, MAX
+// mirrors it.  Overflow (t = +-inf) and NaN make every comparison false:
+// "maybe", the division runs.  (-fmad=false: t is one rounded product.)
 template <bool MAX>
 __device__ __forceinline__ bool bp_may_beat(double num, double a, double m) {
   const double t = m * a;
-  if (!(fabs(t) < 1e300) || !(fabs(num) < 1e300)) return true;
-  const double e = 1e-14 * fabs(t) + 1e-300;
   const bool flip = (a > 0.0) == MAX;
-  return flip ? (num > t - e) : (num < t + e);
+  return flip ? !(num < t) : !(num > t);
 }
 
 // prep_elem with the breakpoint divisions filtered against (fmin, fmax):
