@@ -465,33 +465,9 @@ struct StepAcc {
   }
 };
 
-// L2 prefetch (cp.async.bulk.prefetch, one instruction per contiguous run)
-// of the 16-byte pairs this CTA will read in a grid-stride pair loop:
-// pairs [blockIdx.x * blockDim.x + k * stride, + blockDim.x) for k = 0, 1, ...
-// Issued by warp 0, lane k for run k.  A hint only: no data is written.
-__device__ __forceinline__ void prefetch_cta_pairs_l2(const double* base, int64_t n2,
-                                                      const PassCtx& c) {
-  if (threadIdx.x >= 32 || base == nullptr || !al16(base)) return;
-  const int64_t b0 = (int64_t)blockIdx.x * blockDim.x;
-  for (int64_t k = threadIdx.x; b0 + k * c.stride < n2; k += 32) {
-    const int64_t q = b0 + k * c.stride;
-    const int64_t cnt = (n2 - q) < (int64_t)blockDim.x ? (n2 - q) : (int64_t)blockDim.x;
-    const char* p = reinterpret_cast<const char*>(base) + q * 16;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((unsigned)(cnt * 16))
-                 : "memory");
-  }
-}
-
 __device__ __noinline__ void pass_step_reduce(const PassCtx& c) {
   const Problem& P = c.plan->P;
   const int64_t st = c.stride;
-  // One row, no partition, device-resident (C1/C2): the fused PREP pass that
-  // follows reads d_prev and a_0 besides this pass's x and g; start them
-  // into L2 now so PREP's loads hit L2 (16 bytes per element, small n only).
-  if (P.m == 1 && !P.owner && P.chunk <= 0 && (P.n & 1) == 0 && P.n <= (int64_t(1) << 22)) {
-    prefetch_cta_pairs_l2(P.d_prev, P.n >> 1, c);
-    prefetch_cta_pairs_l2(P.grad, P.n >> 1, c);
-  }
   const double* __restrict__ x = P.x;
   const double* __restrict__ xp = P.x_prev;
   const double* __restrict__ g = P.g;
