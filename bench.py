@@ -32,6 +32,9 @@ sys.path.insert(0, ROOT)
 
 BYTES_PER_VAR = {"C1": 64, "C2": 64, "C3": 64, "C4": 112, "C4p": 112, "C5": 112}
 METRIC = "PGD-TO step throughput (design vars/s)"
+WORKLOADS = {"C1": "C1_min_compliance_256x128", "C2": "C2_min_volume_1024x1024",
+             "C3": "C3_multi_material_4x128x128x64", "C4": "C4_com_256x256x128",
+             "C4p": "C4p_com_256x256x128_comx+0.02", "C5": "C5_com_1024x512x512"}
 
 
 def measured_peak():
@@ -136,21 +139,71 @@ class ClockSampler:
                 "samples": len(rows), "source": src}
 
 
-def make_problem(config, seed, world=1):
-    """The global problem.  N > 1 runs weak scaling: the grid grows along its
-    slowest axis so each rank's slab keeps the single-GPU size (C5 is the
-    fixed-size scale sweep of BASELINE.json and is not grown)."""
+def make_problem(config, seed, world=1, rank=0):
+    """This rank's slab of the global problem (each rank generates only its
+    own slab; synth's chunked streams make it bit-identical to slicing the
+    global arrays).  C5 is BASELINE.json's fixed-size scale sweep (strong
+    scaling: the 268M-element problem is split over the ranks); the others
+    grow along their slowest axis so each rank keeps the single-GPU size
+    (weak scaling)."""
     from paper_2511_13905_b200 import synth
-    if world == 1 or config == "C5":
+    if world == 1:
         return synth.CONFIGS[config](seed)
-    if config == "C1":
-        return synth.min_compliance_volume(256, 128 * world, seed)
-    if config == "C2":
-        return synth.min_volume_compliance(1024, 1024 * world, seed)
-    if config in ("C4", "C4p"):
-        return synth.com_constrained(256, 256, 128 * world, seed,
-                                     com_offset_x=0.02 if config == "C4p" else 0.0)
-    raise SystemExit(f"--gpus > 1 is not supported for {config}")
+    grids = {"C1": lambda: (synth.min_compliance_volume, (256, 128 * world)),
+             "C2": lambda: (synth.min_volume_compliance, (1024, 1024 * world)),
+             "C4": lambda: (synth.com_constrained, (256, 256, 128 * world)),
+             "C4p": lambda: (synth.com_constrained, (256, 256, 128 * world)),
+             "C5": lambda: (synth.com_constrained, (1024, 512, 512))}
+    if config not in grids:
+        raise SystemExit(f"--gpus > 1 is not supported for {config} (partitioned rows)")
+    fn, dims = grids[config]()
+    n = 1
+    for d in dims:
+        n *= d
+    slab = (rank * n // world, (rank + 1) * n // world)
+    kw = {"com_offset_x": 0.02} if config == "C4p" else {}
+    return fn(*dims, seed, slab=slab, **kw)
+
+
+def scaling_kind(config):
+    return "strong" if config == "C5" else "weak"
+
+
+def host_cpu():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
+class pinned_core:
+    """Pin this process to one host core for the single-threaded reference
+    timing (restored afterwards)."""
+
+    def __enter__(self):
+        self.old = None
+        self.core = None
+        try:
+            self.old = os.sched_getaffinity(0)
+            self.core = max(self.old)
+            os.sched_setaffinity(0, {self.core})
+        except (AttributeError, OSError):
+            pass
+        return self
+
+    def __exit__(self, *a):
+        if self.old is not None:
+            try:
+                os.sched_setaffinity(0, self.old)
+            except OSError:
+                pass
+        return False
 
 
 def progress(msg):
@@ -174,6 +227,16 @@ def cpu_reference_sample(p, budget_s=12.0, max_reps=50):
     reference's own build+project (oracle/_ref), 1 thread, a bounded sample."""
     import oracle as O
     kind = "reference" if O.ref_available() else "port"
+    with pinned_core() as pc:
+        reps, dt = _cpu_reps(O, kind, p, budget_s, max_reps)
+    model, ncpu = host_cpu()
+    return {"value": p.n * reps / dt, "unit": "design vars/s", "cores": 1, "kind": kind,
+            "sample": f"{reps} full steps of {p.name} (n={p.n}), single-threaded, "
+                      f"{dt:.1f} s", "ms_per_step": 1e3 * dt / reps,
+            "cpu_model": model, "host_cpus": ncpu, "pinned_core": pc.core}
+
+
+def _cpu_reps(O, kind, p, budget_s, max_reps):
     reps, t0 = 0, time.perf_counter()
     while reps < max_reps:
         d, gd, rt, info = O.step_direction(p.x, p.x_prev, p.g, p.g_prev, p.d_prev, p.t,
@@ -187,35 +250,42 @@ def cpu_reference_sample(p, budget_s=12.0, max_reps=50):
         reps += 1
         if time.perf_counter() - t0 > budget_s:
             break
-    dt = time.perf_counter() - t0
-    return {"value": p.n * reps / dt, "unit": "design vars/s", "cores": 1, "kind": kind,
-            "sample": f"{reps} full steps of {p.name} (n={p.n}), single-threaded, "
-                      f"{dt:.1f} s", "ms_per_step": 1e3 * dt / reps}
+    return reps, time.perf_counter() - t0
+
+
+def bench_config(args, p_global_n, m):
+    """The `config` object both arms print (identical dicts: the workload)."""
+    return {"workload": WORKLOADS.get(args.config, args.config), "n": p_global_n, "m": m,
+            "seed": args.seed}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
     p = cpu_sample_problem(args.config, args.seed)
-    # each "step" is the bounded sample of one full reference step
-    for _ in range(args.warmup):
-        cpu_reference_sample(p, budget_s=0.0, max_reps=1)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        cpu_reference_sample(p, budget_s=0.0, max_reps=1)
-    dt = (time.perf_counter() - t0) / args.steps
     import oracle as O
     kind = "reference" if O.ref_available() else "port"
+    # each "step" is the bounded sample of one full reference step
+    with pinned_core() as pc:
+        _cpu_reps(O, kind, p, 0.0, args.warmup)
+        reps, dt = _cpu_reps(O, kind, p, 0.0, args.steps)
+    dt /= reps
+    model, ncpu = host_cpu()
     val = p.n / dt
+    n_full = {"C1": 32768, "C2": 1 << 20, "C3": 4 << 20, "C4": 8 << 20, "C4p": 8 << 20,
+              "C5": 1 << 28}.get(args.config, p.n)
     line = {"metric": METRIC, "value": val, "unit": "design vars/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded, BASELINE.json config distributions)",
-            "config": {"workload": p.name, "n": p.n, "m": p.m, "seed": args.seed},
+            "higher_is_better": True, "scaling": scaling_kind(args.config), "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config distributions)",
+            "config": bench_config(args, n_full, p.m),
             "impl": "reference",
             "cpu_baseline": {"value": val, "unit": "design vars/s", "cores": 1, "kind": kind,
-                             "sample": f"{args.steps} full steps of {p.name}, 1 thread "
-                                       "(the reference is single-threaded)"},
+                             "sample": f"{args.steps} full steps of {p.name} (n={p.n})"
+                                       + ("" if p.n == n_full else
+                                          f", a bounded sample of the n={n_full} workload")
+                                       + ", 1 thread (the reference is single-threaded)",
+                             "cpu_model": model, "host_cpus": ncpu, "pinned_core": pc.core},
             "e2e": {"value": val, "unit": "design vars/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -229,13 +299,12 @@ def run_ours(args, rank, world):
     dev = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
     progress("problem")
-    gp = make_problem(args.config, args.seed, world)
-    # contiguous element slab of this rank (z-slabs for the 3-D grids)
-    lo, hi = rank * gp.n // world, (rank + 1) * gp.n // world
-    n, m = hi - lo, gp.m
+    gp = make_problem(args.config, args.seed, world, rank)
+    # this rank's contiguous element slab (z-slabs for the 3-D grids)
+    n, m = gp.n, gp.m
     cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{dev}")  # noqa: E731
-    X = {k: cu(getattr(gp, k)[lo:hi]) for k in ("x", "x_prev", "g", "g_prev", "d_prev")}
-    A = cu(gp.grad[:, lo:hi].reshape(-1))
+    X = {k: cu(getattr(gp, k)) for k in ("x", "x_prev", "g", "g_prev", "d_prev")}
+    A = cu(gp.grad.reshape(-1))
     outs = {k: torch.empty(n, dtype=torch.float64, device=f"cuda:{dev}")
             for k in ("x_new", "d", "rho_tilde")}
     if world > 1:
@@ -256,7 +325,7 @@ def run_ours(args, rank, world):
     prepared = api.prepare_pgd_step(X["x"], X["x_prev"], X["g"], X["g_prev"], X["d_prev"], A,
                                     gp.g_values, gp.bounds_g, gp.is_eq, part, t=gp.t,
                                     violation=gp.violation, lower=gp.lower, upper=gp.upper,
-                                    device=dev, out=outs, ctx=ctx, n_global=gp.n)
+                                    device=dev, out=outs, ctx=ctx, n_global=gp.n_global)
 
     def step():
         return prepared.run()
@@ -302,8 +371,8 @@ def run_ours(args, rank, world):
     progress("e2e")
     # ---- e2e: pinned host inputs -> H2D -> step -> D2H x_new, d --------------
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-    H = {k: pin(getattr(gp, k)[lo:hi]) for k in ("x", "x_prev", "g", "g_prev", "d_prev")}
-    HA = pin(gp.grad[:, lo:hi].reshape(-1))
+    H = {k: pin(getattr(gp, k)) for k in ("x", "x_prev", "g", "g_prev", "d_prev")}
+    HA = pin(gp.grad.reshape(-1))
     HO = {k: torch.empty(n, dtype=torch.float64).pin_memory() for k in ("x_new", "d")}
     e2e_steps = max(3, min(args.steps, 10))
 
@@ -351,7 +420,7 @@ def run_ours(args, rank, world):
         return
     peak, peak_kind = measured_peak()
     b_alg = BYTES_PER_VAR.get(args.config, 64) * n
-    total_n = gp.n
+    total_n = gp.n_global
     value = total_n / (ms * 1e-3)
     # dominant kernel: k_pass (every pass of the step is one launch of it)
     per_launch_bytes = b_alg / max(1.0, kern["launches"] / max(1, min(args.steps, 10)))
@@ -365,16 +434,20 @@ def run_ours(args, rank, world):
     line = {
         "metric": METRIC, "value": value, "unit": "design vars/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded, BASELINE.json config distributions)",
-        "config": {"workload": p.name, "n": gp.n, "n_per_rank": n, "m": m, "seed": args.seed,
-                   "parallelism": f"element slabs x{world}" + (", NCCL all-gather of pass "
-                                                               "partials" if world > 1 else ""),
-                   "l2": "flushed (256 MiB write) between timed steps",
-                   "path": res.projection.path.name,
-                   "passes_per_step": res.projection.passes,
-                   "sweeps_per_step": res.projection.sweeps,
-                   "near_ties": res.projection.near_ties},
+        "higher_is_better": True, "scaling": scaling_kind(args.config), "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config distributions)",
+        "config": bench_config(args, gp.n_global, m),
+        "run": {"n_per_rank": n,
+                "parallelism": f"element slabs x{world}" + (", NCCL all-gather of pass "
+                                                            "partials" if world > 1 else ""),
+                "l2": "flushed (256 MiB write) between timed steps",
+                "path": res.projection.path.name,
+                "newton_iters": res.projection.newton_iters,
+                "converged": bool(res.projection.converged),
+                "passes_per_step": res.projection.passes,
+                "sweeps_per_step": res.projection.sweeps,
+                "near_ties": res.projection.near_ties,
+                "parity_mode": "certified"},
         "achieved_hbm_gbs_step": b_alg / (ms * 1e-3) / 1e9,
         "ms_per_step_outer_events": outer_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -408,10 +481,6 @@ def measured_traffic(workload, world):
     return t.get("bytes_per_launch")
 
 
-def ctx_kernel_stats(ctx):
-    return {}
-
-
 def kernel_pass_stats(ctx, step, steps, flush):
     """Average device duration of one k_pass launch (CUDA events on the
     launching stream, inside the library), over `steps` extra steps."""
@@ -431,7 +500,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5",
+                    help="C1..C5 (BASELINE.json order) or C4p; default C5, the largest "
+                         "single-GPU config and north_star's scale target")
     ap.add_argument("--seed", type=int, default=None,
                     help="default: the config's own number (C1 -> 1, ..., C5 -> 5)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -440,8 +511,20 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.seed is None:
         args.seed = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C4p": 4, "C5": 5}.get(args.config, 1)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # not launched by torchrun: start one rank per GPU ourselves
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch
         backend = "gloo" if args.impl == "reference" else "nccl"

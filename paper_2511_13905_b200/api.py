@@ -133,9 +133,26 @@ def _ptr(a):
     return a.ctypes.data
 
 
-def _f64(a):
-    if a is None or _is_torch_cuda(a):
+def _dev_f64(a, name, numel=None, device=None):
+    """A torch CUDA tensor the C-ABI may read as contiguous fp64 at data_ptr():
+    float64, on `device` (a torch.device or None), `numel` elements; strided
+    views are made contiguous (the caller keeps the returned tensor alive).
+    Anything else is a DomainError -- never silently reinterpreted."""
+    import torch
+    if a.dtype != torch.float64:
+        raise DomainError(f"{name}: expected a float64 tensor, got {a.dtype}")
+    if device is not None and a.device != device:
+        raise DomainError(f"{name}: tensor on {a.device}, expected {device}")
+    if numel is not None and a.numel() != numel:
+        raise DomainError(f"{name}: {a.numel()} elements, expected {numel}")
+    return a if a.is_contiguous() else a.contiguous()
+
+
+def _f64(a, name="array"):
+    if a is None:
         return a
+    if _is_torch_cuda(a):
+        return _dev_f64(a, name)
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
@@ -178,12 +195,13 @@ class ConstraintLinearization:
         lin.num_vars = int(n)
         lin._device = device
         if _is_torch_cuda(grad):
+            grad = _dev_f64(grad, "grad", m * n)
             lin.grad = grad.reshape(m, n) if m * n else grad
         else:
             lin.grad = np.ascontiguousarray(np.asarray(grad, np.float64).reshape(-1))
         lin.g_values = np.ascontiguousarray(g_values, np.float64).reshape(-1)
         lin.bounds_g = np.ascontiguousarray(bounds_g, np.float64).reshape(-1)
-        lin.gd_step = _f64(gd_step)
+        lin.gd_step = _f64(gd_step, "gd_step")
         lin.is_equality = (np.zeros(m, np.uint8) if is_equality is None or len(is_equality) == 0
                            else np.ascontiguousarray(is_equality, np.uint8))
         lin.partition = partition
@@ -259,6 +277,11 @@ class _LinC:
         return False
 
 
+def _host_only(lin, rho, fn):
+    if _is_torch_cuda(rho) or _is_torch_cuda(lin.grad) or _is_torch_cuda(lin.gd_step):
+        raise DomainError(f"{fn}: takes host (numpy) arrays")
+
+
 def _check_rho(lin, rho):
     n = rho.numel() if _is_torch_cuda(rho) else np.asarray(rho).size
     if n != lin.num_vars:
@@ -268,6 +291,7 @@ def _check_rho(lin, rho):
 # ---- projection.hpp:66-109 ---------------------------------------------------
 def delta_of_y(y, lin: ConstraintLinearization, rho_tilde, lower, upper):
     rho = _f64(rho_tilde)
+    _host_only(lin, rho, "delta_of_y")
     _check_rho(lin, rho)
     y = np.ascontiguousarray(y, np.float64)
     if y.size != lin.num_constraints:
@@ -286,6 +310,7 @@ def constraint_residual_h(y, lin: ConstraintLinearization, rho_tilde, lower, upp
     y = np.ascontiguousarray(y, np.float64)
     if not (c > 0.0):
         raise ParameterError("constraint_residual_h: c must be > 0")
+    _host_only(lin, rho, "constraint_residual_h")
     _check_rho(lin, rho)
     if y.size != lin.num_constraints:
         raise DomainError("delta_of_y: dual size does not match linearization")
@@ -300,7 +325,12 @@ def constraint_residual_h(y, lin: ConstraintLinearization, rho_tilde, lower, upp
 
 def _project(which, rho_tilde, lin, lower, upper, options: ProjectionOptions,
              want_mask=False):
-    rho = _f64(rho_tilde)
+    rho = _f64(rho_tilde, "rho_tilde")
+    if _is_torch_cuda(rho) != _is_torch_cuda(lin.grad):
+        raise DomainError("projection: rho_tilde and the linearization must both be host "
+                          "arrays or both CUDA tensors")
+    if _is_torch_cuda(rho) and lin.grad.device != rho.device:
+        raise DomainError("projection: rho_tilde and grad are on different devices")
     _check_rho(lin, rho)
     ctx = L.context(lin._device)
     m, n = lin.num_constraints, lin.num_vars
@@ -477,7 +507,23 @@ def prepare_pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_
     o.y, o.slacks, o.g_hat = _ptr(y), _ptr(sl), _ptr(gh)
     if dev:
         import torch
+        dv = x.device
+        x = _dev_f64(x, "x", n, dv)
+        x_prev = _dev_f64(x_prev, "x_prev", n, dv)
+        g = _dev_f64(g, "g", n, dv)
+        g_prev = _dev_f64(g_prev, "g_prev", n, dv)
+        d_prev = _dev_f64(d_prev, "d_prev", n, dv)
+        if grad is not None:
+            grad = _dev_f64(grad, "grad", m * n, dv)
+        elif rows is None:
+            raise DomainError("pgd_step: grad is required unless structured rows are given")
         bufs = out or {}
+        for k in ("x_new", "d", "rho_tilde", "delta"):
+            b = bufs.get(k)
+            if b is not None and (b.dtype != torch.float64 or b.device != dv
+                                  or b.numel() != n or not b.is_contiguous()):
+                raise DomainError(f"pgd_step: out[{k!r}] must be a contiguous float64 tensor "
+                                  f"of {n} elements on {dv}")
         x_new = bufs.get("x_new") if bufs.get("x_new") is not None else torch.empty_like(x)
         d = bufs.get("d") if bufs.get("d") is not None else torch.empty_like(x)
         rt = bufs.get("rho_tilde") if bufs.get("rho_tilde") is not None else torch.empty_like(x)

@@ -373,6 +373,27 @@ __global__ void k_owner_pack(const int32_t* o32, int8_t* o8, int64_t n) {
     o8[i] = (int8_t)o32[i];
 }
 
+// Streaming probe: spin (bounded, ~50 ms) on a flag that the copy stream
+// writes after this launch.  It sees the write only when kernels and copy-
+// stream operations really run concurrently -- not under CUDA_LAUNCH_BLOCKING,
+// a serializing profiler or a sanitizer; the host then uploads first.
+__global__ void k_stream_probe(const unsigned* flag, unsigned epoch, int* seen) {
+  if (threadIdx.x != 0) return;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  int ok = 0;
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if ((int)(v - epoch) >= 0) { ok = 1; break; }
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 50000000ull) break;
+    __nanosleep(1000);
+  }
+  *seen = ok;
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -459,6 +480,9 @@ struct topt_b200_ctx {
   int* h_timed_out = nullptr;      // pinned
   uint32_t epoch = 0;
   int stream_inputs = 1;           // TOPT_B200_STREAM=0 disables
+  int stream_probe = -1;
+  int stream_timeout = 0;          // the last streamed launch timed out waiting for a chunk           // can a running kernel see copy-stream writes? (-1: unknown)
+  int* d_probe = nullptr;
   Plan* hp_pin = nullptr;          // pinned staging of the plan (upload / results)
   // structured rows for the following *_dev / *_ranks steps (topt_b200_set_structured_rows)
   int srows_m = 0;
@@ -700,8 +724,10 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     ctx->hp_pin->cmd.phase = ctx->hp_pin->res.final_phase;
     plan_results_take(ctx, hp);
-    if (si && *ctx->h_timed_out)
+    if (si && *ctx->h_timed_out) {
+      ctx->stream_timeout = 1;
       return fail(ctx, TOPT_ERR_CUDA, "topt_b200: a streamed input chunk never arrived");
+    }
     if (ctx->profile) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
@@ -1070,6 +1096,7 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   ok = ok && cudaMalloc(&ctx->d_flags, sizeof(unsigned) * 4 * MAX_STREAM_CHUNKS) == cudaSuccess;
   ok = ok && cudaMemset(ctx->d_flags, 0, sizeof(unsigned) * 4 * MAX_STREAM_CHUNKS) == cudaSuccess;
   ok = ok && cudaMalloc(&ctx->d_timed_out, sizeof(int)) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_probe, sizeof(int)) == cudaSuccess;
   ok = ok && cudaMallocHost(&ctx->h_timed_out, sizeof(int)) == cudaSuccess;
   ok = ok && cudaMallocHost(&ctx->hp_pin, sizeof(Plan)) == cudaSuccess;
   if (const char* e = getenv("TOPT_B200_STREAM")) ctx->stream_inputs = atoi(e);
@@ -1102,6 +1129,7 @@ void topt_b200_ctx_destroy(topt_b200_ctx* ctx) {
   if (ctx->cstream) cudaStreamSynchronize(ctx->cstream);
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_timed_out);
+  cudaFree(ctx->d_probe);
   if (ctx->h_timed_out) cudaFreeHost(ctx->h_timed_out);
   if (ctx->hp_pin) cudaFreeHost(ctx->hp_pin);
   if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
@@ -1488,10 +1516,9 @@ int topt_b200_pgd_step_dev(topt_b200_ctx* ctx, const topt_step_problem* prob,
   return pgd_step_impl(ctx, hp, prob, settings, opts, meta, out->y, out->slacks, out->g_hat);
 }
 
-int topt_b200_pgd_step(topt_b200_ctx* ctx, const topt_step_problem* prob,
-                       const topt_pgd_settings* settings, const topt_proj_options* opts,
-                       const topt_step_outputs* out, topt_proj_meta* meta) {
-  cudaSetDevice(ctx->device);
+static int pgd_step_host(topt_b200_ctx* ctx, const topt_step_problem* prob,
+                         const topt_pgd_settings* settings, const topt_proj_options* opts,
+                         const topt_step_outputs* out, topt_proj_meta* meta, bool allow_stream) {
   Plan& hp = ctx->h_plan;
   const int64_t n = prob->n;
   const int m = prob->m;
@@ -1502,7 +1529,7 @@ int topt_b200_pgd_step(topt_b200_ctx* ctx, const topt_step_problem* prob,
   // Stream the inputs into the running kernel (copies overlap the BB/PR+ and
   // PREP passes) when the persistent path and the stream memory operations
   // are available; otherwise upload first.
-  const bool streamed = ctx->stream_inputs && !ctx->comm && ctx->persistent &&
+  const bool streamed = allow_stream && ctx->stream_inputs && !ctx->comm && ctx->persistent &&
                         ctx->coop_grid > 0 && n > 0 && m >= 1 && memops().ok &&
                         prob->x && prob->x_prev && prob->g && prob->g_prev && prob->d_prev &&
                         prob->grad;
@@ -1562,6 +1589,51 @@ int topt_b200_pgd_step(topt_b200_ctx* ctx, const topt_step_problem* prob,
   }
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return TOPT_OK;
+}
+
+// Is host-buffer streaming usable on this context?  Probed once: a kernel
+// spins on a flag the copy stream writes after the launch.
+static bool stream_usable(topt_b200_ctx* ctx) {
+  if (ctx->stream_probe >= 0) return ctx->stream_probe == 1;
+  ctx->stream_probe = 0;
+  MemOps& mo = memops();
+  if (!mo.ok) return false;
+  const uint32_t ep = ++ctx->epoch;
+  unsigned* flag = ctx->d_flags + 3 * MAX_STREAM_CHUNKS;
+  if (cudaMemsetAsync(ctx->d_probe, 0, sizeof(int), ctx->stream) != cudaSuccess) return false;
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return false;
+  k_stream_probe<<<1, 32, 0, ctx->stream>>>(flag, ep, ctx->d_probe);
+  ctx->launches++;
+  if (mo.write32((CUstream)ctx->cstream, (CUdeviceptr)flag, ep, 0) != CUDA_SUCCESS) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaGetLastError();
+    return false;
+  }
+  int seen = 0;
+  const bool ok = cudaStreamSynchronize(ctx->cstream) == cudaSuccess &&
+                  cudaMemcpyAsync(&seen, ctx->d_probe, sizeof(int), cudaMemcpyDeviceToHost,
+                                  ctx->stream) == cudaSuccess &&
+                  cudaStreamSynchronize(ctx->stream) == cudaSuccess;
+  cudaGetLastError();
+  ctx->stream_probe = (ok && seen) ? 1 : 0;
+  return ctx->stream_probe == 1;
+}
+
+int topt_b200_pgd_step(topt_b200_ctx* ctx, const topt_step_problem* prob,
+                       const topt_pgd_settings* settings, const topt_proj_options* opts,
+                       const topt_step_outputs* out, topt_proj_meta* meta) {
+  cudaSetDevice(ctx->device);
+  const bool try_stream = ctx->stream_inputs && ctx->persistent && ctx->coop_grid > 0 &&
+                          !ctx->comm && stream_usable(ctx);
+  const int rc = pgd_step_host(ctx, prob, settings, opts, out, meta, try_stream);
+  if (rc == TOPT_ERR_CUDA && try_stream && ctx->stream_timeout) {
+    // the copies did not overlap the running kernel after all (e.g. a
+    // profiler serialized this launch): upload first from now on
+    ctx->stream_timeout = 0;
+    ctx->stream_probe = 0;
+    return pgd_step_host(ctx, prob, settings, opts, out, meta, false);
+  }
+  return rc;
 }
 
 int topt_b200_step_direction(topt_b200_ctx* ctx, int64_t n, const double* x,

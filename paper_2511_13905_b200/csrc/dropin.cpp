@@ -29,6 +29,15 @@ topt_b200_ctx* ctx() {
   return c;
 }
 
+// One process-wide context holds mutable per-call state (plan, staging,
+// streams, last error), so calls through it are serialized: the reference's
+// functions are safe to call concurrently, and so are these.
+std::mutex& ctx_mutex() {
+  static std::mutex mu;
+  return mu;
+}
+std::unique_lock<std::mutex> lock_ctx() { return std::unique_lock<std::mutex>(ctx_mutex()); }
+
 [[noreturn]] void raise(int rc, const char* where) {
   std::string msg = std::string(where) + ": " + topt_b200_last_error(ctx());
   switch (rc) {
@@ -84,6 +93,7 @@ void check_rho(const ConstraintLinearization& lin, std::span<const double> rho) 
 ProjectionResult run_project(int which, std::span<const double> rho,
                              const ConstraintLinearization& lin, double lower, double upper,
                              const ProjectionOptions& o) {
+  const auto lk = lock_ctx();
   check_rho(lin, rho);
   const CsrPartition part = to_csr(lin.partition, lin.num_constraints);
   const topt_linearization v = view(lin, part, true);
@@ -111,6 +121,7 @@ ConstraintLinearization ConstraintLinearization::build(
     std::vector<double> bounds_g, std::vector<double> gd_step,
     std::vector<std::uint8_t> is_equality,
     std::optional<std::vector<std::vector<int>>> partition) {
+  const auto lk = lock_ctx();
   ConstraintLinearization lin;
   lin.num_constraints = m;
   lin.num_vars = n;
@@ -154,6 +165,7 @@ const char* to_string(ProjectionPath path) {
 
 std::vector<double> delta_of_y(std::span<const double> y, const ConstraintLinearization& lin,
                                std::span<const double> rho_tilde, double lower, double upper) {
+  const auto lk = lock_ctx();
   check_rho(lin, rho_tilde);
   if (y.size() != lin.num_constraints)
     throw DomainError("delta_of_y: dual size does not match linearization");
@@ -170,6 +182,7 @@ std::vector<double> constraint_residual_h(std::span<const double> y,
                                           const ConstraintLinearization& lin,
                                           std::span<const double> rho_tilde, double lower,
                                           double upper, double c) {
+  const auto lk = lock_ctx();
   if (!(c > 0.0)) throw ParameterError("constraint_residual_h: c must be > 0");
   check_rho(lin, rho_tilde);
   const CsrPartition none;
@@ -221,6 +234,7 @@ topt_pgd_settings to_c(const PgdSettings& s) {
 }  // namespace
 
 double spectral_step_size(const OptimizerState& st, const PgdSettings& s) {
+  const auto lk = lock_ctx();
   const std::size_t n = st.rho.size();
   std::vector<double> d(n), rt(n);
   double alpha = 0.0, beta = 0.0;
@@ -237,6 +251,7 @@ double spectral_step_size(const OptimizerState& st, const PgdSettings& s) {
 }
 
 std::vector<double> cg_direction(const OptimizerState& st) {
+  const auto lk = lock_ctx();
   if (st.iteration == 0 || st.grad_prev.empty()) return st.grad;   // d_0 = grad f_0
   const std::size_t n = st.rho.size();
   std::vector<double> d(n), rt(n);
@@ -253,6 +268,7 @@ std::vector<double> cg_direction(const OptimizerState& st) {
 
 StepRecord pgd_step(OptimizerState& st, const ConstraintBundle& cons, double lower, double upper,
                     const PgdSettings& s) {
+  const auto lk = lock_ctx();
   const std::size_t n = st.rho.size(), m = cons.m;
   if (cons.grad.size() != m * n || cons.values.size() != m || cons.bounds.size() != m)
     throw DomainError("pgd_step: inconsistent constraint bundle");

@@ -433,11 +433,16 @@ __device__ __forceinline__ unsigned long long global_ns() {
 }
 __device__ __noinline__ void wait_chunk(const unsigned* flag, unsigned epoch, int* timed_out) {
   if (threadIdx.x == 0) {
-    if ((int)(ld_acquire_u32(flag) - epoch) < 0) {
+    // after a first timeout (any CTA) nothing will arrive in time: the launch's
+    // results are discarded and the host re-runs the step upload-first
+    if (*(volatile int*)timed_out == 0 && (int)(ld_acquire_u32(flag) - epoch) < 0) {
       const unsigned long long t0 = global_ns();
       while ((int)(ld_acquire_u32(flag) - epoch) < 0) {
         __nanosleep(256);
-        if (global_ns() - t0 > 4000000000ull) { *timed_out = 1; break; }
+        if (global_ns() - t0 > 4000000000ull || *(volatile int*)timed_out) {
+          *(volatile int*)timed_out = 1;
+          break;
+        }
       }
     }
   }
