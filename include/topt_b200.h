@@ -99,7 +99,7 @@ typedef struct {
   int32_t fallback;
   int32_t local_sweeps;          /* CTA-local sweeps on gathered active elements */
   int32_t gathered;              /* 1 if the active sets were gathered */
-  int32_t reserved;
+  int32_t exact_passes;          /* strict parity: reference-order chain passes run */
   double active;                 /* active elements after the last compacted sweep */
 } topt_proj_meta;
 
@@ -165,6 +165,29 @@ int64_t topt_b200_kernel_launches(const topt_b200_ctx* ctx);
 /* CUDA stream used by the context (cudaStream_t as void*); may be replaced. */
 void* topt_b200_get_stream(const topt_b200_ctx* ctx);
 int topt_b200_set_stream(topt_b200_ctx* ctx, void* stream);
+
+/* Parity mode of the following calls on this context (default CERTIFIED;
+ * environment TOPT_B200_PARITY=strict sets STRICT at context creation).
+ *   CERTIFIED  every decision the reference takes on a floating-point sign
+ *              (bisection midpoints, stage-1 feasibility, Armijo, the
+ *              Newton stop test) is taken on our own tree-summed values; a
+ *              bisection / stage-1 decision is PROVEN to equal the
+ *              reference's unless our |value| lies within the bound on the
+ *              reference's own rounding error (counted in meta.near_ties);
+ *              Newton runs on accurately summed h and Gram (it stops at the
+ *              true tolerance, where the reference's sequentially summed
+ *              ||Phi|| may stall on its own rounding noise).
+ *   STRICT     additionally evaluates every such undecided value, every
+ *              Newton-stage sum, g_hat's dots, the BB / PR+ sums and the
+ *              reported residuals in the reference's own sequential order
+ *              (one chain pass: ~8 GPU cycles per element), so every output
+ *              is bit-identical to the reference built without FMA
+ *              (oracle/_ref).  Single GPU, dense rows, m <= 9.
+ * A context is not thread-safe: serialize calls on one context (the C++
+ * drop-in does); distinct contexts may run concurrently. */
+enum { TOPT_PARITY_CERTIFIED = 0, TOPT_PARITY_STRICT = 1 };
+int topt_b200_set_parity(topt_b200_ctx* ctx, int mode);
+int topt_b200_get_parity(const topt_b200_ctx* ctx);
 
 /* Structured constraint rows (extension beyond the reference interface;
  * SURVEY.md §8(f) rank 1).  Rows the caller can describe instead of storing:

@@ -41,7 +41,7 @@ class ProjMeta(C.Structure):
                 ("near_ties", C.c_int32), ("min_margin", C.c_double),
                 ("bisect_iters", C.c_int32 * MAX_M), ("alpha", C.c_double),
                 ("beta", C.c_double), ("fallback", C.c_int32), ("local_sweeps", C.c_int32),
-                ("gathered", C.c_int32), ("reserved", C.c_int32), ("active", C.c_double)]
+                ("gathered", C.c_int32), ("exact_passes", C.c_int32), ("active", C.c_double)]
 
 
 class Linearization(C.Structure):
@@ -78,7 +78,7 @@ EXPORTS = [
     "topt_b200_set_profiling", "topt_b200_kernel_time", "topt_b200_step_time",
     "topt_b200_debug_trace",
     "topt_b200_nccl_unique_id", "topt_b200_ctx_create_ranks", "topt_b200_pgd_step_ranks",
-    "topt_b200_set_structured_rows",
+    "topt_b200_set_structured_rows", "topt_b200_set_parity", "topt_b200_get_parity",
 ]
 
 _lib = None
@@ -126,6 +126,8 @@ def load():
         "topt_b200_default_options": [vp],
         "topt_b200_set_structured_rows": [vp, i32, vp, vp, i64],
         "topt_b200_default_settings": [vp],
+        "topt_b200_set_parity": [vp, C.c_int],
+        "topt_b200_get_parity": [vp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -218,6 +220,20 @@ class Context:
         rc = self.lib.topt_b200_set_structured_rows(self.h, len(rows), arr, g, int(index_offset))
         if rc != OK:
             raise RuntimeError(self.last_error())
+
+    PARITY = {"certified": 0, "strict": 1}
+
+    def set_parity(self, mode: str):
+        """'certified' (default) or 'strict' (every undecided decision and every
+        Newton-stage sum in the reference's sequential order; include/topt_b200.h)."""
+        rc = self.lib.topt_b200_set_parity(self.h, self.PARITY[mode])
+        if rc != OK:
+            raise RuntimeError(self.last_error())
+
+    @property
+    def parity(self) -> str:
+        v = self.lib.topt_b200_get_parity(self.h)
+        return {0: "certified", 1: "strict"}.get(v, str(v))
 
     def set_profiling(self, on: bool):
         self.lib.topt_b200_set_profiling(self.h, 1 if on else 0)

@@ -108,6 +108,25 @@ class ProjectionResult:
     mask: object = None
     local_sweeps: int = 0
     gathered: bool = False
+    exact_passes: int = 0
+
+
+class parity:
+    """Context manager: run the enclosed calls on `device` in the given parity
+    mode ('strict' or 'certified'; include/topt_b200.h), restoring the old one."""
+
+    def __init__(self, mode: str, device: int = 0):
+        self.mode, self.device = mode, device
+
+    def __enter__(self):
+        self.ctx = L.context(self.device)
+        self.old = self.ctx.parity
+        self.ctx.set_parity(self.mode)
+        return self.ctx
+
+    def __exit__(self, *a):
+        self.ctx.set_parity(self.old)
+        return False
 
 
 def _meta_to_result(meta: L.ProjMeta, delta, y, slacks, m, mask=None) -> ProjectionResult:
@@ -118,7 +137,7 @@ def _meta_to_result(meta: L.ProjMeta, delta, y, slacks, m, mask=None) -> Project
         passes=meta.passes, sweeps=meta.sweeps, stage1_row=meta.stage1_row,
         near_ties=meta.near_ties, min_margin=meta.min_margin,
         bisect_iters=list(meta.bisect_iters[:m]), mask=mask, local_sweeps=meta.local_sweeps,
-        gathered=bool(meta.gathered))
+        gathered=bool(meta.gathered), exact_passes=meta.exact_passes)
 
 
 def _is_torch_cuda(a) -> bool:

@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass(Plan* plan, double* partials,
   c.fixC = c.fixS = nullptr;
   c.list_cap = 0;
   c.timed_out = nullptr;   // never streamed
+  c.ex_smem = nullptr;     // (strict parity runs in the persistent kernel only)
   double* s_rtab = reinterpret_cast<double*>(reinterpret_cast<char*>(s_dyn) + PLAN_SMEM);
   c.rtab = s_rtab;
   build_row_tables(plan->P, s_rtab);
@@ -255,7 +256,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     if (sp.cmd.phase == PH_DONE) break;
     unsigned long long* tr = (trace && pass < 64) ? trace + pass * 8 : nullptr;
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) { tr[0] = gtimer(); tr[5] = sp.cmd.phase; }
-    double* part = partials + (size_t)(pass & 1) * PMAX * nb;
+    // partials alternate between grid-synchronized passes only (a CTA-local
+    // sweep writes none, so it must not flip the buffer a lagging CTA may
+    // still read in the previous combine)
+    double* part = partials + (size_t)(sp.nglobal & 1) * PMAX * nb;
     PassCtx c;
     c.plan = &sp;
     c.cmd = &sp.cmd;
@@ -280,6 +284,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     c.n_items = &s_nitems;
     c.timed_out = gb.timed_out;
     c.rtab = s_rtab;
+    c.ex_smem = reinterpret_cast<char*>(s_dyn) + sp.P.ex_smem;
     if (sp.cmd.phase == PH_SWEEP && sp.cmd.local) {   // CTA-local sweep: no barrier
       local_sweep(c, s_tot);
       if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -305,7 +310,13 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[2] = gtimer();
     if (sp.cmd.phase == PH_PREP && blockIdx.x == 0 && threadIdx.x == 0) signal_out(sp.P);
     if (sp.cmd.phase == PH_GATHER) gather_load(c, nb);
-    finish_reduce(part, nb, sp.cmd.nslots, sp.cmd.phase, s_tot, s_red);
+    if (sp.cmd.phase == PH_EXACT) {   // the chains ran in CTA 0 alone: its values are the sums
+      for (int k = threadIdx.x; k < sp.cmd.nslots; k += BLOCK) s_tot[k] = __ldcg(part + k);
+      __syncthreads();
+    } else {
+      finish_reduce(part, nb, sp.cmd.nslots, sp.cmd.phase, s_tot, s_red);
+    }
+    if (threadIdx.x == 0) sp.nglobal++;   // (read again only after the controller's barrier)
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
       tr[3] = gtimer();
       g_ctl_marks = trace + 512 + pass * 8;
@@ -445,7 +456,7 @@ struct topt_b200_ctx {
   Plan h_plan;
   std::string err;
   int64_t launches = 0;
-  DevBuf bufs[16];
+  DevBuf bufs[20];
   int profile = 0;
   int persistent = 1;       // one cooperative launch per job when possible
   int coop_grid = 0;        // co-resident CTAs for k_step
@@ -480,6 +491,9 @@ struct topt_b200_ctx {
   int* h_timed_out = nullptr;      // pinned
   uint32_t epoch = 0;
   int stream_inputs = 1;           // TOPT_B200_STREAM=0 disables
+  int parity = 0;                  // 0 certified, 1 strict (TOPT_B200_PARITY=strict)
+  const int32_t* last_pidx = nullptr;   // device partition indices of the last owner map
+  int64_t last_poff[MAX_M + 1] = {};
   int stream_probe = -1;
   int stream_timeout = 0;          // the last streamed launch timed out waiting for a chunk           // can a running kernel see copy-stream writes? (-1: unknown)
   int* d_probe = nullptr;
@@ -569,7 +583,7 @@ void* buf(topt_b200_ctx* ctx, int slot, size_t bytes) {
 
 enum BufSlot {
   B_RHO = 0, B_GRAD, B_GD, B_DELTA, B_OWNER, B_OWNER32, B_X, B_XP, B_G, B_GP, B_DP, B_D,
-  B_XNEW, B_PIDX, B_POFF, B_MASK
+  B_XNEW, B_PIDX, B_POFF, B_MASK, B_EXACT
 };
 
 const char* status_msg(int st) {
@@ -694,6 +708,29 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
   // the work area holds the structured rows' tables instead (no active
   // lists in that case)
   dyn_smem = std::max(dyn_smem, PLAN_SMEM + sizeof(double) * (size_t)hp.P.n_tab);
+  if (hp.P.strict) {
+    // strict parity: chain passes (PH_EXACT) run inside the persistent kernel
+    Problem& P = hp.P;
+    if (!persistent || grid < 2)
+      return fail(ctx, TOPT_ERR_UNSUPPORTED, "strict parity needs the persistent (cooperative) kernel");
+    if (P.m > 9)
+      return fail(ctx, TOPT_ERR_UNSUPPORTED, "strict parity supports m <= 9 constraint rows");
+    if (P.structured)
+      return fail(ctx, TOPT_ERR_UNSUPPORTED, "strict parity needs dense constraint rows");
+    if (P.has_part && !P.part_ranges && !P.part_idx)
+      return fail(ctx, TOPT_ERR_UNSUPPORTED,
+                  "strict parity needs the partition's index lists (host-buffer call)");
+    const size_t off = (dyn_smem + 127) & ~size_t(127);
+    const size_t avail = (size_t)ctx->max_dyn_smem > off + 256 ? ctx->max_dyn_smem - off - 256 : 0;
+    const int nst = (int)std::min<size_t>(8, avail / EX_CHUNK_BYTES);
+    if (nst < 2) return fail(ctx, TOPT_ERR_UNSUPPORTED, "strict parity: no shared memory left for the chain ring");
+    P.ex_nst = nst;
+    P.ex_smem = (int32_t)off;
+    dyn_smem = off + (size_t)nst * EX_CHUNK_BYTES + 2 * sizeof(uint64_t) * (size_t)nst;
+    P.ex_seg = std::max<int64_t>(1, std::min<int64_t>(P.n, (int64_t)1 << 21));
+    P.ex_buf = (double*)buf(ctx, B_EXACT, sizeof(double) * 2 * (size_t)P.ex_seg * MAX_EX);
+    if (!P.ex_buf) return fail(ctx, TOPT_ERR_CUDA, "cudaMalloc failed (strict parity staging)");
+  }
   plan_start(hp);
   int phase = hp.cmd.phase;
   if (persistent && phase != PH_DONE) {
@@ -774,6 +811,8 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
 // everywhere, no host arithmetic.  The host only sequences the launches and
 // polls the next phase.
 int run_plan_ranks(topt_b200_ctx* ctx, Plan& hp) {
+  if (hp.P.strict)   // a reference-order sum is sequential across the ranks' slabs
+    return fail(ctx, TOPT_ERR_UNSUPPORTED, "strict parity is single-GPU only");
   const int grid = ctx->grid;
   const int64_t per_thread = (hp.P.n + (int64_t)grid * BLOCK - 1) / ((int64_t)grid * BLOCK);
   hp.P.ours_len = 2.0 * (double)per_thread + (double)grid + 64.0 + (double)ctx->world;
@@ -838,6 +877,7 @@ void fill_meta(const Plan& hp, topt_proj_meta* meta) {
   meta->local_sweeps = r.local_sweeps;
   meta->gathered = r.gathered;
   meta->active = r.active;
+  meta->exact_passes = r.exact_passes;
 }
 
 void default_opts(ProjOptions& o) {
@@ -861,6 +901,7 @@ int init_problem(topt_b200_ctx* ctx, Plan& hp, int64_t n, int m, const topt_proj
     default_opts(P.opt);
   }
   for (int j = 0; j < m; ++j) P.row_count[j] = (double)n;
+  P.strict = ctx->parity;
   return TOPT_OK;
 }
 
@@ -994,6 +1035,13 @@ void apply_ranges(const topt_b200_ctx* ctx, Problem& P) {
   }
 }
 
+// The partition's device index lists (strict parity sums a subset walk over
+// them in the partition's own order, projection.cpp:31-32).
+void set_part_lists(const topt_b200_ctx* ctx, Problem& P) {
+  P.part_idx = ctx->last_pidx;
+  for (int j = 0; j <= P.m && j <= MAX_M; ++j) P.part_off[j] = ctx->last_poff[j];
+}
+
 int owner_map_impl(topt_b200_ctx* ctx, int64_t n, int32_t m, const int64_t* off,
                    const int32_t* idx, int8_t* owner_dev) {
   detect_ranges(ctx, m, off, idx, owner_dev);
@@ -1004,6 +1052,8 @@ int owner_map_impl(topt_b200_ctx* ctx, int64_t n, int32_t m, const int64_t* off,
   void* doff = nullptr;
   int rc = upload(ctx, B_PIDX, idx, sizeof(int32_t) * (size_t)total, &didx);
   if (rc) return rc;
+  ctx->last_pidx = (const int32_t*)didx;
+  for (int j = 0; j <= m && j <= MAX_M; ++j) ctx->last_poff[j] = off[j];
   rc = upload(ctx, B_POFF, off, sizeof(int64_t) * (size_t)(m + 1), &doff);
   if (rc) return rc;
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
@@ -1066,7 +1116,17 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   ok = ok && cudaMalloc(&ctx->d_gr, sizeof(double) * gcap) == cudaSuccess;
   ok = ok && cudaMalloc(&ctx->d_grow, sizeof(int) * gcap) == cudaSuccess;
   ok = ok && cudaMalloc(&ctx->d_gfix, sizeof(double) * 2 * MAX_M * ctx->grid) == cudaSuccess;
-  ctx->max_dyn_smem = 160 * 1024;
+  {   // everything the SM offers a CTA beyond the kernels' static shared memory
+    cudaFuncAttributes fa0, fa1;
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    size_t st = 0;
+    if (cudaFuncGetAttributes(&fa0, k_step<false>) == cudaSuccess) st = fa0.sharedSizeBytes;
+    if (cudaFuncGetAttributes(&fa1, k_step<true>) == cudaSuccess)
+      st = std::max(st, (size_t)fa1.sharedSizeBytes);
+    ctx->max_dyn_smem = (int)std::min<size_t>((size_t)optin - st - 1024, 200 * 1024);
+    cudaGetLastError();
+  }
   ok = ok && cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   ctx->max_dyn_smem) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1100,6 +1160,7 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   ok = ok && cudaMallocHost(&ctx->h_timed_out, sizeof(int)) == cudaSuccess;
   ok = ok && cudaMallocHost(&ctx->hp_pin, sizeof(Plan)) == cudaSuccess;
   if (const char* e = getenv("TOPT_B200_STREAM")) ctx->stream_inputs = atoi(e);
+  if (const char* e = getenv("TOPT_B200_PARITY")) ctx->parity = (std::strcmp(e, "strict") == 0);
   if (!ok) { topt_b200_ctx_destroy(ctx); return TOPT_ERR_CUDA; }
   *out = ctx;
   return TOPT_OK;
@@ -1156,6 +1217,16 @@ int topt_b200_set_structured_rows(topt_b200_ctx* ctx, int32_t m, const topt_row_
   ctx->srows_m = m;
   return TOPT_OK;
 }
+
+int topt_b200_set_parity(topt_b200_ctx* ctx, int mode) {
+  if (!ctx) return TOPT_ERR_INTERNAL;
+  if (mode != TOPT_PARITY_CERTIFIED && mode != TOPT_PARITY_STRICT)
+    return fail(ctx, TOPT_ERR_PARAMETER, "topt_b200_set_parity: unknown mode");
+  ctx->parity = mode;
+  return TOPT_OK;
+}
+
+int topt_b200_get_parity(const topt_b200_ctx* ctx) { return ctx ? ctx->parity : -1; }
 
 int topt_b200_set_stream(topt_b200_ctx* ctx, void* stream) {
   if (!ctx) return TOPT_ERR_INTERNAL;
@@ -1273,6 +1344,7 @@ static int stage_lin(topt_b200_ctx* ctx, Plan& hp, const topt_linearization* lin
     hp.P.owner = own;
     hp.P.has_part = 1;
     apply_ranges(ctx, hp.P);
+    set_part_lists(ctx, hp.P);
   }
   return TOPT_OK;
 }
@@ -1556,6 +1628,7 @@ static int pgd_step_host(topt_b200_ctx* ctx, const topt_step_problem* prob,
     P.owner = own;
     P.has_part = 1;
     apply_ranges(ctx, P);
+    set_part_lists(ctx, P);
   }
   P.rho = (double*)buf(ctx, B_RHO, nb);
   P.d_out = (double*)buf(ctx, B_D, nb);

@@ -181,25 +181,34 @@ TOPT_HD void walk_ingest(Walk& w, const Evals& ev) {
 }
 
 // Replay the reference walk as far as evaluations/certificates allow.
-TOPT_HD void walk_advance(Walk& w, const ProjOptions& o, const Evals& ev) {
-  if (w.status == WK_DONE || w.status == WK_INFEASIBLE || w.status == WK_IDLE) return;
-  const bool hasL = w.hasL, hasH = w.hasH;
-  const double yL = w.yL, yH = w.yH, E = w.E, ghat = w.ghat;
+TOPT_HD void walk_advance(Walk& w, const ProjOptions& o, const Evals& ev, bool strict = false) {
+  if (w.status == WK_DONE || w.status == WK_INFEASIBLE || w.status == WK_IDLE ||
+      w.status == WK_EXACT)
+    return;
+  const bool hasL = w.hasL, hasH = w.hasH, hasL0 = w.hasL0;
+  const double yL = w.yL, yH = w.yH, yL0 = w.yL0, E = w.E, ghat = w.ghat;
   int near = 0, direct = 0, hint = 0;
   double minm = w.min_margin;
   if (!w.feas_done) {
-    // projection.cpp:80-94: r(y_lo) > 0 (down) / r(y_hi) < 0 (up) => infeasible
+    // projection.cpp:80-94: r(y_lo) > 0 (down) / r(y_hi) < 0 (up) => infeasible.
+    // Certificates first (proofs); a direct evaluation otherwise.
     const double yb = w.up ? w.bp_hi : w.bp_lo;
     double R;
     int infeasible;
-    if (evals_lookup(ev, ghat, yb, &R, &hint)) {
-      infeasible = w.up ? (R < 0.0) : (R > 0.0);
-      minm = dmin_(minm, fabs(R) / E);
-      near += (fabs(R) <= E);
-    } else if (hasH && yH <= yb) {
+    if (hasH && yH <= yb) {
       infeasible = w.up ? 0 : 1;
     } else if (hasL && yL >= yb) {
       infeasible = w.up ? 1 : 0;
+    } else if (hasL0 && (w.up ? yL0 == yb : yL0 >= yb)) {
+      infeasible = 0;   // r(yb) <= 0 (down), r(yb) == 0 (up)
+    } else if (evals_lookup(ev, ghat, yb, &R, &hint)) {
+      if (strict && fabs(R) <= E) {   // undecidable from our sum: reference-order value
+        w.status = WK_EXACT; w.ex_state = 1; w.ex_y = yb;
+        return;
+      }
+      infeasible = w.up ? (R < 0.0) : (R > 0.0);
+      minm = dmin_(minm, fabs(R) / E);
+      near += (fabs(R) <= E);
     } else {
       w.status = WK_NEED;
       return;
@@ -219,11 +228,12 @@ TOPT_HD void walk_advance(Walk& w, const ProjOptions& o, const Evals& ev) {
     int d;
     if (hasH && yH <= ym) {
       d = 1;
-    } else if (hasL && yL >= ym) {
+    } else if ((hasL && yL >= ym) || (hasL0 && yL0 >= ym)) {
       d = -1;
     } else {
       double R;
       if (!evals_lookup(ev, ghat, ym, &R, &hint)) { status = WK_NEED; break; }
+      if (strict && fabs(R) <= E) { status = WK_EXACT; w.ex_state = 1; w.ex_y = ym; break; }
       minm = dmin_(minm, fabs(R) / E);
       near += (fabs(R) <= E);
       ++direct;
@@ -374,6 +384,7 @@ TOPT_HDN inline void walk_window(const Walk& w, double* clo, double* chi) {
   double a = w.lo, b = w.hi;
   if (w.feas_done) {   // before that, the infeasibility probe sits at an interval end
     if (w.hasL && w.yL > a) a = w.yL;
+    if (w.hasL0 && w.yL0 > a) a = w.yL0;
     if (w.hasH && w.yH < b) b = w.yH;
   }
   *clo = a; *chi = b;
@@ -486,18 +497,26 @@ TOPT_HD int walk_candidates(const Walk& w, const ProjOptions& o, int K, double* 
   return n;
 }
 
-// Initialise a walk from the PREP totals (projection.cpp:53-97).
+// Initialise a walk from the PREP totals (projection.cpp:53-97).  r0_exact:
+// r0 is the reference-order r(0) (strict parity); otherwise, in strict mode,
+// an r0 within the error bound E of a decision asks for it first.
 TOPT_NOINLINE void walk_init(Walk& w, int eq, double ghat, double E, double r0, double S0,
-                               double bp_lo, double bp_hi, double any, double count) {
+                             double bp_lo, double bp_hi, double any, double count,
+                             bool strict = false, bool r0_exact = false) {
   Walk z = {};
   w = z;
   w.eq = eq; w.ghat = ghat; w.E = E; w.r0 = r0; w.S0 = S0;
-  w.bp_lo = bp_lo; w.bp_hi = bp_hi; w.count = count;
+  w.bp_lo = bp_lo; w.bp_hi = bp_hi; w.count = count; w.any_ = any;
   w.min_margin = 1e300;
+  if (strict && !r0_exact && fabs(r0) <= E) {
+    w.status = WK_EXACT; w.ex_state = 2; w.ex_y = 0.0;
+    return;
+  }
+  const double Ec = r0_exact ? 0.0 : E;   // certificate margin at y = 0
   if (!eq && r0 <= 0.0) {             // inactive: y = 0, residual = max(r0, 0)
     w.status = WK_DONE; w.y = 0.0; w.residual = dmax_(r0, 0.0);
-    if (fabs(r0) <= E) { w.near_ties++; }
-    w.min_margin = fabs(r0) / E;
+    if (!r0_exact && fabs(r0) <= E) { w.near_ties++; }
+    w.min_margin = r0_exact ? 1e300 : fabs(r0) / E;
     return;
   }
   if (eq && r0 == 0.0) { w.status = WK_DONE; w.y = 0.0; w.residual = 0.0; return; }
@@ -505,16 +524,34 @@ TOPT_NOINLINE void walk_init(Walk& w, int eq, double ghat, double E, double r0, 
   if (r0 > 0.0) {
     w.up = 0; w.lo = bp_lo; w.hi = 0.0;
     w.hasB = 1; w.yb = 0.0; w.Rb = r0; w.Sb = S0;
-    if (r0 > E) { w.hasH = 1; w.yH = 0.0; }
+    if (r0 > Ec) { w.hasH = 1; w.yH = 0.0; }
   } else {
     w.up = 1; w.lo = 0.0; w.hi = bp_hi;
     w.hasA = 1; w.ya = 0.0; w.Ra = r0; w.Sa = S0;
-    if (r0 < -E) { w.hasL = 1; w.yL = 0.0; }
+    if (r0 < -Ec) { w.hasL = 1; w.yL = 0.0; }
   }
   w.ym = 0.5 * (w.lo + w.hi);
   w.iters = 0;
   w.status = WK_NEED;
   w.residual = -1.0;   // filled by the FINAL pass (|r(ym)|)
+}
+
+// A reference-order value r(y) (strict parity) as a certificate: r is
+// monotone in y for the reference's own rounding too (every rounded term is
+// monotone, and so is a sequential floating-point sum), so r(y) > 0 decides
+// every midpoint >= y and r(y) <= 0 every midpoint <= y.
+TOPT_HD void walk_exact_value(Walk& w, double y, double r) {
+  if (r > 0.0) {
+    if (!w.hasH || y < w.yH) { w.hasH = 1; w.yH = y; }
+    if (!w.hasB || y < w.yb) { w.hasB = 1; w.yb = y; w.Rb = r; w.Sb = 0.0; }
+  } else {
+    if (r < 0.0) {
+      if (!w.hasL || y > w.yL) { w.hasL = 1; w.yL = y; }
+    } else if (!w.hasL0 || y > w.yL0) {
+      w.hasL0 = 1; w.yL0 = y;
+    }
+    if (!w.hasA || y > w.ya) { w.hasA = 1; w.ya = y; w.Ra = r; w.Sa = 0.0; }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -529,6 +566,29 @@ TOPT_HDN inline void set_error(Plan& pl, int st) {
   pl.stage = SG_DONE;
   pl.cmd.phase = PH_DONE;
   pl.cmd.nslots = 0;
+}
+
+// ---- strict parity: chain passes (PH_EXACT) ------------------------------
+TOPT_HDN inline void ex_begin(Plan& pl, int what, int seq) {
+  Cmd& c = pl.cmd;
+  c.phase = PH_EXACT;
+  c.ex_n = 0;
+  c.ex_seq = seq;
+  c.ex_what = what;
+  c.nslots = 0;
+}
+TOPT_HDN inline void ex_add(Plan& pl, int kind, int j, int k, double y, double start) {
+  Cmd& c = pl.cmd;
+  if (c.ex_n >= MAX_EX) return;
+  ExChain& e = c.ex[c.ex_n++];
+  e.kind = (int8_t)kind; e.j = (int8_t)j; e.k = (int8_t)k; e.pad_ = 0; e.pad2_ = 0;
+  e.y = y; e.start = start;
+  c.nslots = c.ex_n;
+}
+// Element sequence the reference sums a walk of row j over: its partition
+// set on the independent path (projection.cpp:242-248), all of 0..n-1 else.
+TOPT_HD int walk_seq(const Plan& pl, int j) {
+  return (pl.stage == SG_INDEP && pl.P.has_part) ? j : -1;
 }
 
 TOPT_HDN inline void cmd_final(Plan& pl, const double* y, int resid_rows) {
@@ -547,6 +607,15 @@ TOPT_HDN inline void cmd_final(Plan& pl, const double* y, int resid_rows) {
 TOPT_HDN inline void cmd_newton(Plan& pl) {
   Cmd& c = pl.cmd;
   const int m = pl.P.m;
+  if (pl.P.strict) {   // h-dots and the Gram in the reference's order: chains
+    ex_begin(pl, EXW_NEWTON, -1);
+    for (int j = 0; j < MAX_M; ++j) c.y[j] = (j < m) ? pl.nt.ty[j] : 0.0;
+    for (int k = 0; k < m; ++k) ex_add(pl, CH_DOTZ, 0, k, 0.0, 0.0);
+    for (int j = 0; j < m; ++j)
+      for (int k = j; k < m; ++k) ex_add(pl, CH_GRAM, j, k, 0.0, 0.0);
+    pl.stage = SG_NEWTON;
+    return;
+  }
   c.phase = PH_NEWTON;
   c.local = 0;
   for (int j = 0; j < MAX_M; ++j) c.y[j] = (j < m) ? pl.nt.ty[j] : 0.0;
@@ -564,9 +633,52 @@ TOPT_HDN inline void start_newton(Plan& pl) {
   cmd_newton(pl);
 }
 
+// Walks waiting for reference-order values -> one chain pass: the pending
+// point, and (lanes are free) the walk's next midpoints breadth-first, so one
+// pass settles several near-tie levels.  Rows of different element sequences
+// (partition sets) go in separate passes.
+TOPT_NOINLINE bool schedule_exact_walks(Plan& pl) {
+  const int m = pl.P.m;
+  int rows[MAX_M], nr = 0, seq = -2;
+  for (int j = 0; j < m; ++j) {
+    if (pl.w[j].status != WK_EXACT) continue;
+    const int sq = walk_seq(pl, j);
+    if (seq == -2) seq = sq;
+    if (sq == seq) rows[nr++] = j;
+  }
+  if (!nr) return false;
+  ex_begin(pl, EXW_WALK, seq);
+  const int budget = MAX_EX / nr;
+  double* qlo = pl.sc.nlo;
+  double* qhi = pl.sc.nhi;
+  for (int r = 0; r < nr; ++r) {
+    const Walk& w = pl.w[rows[r]];
+    const double start = -w.ghat;
+    if (w.ex_state == 2 || !w.feas_done) {
+      ex_add(pl, CH_RESID, rows[r], 0, w.ex_y, start);
+      continue;
+    }
+    int head = 0, tail = 1, cnt = 0;
+    qlo[0] = w.lo; qhi[0] = w.hi;
+    while (cnt < budget && head < tail) {
+      const double l = qlo[head], h = qhi[head];
+      ++head;
+      const double y = 0.5 * (l + h);
+      ex_add(pl, CH_RESID, rows[r], 0, y, start);
+      ++cnt;
+      if (tail + 2 <= CAND_CAP) {
+        qlo[tail] = l; qhi[tail] = y; ++tail;
+        qlo[tail] = y; qhi[tail] = h; ++tail;
+      }
+    }
+  }
+  return true;
+}
+
 // Build the next sweep over all walks that need evaluations; if none do,
 // advance the stage.  Returns true if a sweep was scheduled.
 TOPT_NOINLINE bool schedule_sweep(Plan& pl) {
+  if (schedule_exact_walks(pl)) return true;
   const int m = pl.P.m;
   int need = 0;
   for (int j = 0; j < m; ++j) need += (pl.w[j].status == WK_NEED);
@@ -756,6 +868,13 @@ TOPT_HDN inline void schedule_feas(Plan& pl) {
 TOPT_NOINLINE void consume_feas(Plan& pl, const double* t) {
   const Problem& P = pl.P;
   const int m = P.m;
+  if (P.strict && pl.cmd.phase == PH_FEAS) {   // every stage-1 dot in the reference's order
+    ex_begin(pl, EXW_FEAS, -1);
+    for (int f = 0; f < pl.cmd.nfeas; ++f)
+      for (int k = 0; k < m; ++k)
+        ex_add(pl, CH_FEAS, pl.cmd.feas_row[f], k, pl.cmd.feas_y[f], 0.0);
+    return;
+  }
   for (int j = 0; j < m; ++j) {
     const int f = pl.feas_map[j];
     if (f < 0) continue;
@@ -829,21 +948,25 @@ TOPT_NOINLINE void consume_prep_core(Plan& pl, const double* t) {
     double ghat, gerr;
     const double cnt = P.row_count[j];
     const double ours = P.ours_len;
+    const bool ex = pl.ghat_ex_ok != 0;     // reference-order dot (strict parity)
+    const double dot = ex ? pl.ghat_dot_ex[j] : s[PS_DOT];
     if (pl.dot_mode) {  // projection.cpp:139-145: (G - g) + dot
-      ghat = P.G_minus_g[j] + s[PS_DOT];
-      gerr = (gamma_k((double)P.n_global + 2.0) + gamma_k(ours)) * s[PS_DABS] +
-             2.0 * kUnit * fabs(ghat);
+      ghat = P.G_minus_g[j] + dot;
+      gerr = ex ? 0.0
+                : (gamma_k((double)P.n_global + 2.0) + gamma_k(ours)) * s[PS_DABS] +
+                      2.0 * kUnit * fabs(ghat);
     } else {
       ghat = P.ghat_in[j];
       gerr = P.ghat_err_in[j];
       if (pl.cmd.validate_part && P.gd_step) {  // validate(): 1e-14 consistency
-        const double expect = P.G_minus_g[j] + s[PS_DOT];
+        const double expect = P.G_minus_g[j] + dot;
         const double scale = dmax_(dmax_(1.0, fabs(expect)), fabs(ghat));
         if (fabs(ghat - expect) > 1e-14 * scale) { set_error(pl, ST_DOMAIN); return; }
       }
     }
     r.ghat[j] = ghat;
-    r.ghat_err[j] = (gamma_k((double)P.n_global + 2.0) + gamma_k(ours)) * s[PS_DABS];
+    r.ghat_err[j] = (ex && pl.dot_mode) ? 0.0
+                    : (gamma_k((double)P.n_global + 2.0) + gamma_k(ours)) * s[PS_DABS];
     if (pl.cmd.validate_part && s[PS_NZOUT] > 0.0) { set_error(pl, ST_DOMAIN); return; }
     // + 16u T: sweeps sum free terms as y * sum(a^2) instead of
     // sum fl(fl(y a) a), and classify regions by breakpoints (passes.cuh).
@@ -852,7 +975,7 @@ TOPT_NOINLINE void consume_prep_core(Plan& pl, const double* t) {
                                16.0 * kUnit * s[PS_T]) + 1e-300;
     const double r0 = s[PS_S0] - ghat;
     walk_init(pl.w[j], P.is_eq[j], ghat, E, r0, s[PS_SLOPE0], s[PS_BPLO], s[PS_BPHI],
-              s[PS_ANY], cnt);
+              s[PS_ANY], cnt, P.strict != 0);
     if (pl.hint_ok[j]) { pl.w[j].hok = 1; pl.w[j].hy = pl.hint_y[j]; pl.w[j].hs = pl.hint_sig[j]; }
   }
   if (P.job == JOB_BUILD || P.job == JOB_DIRECTION) { set_error(pl, ST_OK); return; }
@@ -870,13 +993,28 @@ TOPT_NOINLINE void consume_prep_core(Plan& pl, const double* t) {
     pl.stage = SG_STAGE1;
   }
   const Evals none = {nullptr, nullptr, 0};
-  for (int j = 0; j < m; ++j) walk_advance(pl.w[j], P.opt, none);
+  for (int j = 0; j < m; ++j) walk_advance(pl.w[j], P.opt, none, P.strict != 0);
   pl.cmd.phase = PH_SWEEP;   // marker: the caller schedules the first sweep
   pl.cmd.nslots = -1;
 }
 
+// Strict parity: g_hat's dot (ConstraintLinearization::build / validate,
+// projection.cpp:140-145, :151-155) in the reference's order before any
+// decision uses it; the PREP totals wait in the plan meanwhile.
+TOPT_HD bool prep_needs_exact(const Plan& pl) {
+  return pl.P.strict && !pl.ghat_ex_ok &&
+         (pl.dot_mode || (pl.cmd.validate_part && pl.P.gd_step != nullptr));
+}
+TOPT_NOINLINE void schedule_exact_ghat(Plan& pl, const double* t) {
+  const int m = pl.P.m;
+  for (int k = 0; k < m * PREP_SLOTS; ++k) pl.prep_save[k] = t[k];
+  ex_begin(pl, EXW_GHAT, -1);
+  for (int j = 0; j < m; ++j) ex_add(pl, CH_GHAT, j, 0, 0.0, 0.0);
+}
+
 // (returns with cmd.nslots == -1 when the walks need their first sweep)
 TOPT_NOINLINE void consume_prep(Plan& pl, const double* t) {
+  if (prep_needs_exact(pl)) { schedule_exact_ghat(pl, t); return; }
   consume_prep_core(pl, t);
   if (pl.cmd.phase == PH_SWEEP && pl.cmd.nslots == -1)
     if (!schedule_sweep(pl)) after_walks(pl);
@@ -895,7 +1033,7 @@ TOPT_NOINLINE void consume_sweep(Plan& pl, const double* t) {
     const Evals ev = {c.cand_y + b, t + 2 * b, e - b};
     walk_ingest(w, ev);
     ctl_mark(1);
-    walk_advance(w, pl.P.opt, ev);
+    walk_advance(w, pl.P.opt, ev, pl.P.strict != 0);
     ctl_mark(2);
     pl.w[j] = w;
   }
@@ -928,10 +1066,49 @@ TOPT_NOINLINE void consume_gather(Plan& pl) {
   if (!schedule_sweep(pl)) after_walks(pl);
 }
 
+// Strict parity: |r(y)| of the walked rows in the reference's order
+// (projection.cpp:108), one element sequence per pass.  Returns false when
+// no row is pending.
+TOPT_NOINLINE bool schedule_exact_final(Plan& pl) {
+  const int m = pl.P.m;
+  int seq = -2;
+  for (int j = 0; j < m; ++j) {
+    const Walk& w = pl.w[j];
+    if (!(w.residual < 0.0)) continue;
+    const int sq = walk_seq(pl, j);
+    if (seq == -2) { seq = sq; ex_begin(pl, EXW_FINAL, seq); }
+    if (sq == seq) ex_add(pl, CH_RESID, j, 0, w.y, -w.ghat);
+  }
+  return seq != -2;
+}
+
+TOPT_NOINLINE void finish_final(Plan& pl) {
+  Result& r = pl.res;
+  pl.stage = SG_DONE;
+  pl.cmd.phase = PH_DONE;
+  pl.cmd.nslots = 0;
+  r.status = ST_OK;
+}
+
 TOPT_NOINLINE void consume_final(Plan& pl, const double* t) {
   Problem& P = pl.P;
   Result& r = pl.res;
   const int m = P.m;
+  if (P.strict && pl.cmd.phase == PH_FINAL) {
+    if (P.job == JOB_RESIDUAL_H) {          // the h-dots as chains (cmd.y = the dual)
+      ex_begin(pl, EXW_RESH, -1);
+      for (int k = 0; k < m; ++k) ex_add(pl, CH_DOTZ, 0, k, 0.0, 0.0);
+      return;
+    }
+    if (pl.cmd.resid_rows) {
+      if (schedule_exact_final(pl)) return;
+      double worst = 0.0;
+      for (int j = 0; j < m; ++j) worst = dmax_(worst, pl.w[j].residual);
+      r.residual = worst;
+      finish_final(pl);
+      return;
+    }
+  }
   if (P.job == JOB_RESIDUAL_H) {            // projection.cpp:259-265
     for (int j = 0; j < m; ++j) r.h[j] = t[j] + P.y_in[j] / P.opt.c - P.ghat_in[j];
   } else if (pl.cmd.resid_rows) {           // |r(ym)| per walked row, projection.cpp:108
@@ -953,8 +1130,15 @@ TOPT_NOINLINE void consume_step(Plan& pl, const double* t) {
   const Problem& P = pl.P;
   const PgdSettings& s = P.set;
   Result& r = pl.res;
-  for (int k = 0; k < 6; ++k) r.step_sums[k] = t[k];
   const int fallback = (P.t == 0) || (P.t >= s.t_warmup && P.violation > s.tol_n);
+  if (P.strict && !fallback && pl.cmd.phase == PH_STEP_REDUCE) {
+    // BB / PR+ sums in oracle.c's order (no reference code)
+    for (int k = 0; k < 6; ++k) pl.step_save[k] = t[k];
+    ex_begin(pl, EXW_STEP, -1);
+    for (int k = 0; k < 5; ++k) ex_add(pl, CH_STEP, 0, k, 0.0, 0.0);
+    return;
+  }
+  for (int k = 0; k < 6; ++k) r.step_sums[k] = t[k];
   double alpha, beta = 0.0;
   if (fallback) {                           // SPEC.md:308 / PAPER.md Alg. 3 lines 4-8
     alpha = dmin_(s.alpha_max, s.alpha_fallback / t[5]);
@@ -1015,9 +1199,83 @@ TOPT_HDN inline void plan_start(Plan& pl) {
   pl.dot_mode = (P.job == JOB_BUILD);
 }
 
+// Results of a chain pass (t[c] = chain c's reference-order sum).
+TOPT_NOINLINE void consume_exact(Plan& pl, const double* t) {
+  Problem& P = pl.P;
+  const int m = P.m;
+  Cmd& c = pl.cmd;
+  pl.res.exact_passes++;
+  switch (c.ex_what) {
+    case EXW_STEP: {
+      double tt[6];
+      for (int k = 0; k < 5; ++k) tt[k] = t[k];
+      tt[5] = pl.step_save[5];   // max |g| (exact in any order)
+      consume_step(pl, tt);      // (cmd.phase is PH_EXACT: the sums are consumed)
+      break;
+    }
+    case EXW_GHAT: {
+      for (int j = 0; j < m; ++j) pl.ghat_dot_ex[j] = t[j];
+      pl.ghat_ex_ok = 1;
+      consume_prep(pl, pl.prep_save);
+      break;
+    }
+    case EXW_WALK: {
+      const Evals none = {nullptr, nullptr, 0};
+      int touched[MAX_M];
+      for (int j = 0; j < m; ++j) touched[j] = 0;
+      for (int q = 0; q < c.ex_n; ++q) {
+        const int j = c.ex[q].j;
+        Walk& w = pl.w[j];
+        touched[j] = 1;
+        if (w.ex_state == 2) {   // exact r(0): redo the walk's set-up (projection.cpp:53-97)
+          const int hok = w.hok;
+          const double hy = w.hy, hs = w.hs;
+          walk_init(w, w.eq, w.ghat, w.E, t[q], w.S0, w.bp_lo, w.bp_hi, w.any_, w.count,
+                    true, true);
+          w.hok = hok; w.hy = hy; w.hs = hs;
+        } else {
+          walk_exact_value(w, c.ex[q].y, t[q]);
+        }
+      }
+      for (int j = 0; j < m; ++j) {
+        if (!touched[j]) continue;
+        Walk& w = pl.w[j];
+        if (w.status == WK_EXACT) w.status = WK_NEED;
+        w.ex_state = 0;
+        walk_advance(w, P.opt, none, true);
+      }
+      if (!schedule_sweep(pl)) after_walks(pl);
+      break;
+    }
+    case EXW_FEAS:
+      consume_feas(pl, t);       // (cmd.phase is PH_EXACT: decided on these dots)
+      break;
+    case EXW_NEWTON:
+      consume_newton(pl, t);
+      break;
+    case EXW_FINAL: {
+      for (int q = 0; q < c.ex_n; ++q) pl.w[c.ex[q].j].residual = fabs(t[q]);
+      if (schedule_exact_final(pl)) break;
+      double worst = 0.0;
+      for (int j = 0; j < m; ++j) worst = dmax_(worst, pl.w[j].residual);
+      pl.res.residual = worst;
+      finish_final(pl);
+      break;
+    }
+    case EXW_RESH:
+      for (int j = 0; j < m; ++j) pl.res.h[j] = t[j] + P.y_in[j] / P.opt.c - P.ghat_in[j];
+      finish_final(pl);
+      break;
+    default:
+      set_error(pl, ST_INTERNAL);
+      break;
+  }
+}
+
 TOPT_NOINLINE void plan_consume(Plan& pl, const double* t) {
   pl.res.passes++;
   switch (pl.cmd.phase) {
+    case PH_EXACT: consume_exact(pl, t); break;
     case PH_STEP_REDUCE: consume_step(pl, t); break;
     case PH_PREP: consume_prep(pl, t); break;
     case PH_SWEEP: consume_sweep(pl, t); break;
@@ -1341,6 +1599,12 @@ TOPT_HDN inline void schedule_finish(Plan& pl, int tot) {
 __device__ __noinline__ bool schedule_sweep_warp(Plan& pl, WarpPath& wp) {
   const int lane = threadIdx.x & 31;
   const int m = pl.P.m;
+  {
+    __shared__ int s_ex;
+    if (lane == 0) s_ex = schedule_exact_walks(pl) ? 1 : 0;
+    __syncwarp();
+    if (s_ex) return true;
+  }
   int need = 0;
   for (int j = 0; j < m; ++j) need += (pl.w[j].status == WK_NEED);
   if (!need) return false;
@@ -1397,25 +1661,35 @@ __device__ __noinline__ void consume_sweep_row_warp(Plan& pl, const double* t, i
     if (lane == 0) ctl_mark(0);
     // replay (every lane runs the same loop; a lookup is one ballot)
     if (w.status == WK_NEED) {
-      const bool hasL = w.hasL, hasH = w.hasH;
-      const double yL = w.yL, yH = w.yH;
+      const bool strict = pl.P.strict != 0;
+      const bool hasL = w.hasL, hasH = w.hasH, hasL0 = w.hasL0;
+      const double yL = w.yL, yH = w.yH, yL0 = w.yL0;
       unsigned used = 0u;   // lanes whose value decided a level directly
       bool stop = false;
       if (!w.feas_done) {
         const double yb = w.up ? w.bp_hi : w.bp_lo;
         const unsigned hit = __ballot_sync(0xffffffffu, mine && cy == yb);
         int infeasible = -1;
-        if (hit) {
-          // projection.cpp:80-94: R < 0 (up) / R > 0 (down) => infeasible
-          const double R = __shfl_sync(0xffffffffu, cR, __ffs(hit) - 1);
-          infeasible = w.up ? (R < 0.0) : (R > 0.0);
-          used |= hit;
-        } else if (hasH && yH <= yb) {
+        // certificates first (proofs), then a direct evaluation
+        if (hasH && yH <= yb) {
           infeasible = w.up ? 0 : 1;
         } else if (hasL && yL >= yb) {
           infeasible = w.up ? 1 : 0;
+        } else if (hasL0 && (w.up ? yL0 == yb : yL0 >= yb)) {
+          infeasible = 0;
+        } else if (hit) {
+          // projection.cpp:80-94: R < 0 (up) / R > 0 (down) => infeasible
+          const double R = __shfl_sync(0xffffffffu, cR, __ffs(hit) - 1);
+          if (strict && fabs(R) <= E) {
+            w.status = WK_EXACT; w.ex_state = 1; w.ex_y = yb;
+            stop = true;
+          } else {
+            infeasible = w.up ? (R < 0.0) : (R > 0.0);
+            used |= hit;
+          }
         }
-        if (infeasible < 0) { stop = true; }
+        if (stop) {}
+        else if (infeasible < 0) { stop = true; }
         else if (infeasible) { w.status = WK_INFEASIBLE; stop = true; }
         else w.feas_done = 1;
       }
@@ -1428,10 +1702,15 @@ __device__ __noinline__ void consume_sweep_row_warp(Plan& pl, const double* t, i
         int status = WK_DONE;
 #pragma unroll 1
         while ((hi - lo) > tol_b && it < maxit) {
-          const bool cH = hasH && yH <= ym, cL = hasL && yL >= ym;
+          const bool cH = hasH && yH <= ym;
+          const bool cL = (hasL && yL >= ym) || (hasL0 && yL0 >= ym);
           const unsigned hit = __ballot_sync(0xffffffffu, mine && cy == ym);
           const bool unc = !cH && !cL;
           if (unc && !hit) { status = WK_NEED; break; }
+          if (unc && strict && (hit & mNear) != 0u) {   // within the bound: reference order
+            status = WK_EXACT; w.ex_state = 1; w.ex_y = ym;
+            break;
+          }
           used |= unc ? hit : 0u;
           direct += unc ? 1 : 0;
           const bool up = cH || (unc && (hit & mB) != 0u);   // evaluated: R > 0.0
@@ -1513,7 +1792,9 @@ __device__ void plan_consume_warp(Plan& pl, const double* t) {
     if (lane == 0) {
       pl.res.passes++;
       ctl_mark(0);
-      if (ph == PH_PREP) {
+      if (ph == PH_PREP && prep_needs_exact(pl)) {
+        schedule_exact_ghat(pl, t);
+      } else if (ph == PH_PREP) {
         consume_prep_core(pl, t);
         ctl_mark(1);
       } else {
@@ -1533,10 +1814,12 @@ __device__ void plan_consume_warp(Plan& pl, const double* t) {
     __syncwarp();
     return;
   }
-  if (ph == PH_NEWTON) {   // the m x m solve on the whole warp
+  if (ph == PH_NEWTON || (ph == PH_EXACT && pl.cmd.ex_what == EXW_NEWTON)) {
+    // the m x m solve on the whole warp
     __shared__ int s_pend;
     if (lane == 0) {
       pl.res.passes++;
+      if (ph == PH_EXACT) pl.res.exact_passes++;
       s_pend = consume_newton_core(pl, t);
     }
     __syncwarp();
@@ -1600,11 +1883,14 @@ __device__ __noinline__ void plan_consume_cta(Plan& pl, const double* t) {
     if (threadIdx.x == 0) {
       pl.res.passes++;
       ctl_mark(0);
-      consume_prep_core(pl, t);
+      if (prep_needs_exact(pl)) schedule_exact_ghat(pl, t);
+      else consume_prep_core(pl, t);
       ctl_mark(1);
       s_sched = (pl.cmd.phase == PH_SWEEP && pl.cmd.nslots == -1) ? 1 : 0;
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_sched && schedule_exact_walks(pl)) s_sched = 0;
   __syncthreads();
   if (s_sched) {
     int need = 0;

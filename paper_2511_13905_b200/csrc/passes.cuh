@@ -16,10 +16,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cooperative_groups.h>
+
 #include "controller.h"
 #include "topt_core.h"
 
 namespace topt_b200 {
+namespace cg = cooperative_groups;
 
 constexpr int BLOCK = 512;
 constexpr int NWARP = BLOCK / 32;
@@ -138,6 +141,7 @@ struct PassCtx {
   int* n_items;        // shared scalar
   int* timed_out;      // global flag: a streamed input chunk never arrived
   const double* rtab;  // shared centroid tables of structured rows (P.n_tab entries)
+  void* ex_smem;       // chain ring + mbarriers in dynamic shared memory (strict parity)
 };
 
 // ---- Structured constraint rows ------------------------------------------------
@@ -2185,6 +2189,223 @@ __device__ void pass_newton(const PassCtx& c) {
   else pass_newton_m<16>(c);
 }
 
+// ---- PH_EXACT: reference-order sequential sums (strict parity) -------------
+//
+// A reference sum s = fl(...fl(fl(start + t_0) + t_1)... + t_{L-1}) cannot be
+// reassociated, so it runs as a CHAIN: one lane per sum, one dependent fp64
+// add per element (~8 cycles, the DADD latency).  The pass interleaves two
+// roles per segment of SEG elements of the element sequence:
+//   * fill (CTAs 1..nb-1, grid-stride, full bandwidth): every element's terms
+//     of every chain, with the reference's expressions, into T[p][NCp]
+//     (double-buffered in global memory);
+//   * consume (CTA 0): one thread streams the previous segment's T through a
+//     shared-memory ring with 1-D TMA bulk copies (cp.async.bulk + mbarrier
+//     complete_tx); consumer warps add one staged term per lane per element.
+// Every term is a separately rounded IEEE product (__dmul_rn / __dadd_rn),
+// so the chain reproduces the reference binary's sum bit for bit.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
+}
+
+constexpr int EX_CHUNK_BYTES = 16384;
+
+// Element index of position q of the pass's sequence.
+__device__ __forceinline__ int64_t ex_elem(const Problem& P, int seq, int64_t q) {
+  if (seq < 0) return q;
+  if (P.part_ranges) return P.row_lo[seq] + q;
+  return (int64_t)P.part_idx[P.part_off[seq] + q];
+}
+__device__ __forceinline__ int64_t ex_len(const Problem& P, int seq) {
+  if (seq < 0) return P.n;
+  if (P.part_ranges) return P.row_hi[seq] - P.row_lo[seq];
+  return P.part_off[seq + 1] - P.part_off[seq];
+}
+
+// Terms of every chain at element i (the reference's expressions).
+__device__ __forceinline__ void ex_terms(const Problem& P, const Cmd& cmd, int64_t i,
+                                         double* __restrict__ out) {
+  const int m = P.m;
+  const double* __restrict__ A = P.grad;
+  const int64_t ld = P.ld;
+  double lo = 0.0, hi = 0.0, delta = 0.0;
+  bool freev = false;
+  const bool need_rho = cmd.ex_what != EXW_STEP && cmd.ex_what != EXW_GHAT;
+  if (need_rho) {
+    const double r = P.rho[i];
+    lo = __dsub_rn(P.lower, r);            // projection.cpp:32, :207
+    hi = __dsub_rn(P.upper, r);
+  }
+  if (cmd.ex_what == EXW_NEWTON || cmd.ex_what == EXW_RESH) {
+    double z = 0.0;                        // projection.cpp:199-205: ascending j from 0.0
+    for (int j = 0; j < m; ++j) {
+      const double yj = cmd.y[j];
+      if (yj == 0.0) continue;
+      z = __dadd_rn(z, __dmul_rn(yj, A[(int64_t)j * ld + i]));
+    }
+    delta = clipd(z, lo, hi);
+    freev = !(z < lo || z > hi);           // projection.cpp:369
+  }
+  double sx = 0.0, sy = 0.0, gg = 0.0, gp = 0.0, gd = 0.0;
+  if (cmd.ex_what == EXW_STEP) {
+    const double x = P.x[i], xp = P.x_prev[i];
+    gg = P.g[i];
+    gp = P.g_prev[i];
+    sx = __dsub_rn(x, xp);
+    sy = __dsub_rn(gg, gp);
+  } else if (cmd.ex_what == EXW_GHAT) {
+    gd = P.gd_step ? P.gd_step[i] : __dmul_rn(cmd.wa, P.d_out[i]);   // oracle.c: wa * d
+  }
+  for (int q = 0; q < cmd.ex_n; ++q) {
+    const ExChain& e = cmd.ex[q];
+    double t;
+    switch (e.kind) {
+      case CH_RESID: {
+        const double a = A[(int64_t)e.j * ld + i];
+        t = __dmul_rn(a, clipd(__dmul_rn(e.y, a), lo, hi));
+        break;
+      }
+      case CH_DOTZ:
+        t = __dmul_rn(A[(int64_t)e.k * ld + i], delta);
+        break;
+      case CH_GRAM:
+        t = freev ? __dmul_rn(A[(int64_t)e.j * ld + i], A[(int64_t)e.k * ld + i]) : 0.0;
+        break;
+      case CH_FEAS: {
+        const double z = e.j < 0 ? 0.0 : __dadd_rn(0.0, __dmul_rn(e.y, A[(int64_t)e.j * ld + i]));
+        t = __dmul_rn(A[(int64_t)e.k * ld + i], clipd(z, lo, hi));
+        break;
+      }
+      case CH_GHAT:
+        t = __dmul_rn(gd, A[(int64_t)e.j * ld + i]);
+        break;
+      default: {   // CH_STEP, oracle.c orc_spectral_step_size / orc_pr_beta
+        const int k = e.k;
+        t = k == 0 ? __dmul_rn(sx, sx)
+          : k == 1 ? __dmul_rn(sx, sy)
+          : k == 2 ? __dmul_rn(sy, sy)
+          : k == 3 ? __dmul_rn(gg, sy)
+                   : __dmul_rn(gp, gp);
+        break;
+      }
+    }
+    out[q] = t;
+  }
+}
+
+__device__ __noinline__ void pass_exact(const PassCtx& c) {
+  const Problem& P = c.plan->P;
+  const Cmd& cmd = *c.cmd;
+  cg::grid_group grid = cg::this_grid();
+  const int nc = cmd.ex_n;
+  const int NCp = (nc + 1) & ~1;                 // 16-byte rows
+  const int seq = cmd.ex_seq;
+  const int64_t L = ex_len(P, seq);
+  const int64_t SEG = P.ex_seg;
+  const int S = (int)((L + SEG - 1) / SEG);
+  const int nb = gridDim.x;
+  // consumer side (CTA 0): ring in dynamic shared memory
+  const int NST = P.ex_nst;
+  char* ring = reinterpret_cast<char*>(c.ex_smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)NST * EX_CHUNK_BYTES);
+  uint64_t* empty = full + NST;
+  const int ncw = (nc + 31) / 32;                // consumer warps
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int CE = EX_CHUNK_BYTES / (NCp * 8);     // elements per chunk
+  double acc = 0.0;
+  const int my = warp * 32 + lane;
+  if (blockIdx.x == 0) {
+    if (warp < ncw && my < nc) acc = cmd.ex[my].start;
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < NST; ++k) { mbar_init(full + k, 1); mbar_init(empty + k, ncw); }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  int stage = 0;
+  unsigned phase = 0;
+  for (int s = 0; s <= S; ++s) {
+    if (blockIdx.x != 0 && s < S) {              // fill segment s
+      double* T = P.ex_buf + (size_t)(s & 1) * (size_t)SEG * NCp;
+      const int64_t q0 = (int64_t)s * SEG;
+      const int64_t len = (L - q0 < SEG) ? L - q0 : SEG;
+      for (int64_t p = (int64_t)(blockIdx.x - 1) * BLOCK + threadIdx.x; p < len;
+           p += (int64_t)(nb - 1) * BLOCK)
+        ex_terms(P, cmd, ex_elem(P, seq, q0 + p), T + (size_t)p * NCp);
+      asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> TMA reads
+    }
+    if (blockIdx.x == 0 && s > 0) {              // consume segment s - 1
+      const double* T = P.ex_buf + (size_t)((s - 1) & 1) * (size_t)SEG * NCp;
+      const int64_t q0 = (int64_t)(s - 1) * SEG;
+      const int64_t len = (L - q0 < SEG) ? L - q0 : SEG;
+      const int64_t nch = (len + CE - 1) / CE;
+      if (warp == ncw) {                         // TMA producer (one lane)
+        if (lane == 0) {
+          int st = stage;
+          unsigned ph = phase;
+          for (int64_t k = 0; k < nch; ++k) {
+            mbar_wait(empty + st, ph ^ 1u);
+            const int64_t e0 = k * CE;
+            const int ne = (int)((len - e0 < CE) ? len - e0 : CE);
+            const unsigned bytes = (unsigned)(ne * NCp * 8);
+            mbar_expect_tx(full + st, bytes);
+            bulk_g2s(ring + (size_t)st * EX_CHUNK_BYTES, T + (size_t)e0 * NCp, bytes, full + st);
+            if (++st == NST) { st = 0; ph ^= 1u; }
+          }
+        }
+      } else if (warp < ncw) {                   // consumers: lane = chain
+        int st = stage;
+        unsigned ph = phase;
+        for (int64_t k = 0; k < nch; ++k) {
+          mbar_wait(full + st, ph);
+          const int64_t e0 = k * CE;
+          const int ne = (int)((len - e0 < CE) ? len - e0 : CE);
+          const double* buf = reinterpret_cast<const double*>(ring + (size_t)st * EX_CHUNK_BYTES) +
+                              (my < NCp ? my : 0);
+          int e = 0;
+          for (; e + 8 <= ne; e += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = buf[(size_t)(e + u) * NCp];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
+          }
+          for (; e < ne; ++e) acc = __dadd_rn(acc, buf[(size_t)e * NCp]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + st);
+          if (++st == NST) { st = 0; ph ^= 1u; }
+        }
+      }
+      // every role advanced the ring by nch chunks
+      const int64_t adv = stage + nch;
+      phase ^= (unsigned)((adv / NST) & 1);
+      stage = (int)(adv % NST);
+    }
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && warp < ncw && my < nc) c.out[my] = acc;
+}
+
 __device__ void run_pass(const PassCtx& c) {
   switch (c.cmd->phase) {
     case PH_STEP_REDUCE: pass_step_reduce(c); break;
@@ -2194,6 +2415,7 @@ __device__ void run_pass(const PassCtx& c) {
     case PH_NEWTON: pass_newton(c); break;
     case PH_FINAL: pass_final(c); break;
     case PH_GATHER: pass_gather(c); break;
+    case PH_EXACT: pass_exact(c); break;
     default: break;
   }
 }

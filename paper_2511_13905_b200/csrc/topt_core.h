@@ -46,7 +46,31 @@ enum Phase : int32_t {
   PH_NEWTON = 4,       // K5: delta(y), h-dots and A D A^T at one trial dual
   PH_FINAL = 5,        // K7: delta / x_new writes + residual dots
   PH_DONE = 6,
-  PH_GATHER = 7        // copy the (small) active sets to every CTA; later sweeps run CTA-locally
+  PH_GATHER = 7,       // copy the (small) active sets to every CTA; later sweeps run CTA-locally
+  PH_EXACT = 8         // strict parity: sums in the reference's sequential order (chains)
+};
+
+// Strict-parity "chains": one reference-order sequential sum each
+// (s = start; for i in the reference's element order: s = fl(s + term_i)).
+// A chain pass evaluates up to MAX_EX of them over one element sequence.
+constexpr int MAX_EX = 96;
+enum ChainKind : int8_t {
+  CH_RESID = 0,   // start -g_hat_j; term a_j clip(y a_j, lo, hi)         projection.cpp:30-36
+  CH_DOTZ = 1,    // term a_k delta_i, delta = clip(z(cmd.y), lo, hi)     projection.cpp:287-288
+  CH_GRAM = 2,    // term a_j a_k over free i of z(cmd.y)                 projection.cpp:368-376
+  CH_FEAS = 3,    // term a_k clip(0 + y a_j, lo, hi) (row j < 0: y = 0)  projection.cpp:320-328
+  CH_GHAT = 4,    // term gd_i a_j                                        projection.cpp:140-145
+  CH_STEP = 5     // BB / PR+ sums of oracle.c (k = 0..4)
+};
+// What a chain pass's results feed.
+enum ExWhat : int32_t {
+  EXW_NONE = 0, EXW_STEP, EXW_GHAT, EXW_WALK, EXW_FEAS, EXW_NEWTON, EXW_FINAL, EXW_RESH
+};
+struct ExChain {
+  int8_t kind, j, k, pad_;
+  int32_t pad2_;
+  double y;       // CH_RESID / CH_FEAS dual
+  double start;   // initial value of the sum
 };
 constexpr int GATHER_CAP = 1024;   // max gathered active elements (all rows; = the trigger)
 constexpr int GATHER_BLK = 128;    // per-CTA items a compacted sweep publishes (fused gather)
@@ -77,7 +101,10 @@ enum Job : int32_t {
 enum Stage : int32_t {
   SG_INIT = 0, SG_SINGLE, SG_INDEP, SG_STAGE1, SG_FEAS, SG_NEWTON, SG_FINAL, SG_DONE
 };
-enum WalkStatus : int32_t { WK_IDLE = 0, WK_NEED = 1, WK_DONE = 2, WK_INFEASIBLE = 3 };
+enum WalkStatus : int32_t {
+  WK_IDLE = 0, WK_NEED = 1, WK_DONE = 2, WK_INFEASIBLE = 3,
+  WK_EXACT = 4   // strict parity: a decision needs the reference-order value at ex_y
+};
 
 struct ProjOptions {
   double c, tol_b, tol_n;
@@ -100,6 +127,10 @@ struct Walk {
   double ya, Ra, Sa, yb, Rb, Sb;    // nearest evaluated points with R<=0 / R>0
   double hy, hs;                    // root estimate from the PREP sketch (if hok)
   int32_t hok, pad2_;
+  // strict parity: reference-order evaluations are certificates with E = 0;
+  // r(yL0) == 0 exactly (so r <= 0 below it, not r < 0)
+  int32_t hasL0, ex_state;          // ex_state: 1 exact r(ex_y) pending, 2 exact r(0) pending
+  double yL0, ex_y, any_;
 };
 
 struct Newton {
@@ -137,6 +168,12 @@ struct Cmd {
   int32_t load_fused;            // the items were published by the last global sweep:
   int32_t pad_cmd_;              // every CTA loads them before the first local sweep
   double wlo[MAX_M], whi[MAX_M];
+  // PH_EXACT (strict parity)
+  int32_t ex_n;                  // chains
+  int32_t ex_seq;                // -1: elements 0..n-1; j: row j's partition sequence
+  int32_t ex_what;               // ExWhat
+  int32_t ex_row;                // EXW_FINAL: first row of this batch
+  ExChain ex[MAX_EX];
 };
 
 // Problem description (device pointers are filled by the host).
@@ -207,7 +244,16 @@ struct Problem {
   int32_t axis_tab[3];          // the one table of each axis (-1: none / several)
   int32_t axis_fast;            // every centroid row uses its axis' one table,
   int32_t const_tab;            // ... and the constant rows share one value (entry)
-  int32_t pad2_;
+  // strict parity (PH_EXACT): reference-order sums for every decision the
+  // certificates cannot settle and for every Newton-stage sum
+  int32_t strict;
+  int32_t ex_nst;               // ring stages of the chain consumer (16 KB each)
+  int32_t ex_smem;              // byte offset of the chain ring in dynamic shared memory
+  int32_t pad3_;
+  double* ex_buf;               // 2 x ex_seg x MAX_EX doubles (term staging)
+  int64_t ex_seg;               // elements per staged segment
+  const int32_t* part_idx;      // device partition indices (CSR; for subset chains)
+  int64_t part_off[MAX_M + 1];  // host-copied CSR offsets
 };
 enum RowKind { RK_DENSE = 0, RK_CONST = 1, RK_CENTROID = 2 };
 constexpr int MAX_TAB = 8192;   // centroid table entries (shared memory, 64 KB)
@@ -217,7 +263,8 @@ struct Result {
   int32_t status, path, newton_iters, converged, curvature_violations;
   int32_t passes, sweeps, stage1_row, near_ties, fallback;
   int32_t local_sweeps, gathered;
-  int32_t final_phase, pad_r_;  // cmd.phase when the persistent kernel returned
+  int32_t final_phase, exact_passes;  // cmd.phase when the persistent kernel returned;
+                                      // chain passes (strict parity)
   double active;            // active elements after the last compacted sweep
   int32_t bisect_iters[MAX_M];
   double residual, alpha, beta, min_margin;
@@ -244,6 +291,12 @@ struct Plan {
   // root sketch from the PREP pass (candidate choice only, never a decision)
   double hint_y[MAX_M], hint_sig[MAX_M];
   int32_t hint_ok[MAX_M];
+  // strict parity
+  int32_t ghat_ex_ok;                 // g_hat dots below are reference-order exact
+  int32_t nglobal;                    // grid-synchronized passes so far (partials buffer parity)
+  double ghat_dot_ex[MAX_M];
+  double prep_save[MAX_M * 9];        // PREP totals held across the g_hat chain pass
+  double step_save[6];
   Scratch sc;
 };
 
