@@ -313,6 +313,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     if (sp.cmd.phase == PH_EXACT) {   // the chains ran in CTA 0 alone: its values are the sums
       for (int k = threadIdx.x; k < sp.cmd.nslots; k += BLOCK) s_tot[k] = __ldcg(part + k);
       __syncthreads();
+      if (sp.P.ex_debug && blockIdx.x == 0 && threadIdx.x == 0)
+        printf("[exact] what=%d n=%d seq=%d len=%lld seg=%lld nst=%d wa=%.17g t0=%.17g t1=%.17g\n",
+               sp.cmd.ex_what, sp.cmd.ex_n, sp.cmd.ex_seq, (long long)sp.P.n,
+               (long long)sp.P.ex_seg, sp.P.ex_nst, sp.cmd.wa, s_tot[0],
+               sp.cmd.ex_n > 1 ? s_tot[1] : 0.0);
     } else {
       finish_reduce(part, nb, sp.cmd.nslots, sp.cmd.phase, s_tot, s_red);
     }
@@ -492,6 +497,7 @@ struct topt_b200_ctx {
   uint32_t epoch = 0;
   int stream_inputs = 1;           // TOPT_B200_STREAM=0 disables
   int parity = 0;                  // 0 certified, 1 strict (TOPT_B200_PARITY=strict)
+  int ex_debug = 0;
   const int32_t* last_pidx = nullptr;   // device partition indices of the last owner map
   int64_t last_poff[MAX_M + 1] = {};
   int stream_probe = -1;
@@ -902,6 +908,7 @@ int init_problem(topt_b200_ctx* ctx, Plan& hp, int64_t n, int m, const topt_proj
   }
   for (int j = 0; j < m; ++j) P.row_count[j] = (double)n;
   P.strict = ctx->parity;
+  P.ex_debug = ctx->ex_debug;
   return TOPT_OK;
 }
 
@@ -1161,6 +1168,7 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   ok = ok && cudaMallocHost(&ctx->hp_pin, sizeof(Plan)) == cudaSuccess;
   if (const char* e = getenv("TOPT_B200_STREAM")) ctx->stream_inputs = atoi(e);
   if (const char* e = getenv("TOPT_B200_PARITY")) ctx->parity = (std::strcmp(e, "strict") == 0);
+  if (const char* e = getenv("TOPT_B200_EXDEBUG")) ctx->ex_debug = atoi(e);
   if (!ok) { topt_b200_ctx_destroy(ctx); return TOPT_ERR_CUDA; }
   *out = ctx;
   return TOPT_OK;

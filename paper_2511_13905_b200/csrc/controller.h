@@ -78,8 +78,15 @@ enum PrepSlot {
   PS_BPLO = 6,     // min breakpoint (min-reduced)
   PS_BPHI = 7,     // max breakpoint (max-reduced)
   PS_ANY = 8,      // count of |a_i| >= 1e-300
-  PREP_SLOTS = 9
+  // row-structure detection (single rank, dense rows; 1.0 = not examined):
+  PS_NCONST = 9,   // count of a_i != a_0            (a constant row: volume)
+  PS_AREF = 10,    // a_0 (one contributor)
+  PS_NNEG = 11,    // count of a_i != -a_{j-1,i}      (the +- rows of a two-sided constraint)
+  PREP_SLOTS = 12
 };
+
+static_assert(sizeof(((Plan*)0)->prep_save) == sizeof(double) * MAX_M * PREP_SLOTS,
+              "prep_save holds one PREP pass");
 
 // Reduction operator of a slot: 0 sum, 1 min, 2 max.
 TOPT_HD int slot_op(int phase, int slot) {
@@ -977,6 +984,27 @@ TOPT_NOINLINE void consume_prep_core(Plan& pl, const double* t) {
     walk_init(pl.w[j], P.is_eq[j], ghat, E, r0, s[PS_SLOPE0], s[PS_BPLO], s[PS_BPHI],
               s[PS_ANY], cnt, P.strict != 0);
     if (pl.hint_ok[j]) { pl.w[j].hok = 1; pl.w[j].hy = pl.hint_y[j]; pl.w[j].hs = pl.hint_sig[j]; }
+  }
+  // Row structure seen by PREP (every row was read once): constant rows and
+  // rows that are the exact negation of their predecessor.  The later passes
+  // then read each distinct row once and derive the others bit for bit
+  // (negation and a constant are exact), so results do not change.
+  P.n_alias = 0;
+  P.pat7 = 0;
+  for (int j = 0; j < MAX_M; ++j) { P.alias_kind[j] = AK_DENSE; P.alias_c[j] = 0.0; }
+  if (!P.structured && !P.owner && P.n_global == P.n && m >= 2 && m <= 8) {
+    for (int j = 0; j < m; ++j) {
+      const double* sj = t + j * PREP_SLOTS;
+      if (sj[PS_NCONST] == 0.0) {
+        P.alias_kind[j] = AK_CONST; P.alias_c[j] = sj[PS_AREF]; P.n_alias++;
+      } else if (j >= 1 && sj[PS_NNEG] == 0.0 && P.alias_kind[j - 1] == AK_DENSE) {
+        P.alias_kind[j] = AK_NEG; P.n_alias++;
+      }
+    }
+    P.pat7 = (m == 7 && P.alias_kind[0] == AK_CONST && P.alias_kind[1] == AK_DENSE &&
+              P.alias_kind[2] == AK_NEG && P.alias_kind[3] == AK_DENSE &&
+              P.alias_kind[4] == AK_NEG && P.alias_kind[5] == AK_DENSE &&
+              P.alias_kind[6] == AK_NEG) ? 1 : 0;
   }
   if (P.job == JOB_BUILD || P.job == JOB_DIRECTION) { set_error(pl, ST_OK); return; }
   if (m < 1) { set_error(pl, ST_DOMAIN); return; }

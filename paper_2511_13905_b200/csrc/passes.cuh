@@ -102,7 +102,9 @@ template <int NS>
 __device__ __forceinline__ void block_reduce_store(const double (&v)[NS], int ns, int phase,
                                                    int slot0, double* out, double* smem) {
   const int warp = threadIdx.x >> 5;
-  if (phase == PH_PREP) warp_reduce_slots<NS, true>(v, phase, slot0, smem + warp * NS);
+  // phases with min / max slots (PREP breakpoints, STEP_REDUCE's max |g|)
+  if (phase == PH_PREP || phase == PH_STEP_REDUCE)
+    warp_reduce_slots<NS, true>(v, phase, slot0, smem + warp * NS);
   else warp_reduce_slots<NS, false>(v, phase, slot0, smem + warp * NS);
   __syncthreads();
   if (threadIdx.x < ns) {
@@ -640,13 +642,20 @@ __device__ __forceinline__ void prep_group(const PassCtx& c, int j0, int64_t n, 
   for (int r = 0; r < G; ++r)
     A2[r] = reinterpret_cast<const double2*>(P.grad + (int64_t)(j0 + r) * P.ld);
   PrepAcc A[G];
-  double fmin[G], fmax[G];
+  double fmin[G], fmax[G], aref[G];
+  // row-structure detection (single rank): a constant row, and row r the
+  // exact negation of row r - 1 within the group
+  const bool detect = P.n_global == P.n;
 #pragma unroll
   for (int r = 0; r < G; ++r) {
 #pragma unroll
     for (int s = 0; s < PREP_SLOTS; ++s) A[r].v[s] = 0.0;   // bp_lo = bp_hi = 0 (:58)
     fmin[r] = 0.0;
     fmax[r] = 0.0;
+    aref[r] = (detect && n > 0) ? P.grad[(int64_t)(j0 + r) * P.ld] : 0.0;
+    if (!detect) A[r].v[PS_NCONST] = 1.0;
+    if (!detect || r == 0) A[r].v[PS_NNEG] = 1.0;
+    if (detect && c.i0 == 0) A[r].v[PS_AREF] = aref[r];
   }
   constexpr int UP = 2;   // pairs in flight per thread
   for (int64_t qb = c.i0 - lane; qb < n2; qb += UP * st) {   // warp-uniform trip count
@@ -683,6 +692,12 @@ __device__ __forceinline__ void prep_group(const PassCtx& c, int j0, int64_t n, 
         for (int r = 0; r < G; ++r) {
           prep_elem_w(A[r], a2[u][r].x, r2[u].x, g0, dot, L, U_, fmin[r], fmax[r]);
           prep_elem_w(A[r], a2[u][r].y, r2[u].y, g1, dot, L, U_, fmin[r], fmax[r]);
+          if (detect) {
+            A[r].v[PS_NCONST] += (double)((a2[u][r].x != aref[r]) + (a2[u][r].y != aref[r]));
+            if (r > 0)
+              A[r].v[PS_NNEG] += (double)((a2[u][r].x != -a2[u][r - 1].x) +
+                                          (a2[u][r].y != -a2[u][r - 1].y));
+          }
         }
       }
     }
@@ -700,15 +715,13 @@ constexpr int PREP_GROUP = 2;
 __device__ __noinline__ void prep_dense_grouped(const PassCtx& c, int m, int64_t n, bool dir,
                                                 bool dot, bool use_dp, double beta, double wa,
                                                 double L, double U_) {
+  // row 0 with the direction pass, then pairs (1,2), (3,4), ...: the +- rows
+  // of two-sided constraints (a row and its negation, adjacent) share a group,
+  // where the negation is detected (same 2m + 4 streamed vectors as before)
   int j = 0;
   if (dir) {
-    if (m >= PREP_GROUP) {
-      prep_group<PREP_GROUP, true>(c, 0, n, dot, use_dp, beta, wa, L, U_);
-      j = PREP_GROUP;
-    } else {
-      prep_group<1, true>(c, 0, n, dot, use_dp, beta, wa, L, U_);
-      j = 1;
-    }
+    prep_group<1, true>(c, 0, n, dot, use_dp, beta, wa, L, U_);
+    j = 1;
   }
   for (; j + PREP_GROUP <= m; j += PREP_GROUP)
     prep_group<PREP_GROUP, false>(c, j, n, dot, use_dp, beta, wa, L, U_);
@@ -738,6 +751,7 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
     PrepAcc A;
 #pragma unroll
     for (int s = 0; s < PREP_SLOTS; ++s) A.v[s] = 0.0;   // bp_lo = bp_hi = 0 (:58)
+    A.v[PS_NCONST] = A.v[PS_NNEG] = 1.0;   // (structure not examined here)
     const double* __restrict__ ar = P.grad;
     const int nch = num_chunks(P);
     const bool vec = al16(g) && al16(x) && al16(ar) && al16(dout) && al16(rho) &&
@@ -841,6 +855,7 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
       PrepAcc A;
 #pragma unroll
       for (int s2 = 0; s2 < PREP_SLOTS; ++s2) A.v[s2] = 0.0;   // bp_lo = bp_hi = 0 (:58)
+      A.v[PS_NCONST] = A.v[PS_NNEG] = 1.0;   // (structure not examined here)
       StreamRows Rj;
       Rj.nr = 3;
       Rj.row[0] = P.grad + (int64_t)j * ld; Rj.row[1] = rho;
@@ -956,6 +971,7 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
     PrepAcc A;
 #pragma unroll
     for (int s = 0; s < PREP_SLOTS; ++s) A.v[s] = 0.0;   // bp_lo = bp_hi = 0 (:58)
+    A.v[PS_NCONST] = A.v[PS_NNEG] = 1.0;   // (structure not examined here)
     const double* __restrict__ ar = P.grad + (int64_t)j * ld;
     for (int64_t i0 = c.i0; i0 < n; i0 += U * st) {
       double av[U], rv[U], gdv[U];
@@ -1138,7 +1154,11 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
   const bool gen = P.structured && P.row_kind[j] != RK_DENSE;
   const int gcode = gen ? srow_code(P, j) : 0;
   const GridIx G = grid_ix(P);
-  if ((!owner || P.part_ranges) && ((rlo | rhi) & 1) == 0 && (gen || al16(ar)) && al16(rho)) {
+  // a constant row found by PREP (the volume row) is not read again
+  const bool cst = !gen && P.n_alias && P.alias_kind[j] == AK_CONST;
+  const double cv = cst ? P.alias_c[j] : 0.0;
+  if ((!owner || P.part_ranges) && ((rlo | rhi) & 1) == 0 && (gen || cst || al16(ar)) &&
+      al16(rho)) {
     // 16-byte pairs over the row's elements (its own range for a range
     // partition); the trip count is warp-uniform (push is warp-collective)
     const int64_t n2 = rhi >> 1;
@@ -1147,8 +1167,8 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
     for (int64_t q0 = (rlo >> 1) + c.i0 - lane; q0 < n2; q0 += 2 * st) {
       const int64_t qa = q0 + lane, qb = q0 + st + lane;
       const bool oa = qa < n2, ob = qb < n2;
-      double2 a0 = (oa && !gen) ? A2[qa] : make_double2(0.0, 0.0);
-      double2 a1 = (ob && !gen) ? A2[qb] : make_double2(0.0, 0.0);
+      double2 a0 = (oa && !gen && !cst) ? A2[qa] : make_double2(cv, cv);
+      double2 a1 = (ob && !gen && !cst) ? A2[qb] : make_double2(cv, cv);
       const double2 r0 = oa ? R2[qa] : make_double2(0.0, 0.0), r1 = ob ? R2[qb] : make_double2(0.0, 0.0);
       if (gen) {   // structured row: generated from the element coordinates
         int64_t c0[3], c1[3];
@@ -1776,6 +1796,8 @@ __device__ __noinline__ void pass_feas_dense(const PassCtx& c) {
   }
 }
 
+__device__ __noinline__ void pass_feas_pat7(const PassCtx& c);
+
 __device__ __noinline__ void pass_feas(const PassCtx& c) {
   const Plan& pl = *c.plan;
   const Problem& P = pl.P;
@@ -1786,7 +1808,8 @@ __device__ __noinline__ void pass_feas(const PassCtx& c) {
   const double* __restrict__ rho = P.rho;
   const double* __restrict__ grad = P.grad;
   if (m == 7 && !P.structured && (n & 1) == 0 && (ld & 1) == 0 && al16(rho) && al16(grad)) {
-    pass_feas_dense<7>(c);
+    if (P.pat7) pass_feas_pat7(c);
+    else pass_feas_dense<7>(c);
     return;
   }
   if (m <= 8) {   // 16-byte pairs, FEAS_GROUP candidates per pass
@@ -1883,6 +1906,139 @@ __device__ __noinline__ void pass_newton_dense(const PassCtx& c) {
 #pragma unroll
   for (int k = 0; k < NG; ++k) v[M + k] = G[k];   // m = M: gram_idx is the packed order
   block_reduce_store<M + NG>(v, M + NG, PH_NEWTON, 0, c.out, c.smem);
+}
+
+// The C4/C5 row layout detected by PREP (P.pat7): row 0 constant (volume),
+// rows 2, 4, 6 the exact negations of rows 1, 3, 5 (the two-sided centre-of-
+// mass bands).  Only rho and rows 1, 3, 5 are read (32 instead of 64 bytes
+// per element), h is accumulated for rows 0, 1, 3, 5 and the Gram for their
+// 10 distinct products; the rest follow by exact sign flips:
+// h_{2k} = -h_{2k-1}; G(j, k) = s_j s_k G(b_j, b_k) (an FMA chain with
+// negated operands rounds to the negated value).  Bit-identical to
+// pass_newton_dense<7> (same elements per thread, same order, same ops).
+__device__ __forceinline__ int p7_base(int k) { return (k >= 2 && (k & 1) == 0) ? k - 1 : k; }
+__device__ __forceinline__ bool p7_neg(int k) { return k >= 2 && (k & 1) == 0; }
+
+__device__ __noinline__ void pass_newton_pat7(const PassCtx& c) {
+  constexpr int M = 7;
+  const Plan& pl = *c.plan;
+  const Problem& P = pl.P;
+  const Cmd& cmd = *c.cmd;
+  const double L = P.lower, U = P.upper;
+  const double a0 = P.alias_c[0];
+  const bool want_gram = cmd.want_gram;
+  constexpr int NB = 4;                 // distinct rows 0, 1, 3, 5
+  double h[NB], G[NB * (NB + 1) / 2];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) h[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < NB * (NB + 1) / 2; ++k) G[k] = 0.0;
+  const volatile double* ys = cmd.y;
+  const double2* __restrict__ R2 = reinterpret_cast<const double2*>(P.rho);
+  const double2* __restrict__ A2 = reinterpret_cast<const double2*>(P.grad);
+  const int64_t n2 = P.n >> 1, st = c.stride, ld2 = P.ld >> 1;
+  auto one = [&](double u, double v, double w, double r) {
+    const double a[M] = {a0, u, -u, v, -v, w, -w};
+    const double lo = L - r, hi = U - r;
+    double z = 0.0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const double yk = ys[k];
+      if (yk != 0.0) z += yk * a[k];
+    }
+    const bool clipped = (z < lo) || (z > hi);
+    const double dl = clipd(z, lo, hi);
+    const double b[NB] = {a0, u, v, w};
+#pragma unroll
+    for (int k = 0; k < NB; ++k) h[k] += b[k] * dl;
+    if (want_gram && !clipped) {
+      int q = 0;
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+#pragma unroll
+        for (int k = j; k < NB; ++k) { G[q] = __fma_rn(b[j], b[k], G[q]); ++q; }
+    }
+  };
+  for (int64_t q = c.i0; q < n2; q += st) {
+    const double2 r2 = R2[q], u2 = A2[ld2 + q], v2 = A2[3 * ld2 + q], w2 = A2[5 * ld2 + q];
+    one(u2.x, v2.x, w2.x, r2.x);
+    one(u2.y, v2.y, w2.y, r2.y);
+  }
+  // expand to the m = 7 layout: slots [0, 7) h, [7, 35) packed Gram
+  constexpr int NG = M * (M + 1) / 2;
+  double vv[M + NG];
+  const int bi[M] = {0, 1, 1, 2, 2, 3, 3};   // row -> distinct row
+#pragma unroll
+  for (int k = 0; k < M; ++k) vv[k] = p7_neg(k) ? -h[bi[k]] : h[bi[k]];
+  int q = 0;
+#pragma unroll
+  for (int j = 0; j < M; ++j)
+#pragma unroll
+    for (int k = j; k < M; ++k) {
+      const int x = bi[j] < bi[k] ? bi[j] : bi[k], y = bi[j] < bi[k] ? bi[k] : bi[j];
+      const int gi = x * NB - x * (x - 1) / 2 + (y - x);
+      vv[M + q] = (p7_neg(j) != p7_neg(k)) ? -G[gi] : G[gi];
+      ++q;
+    }
+  block_reduce_store<M + NG>(vv, M + NG, PH_NEWTON, 0, c.out, c.smem);
+}
+
+// FEAS for the P.pat7 layout (see pass_newton_pat7): rho and rows 1, 3, 5.
+__device__ __noinline__ void pass_feas_pat7(const PassCtx& c) {
+  constexpr int M = 7, NB = 4;
+  const Plan& pl = *c.plan;
+  const Problem& P = pl.P;
+  const Cmd& cmd = *c.cmd;
+  const double L = P.lower, U = P.upper;
+  const double a0 = P.alias_c[0];
+  const int64_t n2 = P.n >> 1, st = c.stride, ld2 = P.ld >> 1;
+  const double2* __restrict__ R2 = reinterpret_cast<const double2*>(P.rho);
+  const double2* __restrict__ A2 = reinterpret_cast<const double2*>(P.grad);
+  const volatile int* frow = cmd.feas_row;
+  const volatile double* fy = cmd.feas_y;
+  for (int f0 = 0; f0 < cmd.nfeas; f0 += FEAS_GROUP) {
+    const int ng = cmd.nfeas - f0 < FEAS_GROUP ? cmd.nfeas - f0 : FEAS_GROUP;
+    double acc[FEAS_GROUP][NB];
+#pragma unroll
+    for (int g = 0; g < FEAS_GROUP; ++g)
+#pragma unroll
+      for (int k = 0; k < NB; ++k) acc[g][k] = 0.0;
+    auto one = [&](double u, double v, double w, double r) {
+      const double a[M] = {a0, u, -u, v, -v, w, -w};
+      const double b[NB] = {a0, u, v, w};
+      const double lo = L - r, hi = U - r;
+#pragma unroll
+      for (int g = 0; g < FEAS_GROUP; ++g) {
+        const int rj = g < ng ? frow[f0 + g] : -1;
+        const double yj = g < ng ? fy[f0 + g] : 0.0;
+        double z = 0.0;
+        if (rj >= 0 && yj != 0.0) {
+          double arj = 0.0;
+#pragma unroll
+          for (int k = 0; k < M; ++k)
+            if (k == rj) arj = a[k];
+          z = 0.0 + yj * arj;
+        }
+        const double dl = clipd(z, lo, hi);
+#pragma unroll
+        for (int k = 0; k < NB; ++k) acc[g][k] += b[k] * dl;
+      }
+    };
+    for (int64_t q = c.i0; q < n2; q += st) {
+      const double2 r2 = R2[q], u2 = A2[ld2 + q], v2 = A2[3 * ld2 + q], w2 = A2[5 * ld2 + q];
+      one(u2.x, v2.x, w2.x, r2.x);
+      one(u2.y, v2.y, w2.y, r2.y);
+    }
+    const int bi[M] = {0, 1, 1, 2, 2, 3, 3};
+#pragma unroll
+    for (int g = 0; g < FEAS_GROUP; ++g) {
+      if (g >= ng) continue;
+      double vv[M];
+#pragma unroll
+      for (int k = 0; k < M; ++k) vv[k] = p7_neg(k) ? -acc[g][bi[k]] : acc[g][bi[k]];
+      block_reduce_store<M>(vv, M, PH_FEAS, (f0 + g) * M, c.out, c.smem);
+    }
+  }
 }
 
 template <int M>
@@ -2006,16 +2162,29 @@ __device__ __noinline__ void pass_final_m(const PassCtx& c) {
       };
       const bool sr = P.structured;
       const GridIx G = grid_ix(P);
-      int scode[M];
+      int scode[M], ak[M];
+      bool need[M];
 #pragma unroll
-      for (int k = 0; k < M; ++k) scode[k] = (sr && k < m && P.row_kind[k] != RK_DENSE) ? srow_code(P, k) : -1;
+      for (int k = 0; k < M; ++k) {
+        scode[k] = (sr && k < m && P.row_kind[k] != RK_DENSE) ? srow_code(P, k) : -1;
+        ak[k] = (P.n_alias && k < m) ? P.alias_kind[k] : AK_DENSE;
+        need[k] = k < m && (resid || yv[k] != 0.0);   // rows with y_k = 0: no read
+      }
+#pragma unroll
+      for (int k = M - 1; k >= 1; --k)   // a negated row reads its predecessor
+        if (ak[k] == AK_NEG && need[k]) need[k - 1] = true;
       for (int64_t q = c.i0; q < n2; q += st) {
         const double2 r2 = reinterpret_cast<const double2*>(rho)[q];
         double2 a2[M];
 #pragma unroll
-        for (int k = 0; k < M; ++k)   // rows with y_k = 0 are not read unless their dot is wanted
-          a2[k] = (k < m && scode[k] < 0 && (resid || yv[k] != 0.0))
+        for (int k = 0; k < M; ++k)
+          a2[k] = (need[k] && scode[k] < 0 && ak[k] == AK_DENSE)
                       ? reinterpret_cast<const double2*>(rows[k])[q] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < M; ++k) {   // structure found by PREP: exact copies
+          if (ak[k] == AK_CONST) a2[k] = make_double2(P.alias_c[k], P.alias_c[k]);
+          if (k > 0 && ak[k] == AK_NEG) a2[k] = make_double2(-a2[k - 1].x, -a2[k - 1].y);
+        }
         if (sr) {   // structured rows: generated from the element coordinates
           int64_t c0[3], c1[3];
           grid_coords(G, 2 * q + G.off, c0);
@@ -2176,8 +2345,10 @@ __device__ void pass_newton(const PassCtx& c) {
   const int m = c.plan->P.m;
   if (m == 7) {
     const Problem& P = c.plan->P;
-    if (!P.structured && (P.n & 1) == 0 && (P.ld & 1) == 0 && al16(P.rho) && al16(P.grad))
-      pass_newton_dense<7>(c);
+    if (!P.structured && (P.n & 1) == 0 && (P.ld & 1) == 0 && al16(P.rho) && al16(P.grad)) {
+      if (P.pat7) pass_newton_pat7(c);
+      else pass_newton_dense<7>(c);
+    }
     else
       pass_newton_m<7>(c);
     return;
@@ -2361,6 +2532,9 @@ __device__ __noinline__ void pass_exact(const PassCtx& c) {
       const int64_t nch = (len + CE - 1) / CE;
       if (warp == ncw) {                         // TMA producer (one lane)
         if (lane == 0) {
+          // the segment was written through the generic proxy by other CTAs
+          // (ordered by the grid barrier): order it before these async-proxy reads
+          asm volatile("fence.proxy.async.global;" ::: "memory");
           int st = stage;
           unsigned ph = phase;
           for (int64_t k = 0; k < nch; ++k) {
@@ -2403,7 +2577,17 @@ __device__ __noinline__ void pass_exact(const PassCtx& c) {
     }
     grid.sync();
   }
-  if (blockIdx.x == 0 && warp < ncw && my < nc) c.out[my] = acc;
+  if (blockIdx.x == 0) {
+    if (warp < ncw && my < nc) c.out[my] = acc;
+    // every chunk was consumed (the grid barrier above): retire the barriers,
+    // the next chain pass initializes them afresh
+    if (threadIdx.x == 0)
+      for (int k = 0; k < NST; ++k) {
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(full + k)) : "memory");
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(empty + k)) : "memory");
+      }
+    __syncthreads();
+  }
 }
 
 __device__ void run_pass(const PassCtx& c) {

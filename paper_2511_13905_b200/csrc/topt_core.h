@@ -249,13 +249,21 @@ struct Problem {
   int32_t strict;
   int32_t ex_nst;               // ring stages of the chain consumer (16 KB each)
   int32_t ex_smem;              // byte offset of the chain ring in dynamic shared memory
-  int32_t pad3_;
+  int32_t ex_debug;             // print each chain pass's first results (TOPT_B200_EXDEBUG)
   double* ex_buf;               // 2 x ex_seg x MAX_EX doubles (term staging)
   int64_t ex_seg;               // elements per staged segment
   const int32_t* part_idx;      // device partition indices (CSR; for subset chains)
   int64_t part_off[MAX_M + 1];  // host-copied CSR offsets
+  // row structure found by PREP (controller-written; the passes after PREP
+  // read each distinct row once): AK_CONST rows a_i = alias_c, AK_NEG rows
+  // a_i = -a_{k-1,i}; pat7: the volume + 3 paired centre-of-mass layout
+  int8_t alias_kind[MAX_M];
+  int32_t n_alias, pat7;
+  double alias_c[MAX_M];
 };
 enum RowKind { RK_DENSE = 0, RK_CONST = 1, RK_CENTROID = 2 };
+// Row structure detected in the data by PREP (dense rows, single rank).
+enum AliasKind { AK_DENSE = 0, AK_CONST = 1, AK_NEG = 2 };
 constexpr int MAX_TAB = 8192;   // centroid table entries (shared memory, 64 KB)
 
 // Controller-visible result.
@@ -295,7 +303,7 @@ struct Plan {
   int32_t ghat_ex_ok;                 // g_hat dots below are reference-order exact
   int32_t nglobal;                    // grid-synchronized passes so far (partials buffer parity)
   double ghat_dot_ex[MAX_M];
-  double prep_save[MAX_M * 9];        // PREP totals held across the g_hat chain pass
+  double prep_save[MAX_M * 12];       // PREP totals held across the g_hat chain pass
   double step_save[6];
   Scratch sc;
 };

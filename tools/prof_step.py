@@ -62,7 +62,7 @@ def trace(config="C2", seed=2, structured=False):
     allt = np.array(buf, dtype=np.float64).reshape(128, 8)
     t, mk = allt[:64], allt[64:]
     t0 = t[0, 0]
-    names = {0: "STEP", 1: "PREP", 2: "SWEEP", 3: "FEAS", 4: "NEWTON", 5: "FINAL", 7: "GATHER"}
+    names = {0: "STEP", 1: "PREP", 2: "SWEEP", 3: "FEAS", 4: "NEWTON", 5: "FINAL", 7: "GATHER", 8: "EXACT"}
     print(p.name, "n", p.n, "m", p.m)
     for k in range(64):
         if t[k, 0] == 0:
