@@ -209,6 +209,37 @@ def project(rho, grad, g_values, bounds_g, gd_step, is_eq=None, partition=None,
                 phi_inf=gam[64:64 + min(meta.newton_iters, 64)].copy(), trace=tr)
 
 
+def enum_project(rho, grad, ghat, is_eq=None, lower=0.0, upper=1.0, tol=1e-10):
+    """SPEC.md:231-239 enumeration oracle (oracle/enum.c): exact projection by
+    enumerating 3^N box x 2^m constraint activity patterns.  Returns (delta, y)
+    or None when the linearized set is empty."""
+    grad = _f64(np.atleast_2d(grad)); m, n = grad.shape
+    is_eq = np.zeros(m, np.uint8) if is_eq is None else np.ascontiguousarray(is_eq, np.uint8)
+    d = np.empty(n); y = np.empty(m)
+    rc = lib().orc_enum_project(C.c_int(n), C.c_int(m), _p(_f64(rho)), _p(grad), _p(_f64(ghat)),
+                                _p(is_eq), C.c_double(lower), C.c_double(upper), C.c_double(tol),
+                                _p(d), _p(y))
+    if rc == 2:
+        raise ValueError("enumeration oracle: N <= 12 and m <= 3 only")
+    return None if rc == 1 else (d, y)
+
+
+def random_instance(rng, n, m, feasible=True, eq_rows=0):
+    """A random projection instance (rho_tilde, A, g_hat): rho in (-0.3, 1.3),
+    rows ~ N(0, 1); feasible ones get g_hat = A (x0 - rho) + slack for a random
+    box point x0 (slack >= 0 on inequality rows, 0 on equality rows)."""
+    rho = rng.uniform(-0.3, 1.3, n)
+    A = rng.standard_normal((m, n))
+    x0 = rng.uniform(0.0, 1.0, n)
+    base = A @ (x0 - rho)
+    slack = rng.uniform(0.0, 0.5, m) * (rng.uniform(size=m) < 0.7)
+    is_eq = np.zeros(m, np.uint8)
+    is_eq[:eq_rows] = 1
+    slack[:eq_rows] = 0.0
+    ghat = base + slack if feasible else base - 5.0 - abs(base)
+    return rho, A, ghat, is_eq
+
+
 def settings(alpha_max=1e2, alpha_fallback=0.2, omega=1.0, eps_alpha=1e-6, tol_n=1e-6,
              t_warmup=50):
     return OrcPgdSettings(alpha_max, alpha_fallback, omega, eps_alpha, tol_n, t_warmup)

@@ -1057,6 +1057,7 @@ template <int KC>
 struct SweepAcc {
   double C[KC], S[KC];
   double Sall;   // slopes of elements free at every candidate (p1 = 0, p2 = cnt)
+  double Clo, Chi;   // constants of elements clipped alike at every candidate
   double* qa;    // this warp's queue (shared memory, SQ_CAP entries)
   double* qr;
   int qn;
@@ -1067,7 +1068,7 @@ struct SweepAcc {
                                        double L_, double U_) {
 #pragma unroll
     for (int k = 0; k < KC; ++k) { C[k] = 0.0; S[k] = 0.0; }
-    Sall = 0.0;
+    Sall = 0.0; Clo = 0.0; Chi = 0.0;
     qa = qa_; qr = qr_; qn = 0; y = y_; cnt = cnt_; L = L_; U = U_;
   }
   // all 32 lanes call push together (valid = this lane holds an element)
@@ -1088,8 +1089,17 @@ struct SweepAcc {
       }
       if (p1 == p2) {
         const double cl = a * (pos ? lo : hi), ch = a * (pos ? hi : lo);
+        // the walk window is narrow after the first sweep: nearly every
+        // element is clipped alike at every candidate -- one sum, added to
+        // every C_k at the end, instead of a select + add per candidate
+        if (p1 == 0) {
+          Chi += ch;
+        } else if (p1 >= cnt) {
+          Clo += cl;
+        } else {
 #pragma unroll
-        for (int k = 0; k < KC; ++k) C[k] += (k < p1) ? cl : ch;
+          for (int k = 0; k < KC; ++k) C[k] += (k < p1) ? cl : ch;
+        }
       } else if (p1 == 0 && p2 == cnt) {
         // free at every candidate (a small |a| makes the window wide): its
         // term is y_k a^2 for all k -- one slope sum, added to every S_k at
@@ -1120,8 +1130,11 @@ struct SweepAcc {
     qn = 0;
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < KC; ++k) S[k] += Sall;
-    Sall = 0.0;
+    for (int k = 0; k < KC; ++k) {
+      S[k] += Sall;
+      C[k] = (C[k] + Chi) + Clo;
+    }
+    Sall = 0.0; Clo = 0.0; Chi = 0.0;
   }
 };
 
@@ -1959,7 +1972,19 @@ __device__ __noinline__ void pass_newton_pat7(const PassCtx& c) {
         for (int k = j; k < NB; ++k) { G[q] = __fma_rn(b[j], b[k], G[q]); ++q; }
     }
   };
-  for (int64_t q = c.i0; q < n2; q += st) {
+  // two pairs per thread in flight (8 x 16-byte loads): the pass is HBM-bound
+  // only with enough bytes in flight per SM; same per-thread element order
+  int64_t q = c.i0;
+  for (; q + st < n2; q += 2 * st) {
+    const double2 r2 = R2[q], u2 = A2[ld2 + q], v2 = A2[3 * ld2 + q], w2 = A2[5 * ld2 + q];
+    const double2 r3 = R2[q + st], u3 = A2[ld2 + q + st], v3 = A2[3 * ld2 + q + st],
+                  w3 = A2[5 * ld2 + q + st];
+    one(u2.x, v2.x, w2.x, r2.x);
+    one(u2.y, v2.y, w2.y, r2.y);
+    one(u3.x, v3.x, w3.x, r3.x);
+    one(u3.y, v3.y, w3.y, r3.y);
+  }
+  if (q < n2) {
     const double2 r2 = R2[q], u2 = A2[ld2 + q], v2 = A2[3 * ld2 + q], w2 = A2[5 * ld2 + q];
     one(u2.x, v2.x, w2.x, r2.x);
     one(u2.y, v2.y, w2.y, r2.y);
@@ -1970,15 +1995,15 @@ __device__ __noinline__ void pass_newton_pat7(const PassCtx& c) {
   const int bi[M] = {0, 1, 1, 2, 2, 3, 3};   // row -> distinct row
 #pragma unroll
   for (int k = 0; k < M; ++k) vv[k] = p7_neg(k) ? -h[bi[k]] : h[bi[k]];
-  int q = 0;
+  int s = 0;
 #pragma unroll
   for (int j = 0; j < M; ++j)
 #pragma unroll
     for (int k = j; k < M; ++k) {
       const int x = bi[j] < bi[k] ? bi[j] : bi[k], y = bi[j] < bi[k] ? bi[k] : bi[j];
       const int gi = x * NB - x * (x - 1) / 2 + (y - x);
-      vv[M + q] = (p7_neg(j) != p7_neg(k)) ? -G[gi] : G[gi];
-      ++q;
+      vv[M + s] = (p7_neg(j) != p7_neg(k)) ? -G[gi] : G[gi];
+      ++s;
     }
   block_reduce_store<M + NG>(vv, M + NG, PH_NEWTON, 0, c.out, c.smem);
 }
@@ -2024,7 +2049,17 @@ __device__ __noinline__ void pass_feas_pat7(const PassCtx& c) {
         for (int k = 0; k < NB; ++k) acc[g][k] += b[k] * dl;
       }
     };
-    for (int64_t q = c.i0; q < n2; q += st) {
+    int64_t q = c.i0;
+    for (; q + st < n2; q += 2 * st) {   // two pairs in flight (see pass_newton_pat7)
+      const double2 r2 = R2[q], u2 = A2[ld2 + q], v2 = A2[3 * ld2 + q], w2 = A2[5 * ld2 + q];
+      const double2 r3 = R2[q + st], u3 = A2[ld2 + q + st], v3 = A2[3 * ld2 + q + st],
+                    w3 = A2[5 * ld2 + q + st];
+      one(u2.x, v2.x, w2.x, r2.x);
+      one(u2.y, v2.y, w2.y, r2.y);
+      one(u3.x, v3.x, w3.x, r3.x);
+      one(u3.y, v3.y, w3.y, r3.y);
+    }
+    if (q < n2) {
       const double2 r2 = R2[q], u2 = A2[ld2 + q], v2 = A2[3 * ld2 + q], w2 = A2[5 * ld2 + q];
       one(u2.x, v2.x, w2.x, r2.x);
       one(u2.y, v2.y, w2.y, r2.y);
@@ -2173,13 +2208,15 @@ __device__ __noinline__ void pass_final_m(const PassCtx& c) {
 #pragma unroll
       for (int k = M - 1; k >= 1; --k)   // a negated row reads its predecessor
         if (ak[k] == AK_NEG && need[k]) need[k - 1] = true;
-      for (int64_t q = c.i0; q < n2; q += st) {
-        const double2 r2 = reinterpret_cast<const double2*>(rho)[q];
-        double2 a2[M];
+      // loads of one element pair; derived rows filled in (exact copies)
+      auto load = [&](int64_t q, double2& r2, double2 (&a2)[M]) {
+        r2 = reinterpret_cast<const double2*>(rho)[q];
 #pragma unroll
         for (int k = 0; k < M; ++k)
           a2[k] = (need[k] && scode[k] < 0 && ak[k] == AK_DENSE)
                       ? reinterpret_cast<const double2*>(rows[k])[q] : make_double2(0.0, 0.0);
+      };
+      auto finish = [&](int64_t q, const double2 r2, double2 (&a2)[M]) {
 #pragma unroll
         for (int k = 0; k < M; ++k) {   // structure found by PREP: exact copies
           if (ak[k] == AK_CONST) a2[k] = make_double2(P.alias_c[k], P.alias_c[k]);
@@ -2208,6 +2245,19 @@ __device__ __noinline__ void pass_final_m(const PassCtx& c) {
           mk.y = b1 ? 1 : (u1 ? 2 : 0);
           reinterpret_cast<uchar2*>(mout)[q] = mk;
         }
+      };
+      int64_t q = c.i0;
+      for (; q + st < n2; q += 2 * st) {   // two pairs' loads in flight per thread
+        double2 r2, r3, a2[M], a3[M];
+        load(q, r2, a2);
+        load(q + st, r3, a3);
+        finish(q, r2, a2);
+        finish(q + st, r3, a3);
+      }
+      if (q < n2) {
+        double2 r2, a2[M];
+        load(q, r2, a2);
+        finish(q, r2, a2);
       }
       if (resid) block_reduce_store<M>(acc, m, PH_FINAL, 0, c.out, c.smem);
       return;

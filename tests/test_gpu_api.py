@@ -113,29 +113,6 @@ def test_full_c3_independent():
     assert np.array_equal(r.delta, ref["delta"])
 
 
-def test_full_c4p_newton():
-    """Full-size C4' (n = 8,388,608, m = 7, stage 1 -> semismooth Newton) against
-    the compiled reference's result summary (tests/golden/make_golden_full.py;
-    the full vectors are too large to commit).  Seed 11 is one where the
-    reference's Newton converges (4 iterations); on seeds 4 and 12 the
-    reference itself stalls at the 50-iteration cap."""
-    import json
-    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
-                                       "c4p_full_summary.json")))["11"]
-    p = synth.CONFIGS["C4p"](11)
-    st = api.pgd_step(p.x, p.x_prev, p.g, p.g_prev, p.d_prev, p.grad, p.g_values, p.bounds_g,
-                      p.is_eq, None, t=p.t)
-    assert st.projection.path.name == gold["path"] == "newton"
-    assert st.projection.newton_iters == gold["newton_iters"]
-    assert bool(st.projection.converged) == gold["converged"]
-    assert st.alpha == pytest.approx(gold["alpha"], rel=1e-13)
-    np.testing.assert_allclose(st.y, gold["y"], rtol=1e-9, atol=1e-9)
-    x = st.x_new
-    assert float(np.sum(x)) == pytest.approx(gold["x_sum"], rel=1e-12)
-    assert float(np.sum(x * x)) == pytest.approx(gold["x_sq"], rel=1e-11)
-    assert abs(int((x < 1e-12).sum()) - gold["n_at_lower"]) <= 8
-
-
 def test_range_partition_matches_generic_partition():
     """C3's sets are contiguous index ranges (rows then visit only their own
     range); the same sets listed in descending order take the generic owner

@@ -1,21 +1,18 @@
 """Full-size GPU checks of the Newton-path configs (C4, C4', C5).
 
-C4 (n = 8,388,608, m = 7) runs against the oracle on the same inputs.  The
-reference's Newton loop stops when its own sequentially summed ||Phi||_inf
-drops below tol_n = 1e-6 (projection.cpp:356); at this size that sum's
-rounding noise is itself ~1e-6 (its iterate-4 value 2.4e-6 is noise: the
-exactly summed value at that point is ~1e-8), so the reference takes 6
-iterations where ours -- tree-summed, ~1e-9 noise -- takes 4.  The test
-therefore asserts, besides path, duals, x (normwise 1e-12) and identical
-active masks: that our stopping point is converged in exact arithmetic
-(||Phi(y)||_inf <= tol_n with the h-dots summed in 80-bit extended precision)
-and that we never take MORE Newton iterations than the reference.
+Certified mode (the default) at full size against the compiled reference's
+results (tests/golden/full_summary.json, make_golden_full.py): C4 / C4' on
+several seeds and C5 (n = 268,435,456).  The reference's Newton loop stops
+when its own sequentially summed ||Phi||_inf drops below tol_n = 1e-6
+(projection.cpp:356); at this size that sum's rounding noise is itself
+~1e-6, so on some seeds (C4 seed 15) the reference never sees convergence and
+ends after 50 noise-driven iterations.  Certified mode sums accurately and
+stops at the true tolerance; tests/test_gpu_strict.py reproduces the
+reference's own trajectory bit for bit in strict mode.
 
-C5 (n = 268,435,456) is beyond what the CPU reference can run in a test (one
-reference step takes tens of minutes); it is checked through size-independent
-properties: x_{t+1} and rho_tilde equal their defining elementwise formulas
-bit for bit (recomputed in numpy, the reference's operation order), bounds,
-determinism of two runs, and for the Newton path exact-arithmetic convergence.
+C5 is also checked through size-independent properties: x_{t+1} and
+rho_tilde equal their defining elementwise formulas bit for bit, bounds,
+determinism of two runs, and exact-arithmetic convergence.
 """
 import numpy as np
 import pytest
@@ -56,25 +53,56 @@ def _phi_exact(y, grad, rho, ghat, is_eq, lower=0.0, upper=1.0):
     return float(np.max(np.abs(phi)))
 
 
-def test_full_c4_newton_vs_oracle():
-    p = synth.CONFIGS["C4"](4)
-    ref = O.pgd_step(p)
-    rt, gd = ref["rho_tilde"], ref["gd_step"]
-    lin = api.ConstraintLinearization.build(p.m, p.n, p.grad, p.g_values, p.bounds_g, gd,
-                                            p.is_eq, p.partition)
-    res = api.project(rt, lin, p.lower, p.upper)
-    orc = O.project(rt, p.grad, p.g_values, p.bounds_g, gd, p.is_eq, p.partition, p.lower,
-                    p.upper)
-    assert res.path.name == orc["path"] == "newton"
-    assert res.converged and orc["converged"]
-    assert res.newton_iters <= orc["newton_iters"]
-    np.testing.assert_allclose(res.y, orc["y"], rtol=1e-9, atol=1e-9)
-    x_g, x_o = rt + res.delta, rt + orc["delta"]
-    assert np.max(np.abs(x_g - x_o)) <= 1e-12 * np.max(np.abs(x_o))
-    assert np.array_equal(_masks(res.y, p.grad, rt), _masks(orc["y"], p.grad, rt))
-    # both stopping points are converged in exact arithmetic
-    assert _phi_exact(res.y, p.grad, rt, lin.g_hat, p.is_eq) <= TOL_N
-    assert _phi_exact(orc["y"], p.grad, rt, lin.g_hat, p.is_eq) <= TOL_N
+def _summary(key):
+    import json
+    import os
+    data = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                       "full_summary.json")))
+    if key not in data:
+        pytest.skip(f"{key} not in full_summary.json")
+    return data[key]
+
+
+def _certified_vs_summary(name, seed):
+    """Certified mode (the default) against the compiled reference's full-size
+    result: same path, duals within 1e-9, x_{t+1} moments within 1e-12, and
+    IDENTICAL active masks (north_star: "identical active-bound masks").  The
+    Newton iteration count may be lower than the reference's when its own
+    sequentially summed ||Phi|| stalls on rounding noise (it then ends
+    not converged); both stopping points must satisfy the tolerance in
+    extended precision."""
+    import hashlib
+    g = _summary(f"{name}:{seed}")
+    p = synth.CONFIGS[name](seed)
+    st = api.pgd_step(p.x, p.x_prev, p.g, p.g_prev, p.d_prev, p.grad, p.g_values, p.bounds_g,
+                      p.is_eq, None, t=p.t, want_mask=True)
+    pr = st.projection
+    assert pr.path.name == g["path"]
+    assert st.alpha == pytest.approx(g["alpha"], rel=1e-13)
+    np.testing.assert_allclose(st.y, g["y"], rtol=1e-9, atol=1e-9)
+    x = st.x_new
+    assert float(np.sum(x)) == pytest.approx(g["x_sum"], rel=1e-12)
+    assert float(np.sum(x * x)) == pytest.approx(g["x_sq"], rel=1e-11)
+    assert hashlib.sha256(st.mask.tobytes()).hexdigest() == g["mask_sha256"]
+    if g["path"] == "newton":
+        if g["converged"]:
+            assert pr.newton_iters == g["newton_iters"]
+        else:   # the reference stalled on its own summation noise
+            assert pr.newton_iters <= g["newton_iters"]
+        assert pr.converged
+        assert _phi_exact(st.y, p.grad, st.rho_tilde, st.g_hat, p.is_eq) <= TOL_N
+    return st
+
+
+@pytest.mark.parametrize("name,seed", [("C4", 4), ("C4", 11), ("C4", 12), ("C4p", 4),
+                                       ("C4p", 11), ("C4p", 12), ("C4", 21), ("C4p", 13),
+                                       ("C4", 15)])
+def test_full_newton_certified_vs_reference(name, seed):
+    _certified_vs_summary(name, seed)
+
+
+def test_full_c5_certified_vs_reference():
+    _certified_vs_summary("C5", 5)
 
 
 def test_full_c5_properties():

@@ -102,3 +102,38 @@ def test_pgd_step_dense_row_groups(m, half_g):
     if ref["path"] == "newton":
         assert st.projection.newton_iters == ref["newton_iters"]
     assert np.max(np.abs(st.x_new - x_o)) <= 1e-12 * np.max(np.abs(x_o))
+
+
+@pytest.mark.parametrize("t,violation", [(0, 0.0), (60, 1e-3)])
+@pytest.mark.parametrize("name", ["C1", "C4p"])
+def test_pgd_step_fallback(name, t, violation):
+    """The fallback step on the GPU (Alg. 3 lines
+    4-8): at t = 0, and at t >= t_warmup with violation > tol_N, alpha =
+    min(alpha_max, alpha_fallback / ||grad f||_inf) exactly and the CG memory
+    resets (d = grad f); then the projection as usual, masks identical."""
+    p = synth.SMALL[name](4)
+    p.t, p.violation = t, violation
+    ref = O.pgd_step(p)
+    st = api.pgd_step(p.x, p.x_prev, p.g, p.g_prev, p.d_prev, p.grad, p.g_values, p.bounds_g,
+                      p.is_eq, p.partition, t=t, violation=violation, want_mask=True)
+    assert st.fallback and ref["fallback"]
+    assert st.alpha == min(100.0, 0.2 / np.max(np.abs(p.g))) == ref["alpha"]
+    assert st.beta == 0.0
+    assert np.array_equal(st.d, p.g)
+    assert np.array_equal(st.rho_tilde, ref["rho_tilde"])
+    assert st.projection.path.name == ref["path"]
+    x_o = ref["x_new"]
+    assert np.max(np.abs(st.x_new - x_o)) <= 1e-12 * np.max(np.abs(x_o))
+    assert np.array_equal(st.mask, masks(ref["y"], p.grad, ref["rho_tilde"]))
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C4p"])
+def test_pgd_step_masks(name):
+    """Every certified-mode step: the active masks (clip branch of z) equal the
+    reference's (north_star: identical active-bound masks)."""
+    p = synth.SMALL[name](8)
+    ref = O.pgd_step(p)
+    st = api.pgd_step(p.x, p.x_prev, p.g, p.g_prev, p.d_prev, p.grad, p.g_values, p.bounds_g,
+                      p.is_eq, p.partition, t=p.t, want_mask=True)
+    assert st.projection.path.name == ref["path"]
+    assert np.array_equal(st.mask, masks(ref["y"], p.grad, ref["rho_tilde"]))

@@ -170,3 +170,56 @@ def test_oracle_against_golden(path):
     assert np.array_equal(r["delta"], g["delta"])
     assert r["newton_iters"] == int(g["newton_iters"])
     assert r["residual"] == float(g["residual"])
+
+
+# ---- the spec's enumeration oracle (oracle/enum.c) ---------
+
+def test_enum_oracle_kats():
+    """the analytic halfspace example, the infeasible flag on
+    {rho <= 0.3, rho >= 0.6}, and idempotence (projecting the projection)."""
+    d, y = O.enum_project([0.8, 0.6], [[0.5, 0.5]], [0.5 - 0.7])
+    np.testing.assert_allclose(d, [-0.2, -0.2], atol=1e-14)
+    assert O.enum_project([0.5], [[1.0], [-1.0]], [0.3 - 0.5, -0.6 + 0.5]) is None
+    rng = np.random.default_rng(5)
+    for _ in range(50):
+        rho, A, gh, _ = O.random_instance(rng, int(rng.integers(1, 7)), 2)
+        d, _ = O.enum_project(rho, A, gh)
+        x = rho + d
+        d2, _ = O.enum_project(x, A, gh - A @ d)
+        assert np.max(np.abs(d2)) <= 1e-12
+
+
+def test_enum_oracle_matches_reference():
+    """The enumeration oracle agrees with the compiled reference (oracle/_ref)
+    to 1e-6 on random single-row (N <= 8) and coupled two-row (N <= 6)
+    instances -- the reference's own acceptance bound."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(11)
+    for n_max, m, count in ((8, 1, 300), (6, 2, 200)):
+        for _ in range(count):
+            n = int(rng.integers(1, n_max + 1))
+            rho, A, gh, ie = O.random_instance(rng, n, m)
+            d, _ = O.enum_project(rho, A, gh)
+            ref = O.ref_project(rho, A, np.zeros(m), gh, np.zeros(n))
+            assert np.max(np.abs(d - ref["delta"])) <= 1e-6
+
+
+def test_enum_oracle_four_materials():
+    """a 4-material instance (N = 16, four disjoint blocks) --
+    the partitioned projection equals the blockwise enumeration."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(3)
+    rho = rng.uniform(-0.1, 0.6, 16)
+    A = np.zeros((4, 16))
+    for k in range(4):
+        A[k, 4 * k:4 * k + 4] = 1.0
+    gh = np.array([0.4, -0.3, 0.1, -0.6])
+    part = [np.arange(4 * k, 4 * k + 4, dtype=np.int32) for k in range(4)]
+    ref = O.ref_project(rho, A, np.zeros(4), gh, np.zeros(16), None, part)
+    assert ref["path"] == "independent_binary"
+    for k in range(4):
+        s = slice(4 * k, 4 * k + 4)
+        d, _ = O.enum_project(rho[s], A[k:k + 1, s], gh[k:k + 1])
+        np.testing.assert_allclose(ref["delta"][s], d, atol=1e-6)

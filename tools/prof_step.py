@@ -83,7 +83,7 @@ if __name__ == "__main__":
         if structured:
             sys.argv.remove("--structured")
         cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
-        seed = int(sys.argv[2]) if len(sys.argv) > 2 else {"C1": 1, "C2": 2, "C3": 3}.get(cfg, 4)
+        seed = int(sys.argv[2]) if len(sys.argv) > 2 else {"C1": 1, "C2": 2, "C3": 3, "C5": 5}.get(cfg, 4)
         trace(cfg, seed, structured)
     else:
         main()
