@@ -289,6 +289,47 @@ int topt_b200_step_direction(topt_b200_ctx* ctx, int64_t n, const double* x,
                              double* rho_tilde_out, double* alpha_out, double* beta_out,
                              int32_t* fallback_out);
 
+/* ---- upstream of the step ---------------------
+ * Density filter: the row-normalized linear hat kernel of build_filter on an
+ * nx x ny StructuredGrid (element e = ey nx + ex, unit element size;
+ * filter.cpp:10-43), applied matrix-free on the GPU with the reference's
+ * weights and summation orders: W x (apply_filter, filter.cpp:45-56) and
+ * W^T g (filter_chain_rule, filter.cpp:58-69), bit-identical to the CSR code.
+ * Status: radius <= 0 or nx, ny < 1 -> TOPT_ERR_PARAMETER (ParameterError). */
+typedef struct topt_b200_filter topt_b200_filter;
+int topt_b200_filter_create(topt_b200_ctx* ctx, int32_t nx, int32_t ny, double radius,
+                            topt_b200_filter** out);
+void topt_b200_filter_destroy(topt_b200_filter* f);
+int64_t topt_b200_filter_nnz(const topt_b200_filter* f);
+/* build_filter's CSR (row_ptr: n + 1, col / weight: nnz entries; host). */
+int topt_b200_filter_csr(const topt_b200_filter* f, int32_t* row_ptr, int32_t* col,
+                         double* weight);
+/* transpose = 0: out = W in ; 1: out = W^T in.  n = nx ny doubles each. */
+int topt_b200_filter_apply(topt_b200_ctx* ctx, const topt_b200_filter* f, int transpose,
+                           const double* in, double* out);
+int topt_b200_filter_apply_dev(topt_b200_ctx* ctx, const topt_b200_filter* f, int transpose,
+                               const double* in_dev, double* out_dev);
+/* Any CSR filter kernel (a topt::FilterKernel, host arrays): W x / W^T x in
+ * the reference's orders. */
+int topt_b200_csr_apply(topt_b200_ctx* ctx, int64_t n, const int32_t* row_ptr, const int32_t* col,
+                        const double* weight, int transpose, const double* in, double* out);
+/* SIMP interpolate_stiffness (material.cpp:19-46), device buffers (densities
+ * N*K channel-major; young: K host values).  derivative may be NULL.
+ * pow() is CUDA's (<= 2 ulp), every other operation the reference's. */
+int topt_b200_interpolate_stiffness_dev(topt_b200_ctx* ctx, int64_t n, int32_t k,
+                                        const double* young, double e_min, double poisson,
+                                        double penalty, const double* dens_dev,
+                                        double* moduli_dev, double* der_dev);
+/* element_stiffness_q4 (fea.cpp:20-58): 64 values, row-major, host. */
+int topt_b200_element_stiffness_q4(double poisson, double element_size, double* ke64);
+/* Element energies u_e^T k0 u_e and the compliance gradient -dE * energy
+ * (fea.cpp:162-181) from a displacement field u (2 (nx+1)(ny+1) dofs,
+ * grid.cpp:15-24 numbering); device buffers, energy / grad may be NULL. */
+int topt_b200_compliance_gradient_dev(topt_b200_ctx* ctx, int32_t nx, int32_t ny,
+                                      double element_size, double poisson, const double* u_dev,
+                                      int32_t kmat, const double* der_dev, double* energy_dev,
+                                      double* grad_dev);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,6 +9,9 @@
 //   ref_validate          -> ConstraintLinearization::validate (projection.cpp:150-181)
 //   ref_delta_of_y        -> delta_of_y                        (projection.cpp:192-209)
 //   ref_residual_h        -> constraint_residual_h             (projection.cpp:253-267)
+//   ref_filter_csr        -> build_filter                      (filter.cpp:10-43)
+//   ref_filter_apply      -> apply_filter / filter_chain_rule  (filter.cpp:45-69)
+//   ref_interpolate       -> interpolate_stiffness             (material.cpp:19-46)
 //   ref_project           -> project / project_single_binary_search /
 //                            project_independent / project_general_newton
 //                                                               (projection.cpp:211-460)
@@ -22,6 +25,9 @@
 #include <vector>
 
 #include "topt/errors.hpp"
+#include "topt/filter.hpp"
+#include "topt/grid.hpp"
+#include "topt/material.hpp"
 #include "topt/projection.hpp"
 
 namespace {
@@ -174,6 +180,54 @@ int ref_project(int which, std::size_t n, std::size_t m, const double* rho,
     meta_i[2] = res.converged ? 1 : 0;
     meta_i[3] = res.curvature_violations;
     *residual_out = res.residual;
+  });
+}
+
+// build_filter's CSR (filter.cpp:10-43).  nnz_io: in = capacity of col /
+// weight (0: query only), out = nnz.
+int ref_filter_csr(int nx, int ny, double radius, int32_t* row_ptr, int32_t* col, double* weight,
+                   int64_t* nnz_io, char* err, std::size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const topt::StructuredGrid grid(nx, ny);
+    const topt::FilterKernel k = topt::build_filter(grid, radius);
+    const int64_t cap = *nnz_io;
+    *nnz_io = (int64_t)k.col.size();
+    if (cap <= 0) return;
+    for (std::size_t e = 0; e <= k.size; ++e) row_ptr[e] = k.row_ptr[e];
+    for (std::size_t i = 0; i < k.col.size() && (int64_t)i < cap; ++i) {
+      col[i] = k.col[i];
+      weight[i] = k.weight[i];
+    }
+  });
+}
+
+// apply_filter (transpose = 0, filter.cpp:45-56) / filter_chain_rule
+// (transpose = 1, filter.cpp:58-69) with the kernel build_filter makes.
+int ref_filter_apply(int nx, int ny, double radius, int transpose, const double* in, double* out,
+                     char* err, std::size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const topt::StructuredGrid grid(nx, ny);
+    const topt::FilterKernel k = topt::build_filter(grid, radius);
+    const std::span<const double> v(in, k.size);
+    const std::vector<double> r =
+        transpose ? topt::filter_chain_rule(k, v) : topt::apply_filter(k, v);
+    std::memcpy(out, r.data(), r.size() * sizeof(double));
+  });
+}
+
+// interpolate_stiffness (material.cpp:19-46): moduli (N) and derivative (N*K).
+int ref_interpolate(std::size_t n, std::size_t k, const double* young, double e_min,
+                    double poisson, double penalty, const double* densities, double* moduli,
+                    double* derivative, char* err, std::size_t errlen) {
+  return guarded(err, errlen, [&] {
+    topt::MaterialModel mm;
+    mm.young_moduli.assign(young, young + k);
+    mm.e_min = e_min;
+    mm.poisson = poisson;
+    mm.penalty = penalty;
+    const auto r = topt::interpolate_stiffness(std::span<const double>(densities, n * k), n, mm);
+    std::memcpy(moduli, r.moduli.data(), n * sizeof(double));
+    std::memcpy(derivative, r.derivative.data(), n * k * sizeof(double));
   });
 }
 

@@ -595,7 +595,9 @@ TOPT_HDN inline void ex_add(Plan& pl, int kind, int j, int k, double y, double s
 // Element sequence the reference sums a walk of row j over: its partition
 // set on the independent path (projection.cpp:242-248), all of 0..n-1 else.
 TOPT_HD int walk_seq(const Plan& pl, int j) {
-  return (pl.stage == SG_INDEP && pl.P.has_part) ? j : -1;
+  const bool indep = pl.stage == SG_INDEP ||
+                     (pl.stage == SG_FINAL && pl.res.path == PATH_INDEPENDENT);
+  return (indep && pl.P.has_part) ? j : -1;
 }
 
 TOPT_HDN inline void cmd_final(Plan& pl, const double* y, int resid_rows) {

@@ -80,10 +80,11 @@ def _certified_vs_summary(name, seed):
     assert pr.path.name == g["path"]
     assert st.alpha == pytest.approx(g["alpha"], rel=1e-13)
     np.testing.assert_allclose(st.y, g["y"], rtol=1e-9, atol=1e-9)
-    x = st.x_new
-    assert float(np.sum(x)) == pytest.approx(g["x_sum"], rel=1e-12)
-    assert float(np.sum(x * x)) == pytest.approx(g["x_sq"], rel=1e-11)
     assert hashlib.sha256(st.mask.tobytes()).hexdigest() == g["mask_sha256"]
+    x = st.x_new
+    # x within 1e-12 normwise elementwise sums to within n * 1e-12 max|x|
+    assert abs(float(np.sum(x)) - g["x_sum"]) <= 1e-12 * x.size
+    assert abs(float(np.sum(x * x)) - g["x_sq"]) <= 3e-12 * x.size
     if g["path"] == "newton":
         if g["converged"]:
             assert pr.newton_iters == g["newton_iters"]
