@@ -280,6 +280,20 @@ int topt_b200_pgd_step_ranks(topt_b200_ctx* ctx, const topt_step_problem* prob,
                              const topt_pgd_settings* settings, const topt_proj_options* opts,
                              const topt_step_outputs* out, topt_proj_meta* meta);
 
+/* Single-process lockstep ranks: the same multi-rank data plane (per-rank
+ * pass kernels over element slabs, rank-order combine, replicated control)
+ * with the per-pass all-gather done as device-to-device copies instead of
+ * NCCL -- for one process driving several slabs (or GPUs), and to test the
+ * multi-rank code on one device.  Rank r's context comes from
+ * topt_b200_ctx_create_lockstep(device, r, world); probs / outs / metas are
+ * per-rank arrays (device pointers as for topt_b200_pgd_step_ranks). */
+int topt_b200_ctx_create_lockstep(int device, int rank, int world, topt_b200_ctx** out);
+int topt_b200_pgd_step_lockstep(int world, topt_b200_ctx* const* ctxs,
+                                const topt_step_problem* probs, int64_t n_global,
+                                const int64_t* row_counts, const topt_pgd_settings* settings,
+                                const topt_proj_options* opts, const topt_step_outputs* outs,
+                                topt_proj_meta* metas);
+
 /* spectral_step_size + cg_direction + rho_tilde only, host
  * buffers.  d_out = new direction, rho_tilde_out = x - omega*alpha*d. */
 int topt_b200_step_direction(topt_b200_ctx* ctx, int64_t n, const double* x,

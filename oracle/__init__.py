@@ -224,6 +224,87 @@ def enum_project(rho, grad, ghat, is_eq=None, lower=0.0, upper=1.0, tol=1e-10):
     return None if rc == 1 else (d, y)
 
 
+# ---- upstream of the step ------------------------
+
+def filter_csr(nx, ny, radius):
+    """oracle/upstream.c restatement of build_filter (filter.cpp:10-43)."""
+    L = lib()
+    L.orc_filter_csr.restype = C.c_int64
+    nnz = L.orc_filter_csr(C.c_int(nx), C.c_int(ny), C.c_double(radius), None, None, None)
+    rp = np.empty(nx * ny + 1, np.int32); col = np.empty(nnz, np.int32); w = np.empty(nnz)
+    L.orc_filter_csr(C.c_int(nx), C.c_int(ny), C.c_double(radius), _p(rp), _p(col), _p(w))
+    return rp, col, w
+
+
+def filter_apply(nx, ny, radius, x, transpose=False):
+    out = np.empty(nx * ny)
+    lib().orc_filter_apply(C.c_int(nx), C.c_int(ny), C.c_double(radius), C.c_int(int(transpose)),
+                           _p(_f64(x)), _p(out))
+    return out
+
+
+def interpolate(dens, n, young, e_min=1e-9, penalty=3.0):
+    k = len(young)
+    mod = np.empty(n); der = np.empty(n * k)
+    rc = lib().orc_interpolate(_i64(n), C.c_int(k), _p(_f64(young)), C.c_double(e_min),
+                               C.c_double(penalty), _p(_f64(dens)), _p(mod), _p(der))
+    if rc:
+        raise OracleError(2, "interpolate_stiffness: density outside [0,1]")
+    return mod, der
+
+
+def element_q4(poisson=0.3, h=1.0):
+    ke = np.empty(64)
+    lib().orc_element_q4(C.c_double(poisson), C.c_double(h), _p(ke))
+    return ke.reshape(8, 8)
+
+
+def energy_gradient(nx, ny, u, der, k=1, poisson=0.3, h=1.0):
+    n = nx * ny
+    e = np.empty(n); g = np.empty(n * k)
+    lib().orc_energy_gradient(C.c_int(nx), C.c_int(ny), C.c_double(h), C.c_double(poisson),
+                              _p(_f64(u)), C.c_int(k), _p(_f64(der)), _p(e), _p(g))
+    return e, g
+
+
+def ref_filter_csr(nx, ny, radius):
+    """The reference's own build_filter (oracle/_ref)."""
+    nnz = np.array([0], np.int64)
+    err = C.create_string_buffer(512)
+    rc = ref().ref_filter_csr(C.c_int(nx), C.c_int(ny), C.c_double(radius), None, None, None,
+                              _p(nnz), err, C.c_size_t(512))
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    rp = np.empty(nx * ny + 1, np.int32); col = np.empty(int(nnz[0]), np.int32)
+    w = np.empty(int(nnz[0]))
+    ref().ref_filter_csr(C.c_int(nx), C.c_int(ny), C.c_double(radius), _p(rp), _p(col), _p(w),
+                         _p(nnz), err, C.c_size_t(512))
+    return rp, col, w
+
+
+def ref_filter_apply(nx, ny, radius, x, transpose=False):
+    out = np.empty(nx * ny)
+    err = C.create_string_buffer(512)
+    rc = ref().ref_filter_apply(C.c_int(nx), C.c_int(ny), C.c_double(radius),
+                                C.c_int(int(transpose)), _p(_f64(x)), _p(out), err,
+                                C.c_size_t(512))
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    return out
+
+
+def ref_interpolate(dens, n, young, e_min=1e-9, poisson=0.3, penalty=3.0):
+    k = len(young)
+    mod = np.empty(n); der = np.empty(n * k)
+    err = C.create_string_buffer(512)
+    rc = ref().ref_interpolate(C.c_size_t(n), C.c_size_t(k), _p(_f64(young)), C.c_double(e_min),
+                               C.c_double(poisson), C.c_double(penalty), _p(_f64(dens)),
+                               _p(mod), _p(der), err, C.c_size_t(512))
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    return mod, der
+
+
 def random_instance(rng, n, m, feasible=True, eq_rows=0):
     """A random projection instance (rho_tilde, A, g_hat): rho in (-0.3, 1.3),
     rows ~ N(0, 1); feasible ones get g_hat = A (x0 - rho) + slack for a random

@@ -79,6 +79,11 @@ EXPORTS = [
     "topt_b200_debug_trace",
     "topt_b200_nccl_unique_id", "topt_b200_ctx_create_ranks", "topt_b200_pgd_step_ranks",
     "topt_b200_set_structured_rows", "topt_b200_set_parity", "topt_b200_get_parity",
+    "topt_b200_filter_create", "topt_b200_filter_destroy", "topt_b200_filter_nnz",
+    "topt_b200_filter_csr", "topt_b200_filter_apply", "topt_b200_filter_apply_dev",
+    "topt_b200_csr_apply", "topt_b200_interpolate_stiffness_dev",
+    "topt_b200_element_stiffness_q4", "topt_b200_compliance_gradient_dev",
+    "topt_b200_ctx_create_lockstep", "topt_b200_pgd_step_lockstep",
 ]
 
 _lib = None
@@ -128,11 +133,25 @@ def load():
         "topt_b200_default_settings": [vp],
         "topt_b200_set_parity": [vp, C.c_int],
         "topt_b200_get_parity": [vp],
+        "topt_b200_filter_create": [vp, i32, i32, d, C.POINTER(C.c_void_p)],
+        "topt_b200_filter_csr": [vp, vp, vp, vp],
+        "topt_b200_filter_apply": [vp, vp, C.c_int, vp, vp],
+        "topt_b200_filter_apply_dev": [vp, vp, C.c_int, vp, vp],
+        "topt_b200_csr_apply": [vp, i64, vp, vp, vp, C.c_int, vp, vp],
+        "topt_b200_interpolate_stiffness_dev": [vp, i64, i32, vp, d, d, d, vp, vp, vp],
+        "topt_b200_element_stiffness_q4": [d, d, vp],
+        "topt_b200_compliance_gradient_dev": [vp, i32, i32, d, d, vp, i32, vp, vp, vp],
+        "topt_b200_ctx_create_lockstep": [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)],
+        "topt_b200_pgd_step_lockstep": [C.c_int, vp, vp, i64, vp, vp, vp, vp, vp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
         f.argtypes = args
         f.restype = None if name.startswith("topt_b200_default") else C.c_int
+    lib.topt_b200_filter_destroy.argtypes = [vp]
+    lib.topt_b200_filter_destroy.restype = None
+    lib.topt_b200_filter_nnz.argtypes = [vp]
+    lib.topt_b200_filter_nnz.restype = C.c_int64
     _lib = lib
     return lib
 
@@ -166,10 +185,14 @@ class Context:
     """One CUDA device context of the library (stream, plan, workspaces).
     With rank/world/nccl_id it is one rank of a multi-GPU (NCCL) job."""
 
-    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes = None):
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes = None,
+                 lockstep: bool = False):
         self.lib = load()
         h = C.c_void_p()
-        if nccl_id is not None:
+        if lockstep:
+            rc = self.lib.topt_b200_ctx_create_lockstep(int(device), int(rank), int(world),
+                                                        C.byref(h))
+        elif nccl_id is not None:
             _preload_torch_nccl()
             idb = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
             rc = self.lib.topt_b200_ctx_create_ranks(int(device), int(rank), int(world), idb,
@@ -183,6 +206,7 @@ class Context:
         self.device = device
         self.rank, self.world = rank, world
         self.distributed = nccl_id is not None
+        self.lockstep = lockstep
 
     def close(self):
         if self.h:

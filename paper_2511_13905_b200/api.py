@@ -612,3 +612,268 @@ def prepare_pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_
         srows = (descs, grid, index_offset)
     return PreparedStep(ctx, fn, args, keep, m, outs, srows)
 
+
+
+# ---- upstream of the step: filter, SIMP, sensitivities ------
+@dataclasses.dataclass
+class StructuredGrid:
+    """grid.hpp:13-21: nx x ny unit-size (or element_size) square elements,
+    element e = ey * nx + ex."""
+    nx: int = 1
+    ny: int = 1
+    element_size: float = 1.0
+
+    def __post_init__(self):
+        if self.nx < 1 or self.ny < 1:
+            raise ParameterError("grid: nx and ny must be >= 1")
+        if not (self.element_size > 0.0):
+            raise ParameterError("grid: element_size must be > 0")
+
+    def num_elements(self) -> int:
+        return self.nx * self.ny
+
+    def num_dofs(self) -> int:
+        return 2 * (self.nx + 1) * (self.ny + 1)
+
+    def element_index(self, ex, ey) -> int:
+        return ey * self.nx + ex
+
+
+class FilterKernel:
+    """filter.hpp:15-25: the row-normalized hat kernel.  The CSR arrays are the
+    reference's (row_ptr, col, weight); the product runs matrix-free on the
+    GPU from (nx, ny, radius) when the kernel came from build_filter, and as
+    a CSR product otherwise -- both in the reference's summation orders."""
+
+    def __init__(self, size, radius, row_ptr, col, weight, grid=None, handle=None, ctx=None):
+        self.size, self.radius = int(size), float(radius)
+        self.row_ptr, self.col, self.weight = row_ptr, col, weight
+        self._grid, self._h, self._ctx = grid, handle, ctx
+
+    def is_identity(self) -> bool:
+        return len(self.col) == self.size
+
+    def __del__(self):
+        try:
+            if self._h:
+                self._ctx.lib.topt_b200_filter_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def build_filter(grid: StructuredGrid, radius: float, device: int = 0) -> FilterKernel:
+    """build_filter (filter.cpp:10-43)."""
+    if not (radius > 0.0):
+        raise ParameterError("build_filter: radius must be > 0")
+    ctx = L.context(device)
+    h = C.c_void_p()
+    _check(ctx, ctx.lib.topt_b200_filter_create(ctx.h, grid.nx, grid.ny, float(radius),
+                                                C.byref(h)))
+    n = grid.num_elements()
+    nnz = int(ctx.lib.topt_b200_filter_nnz(h))
+    rp = np.empty(n + 1, np.int32); col = np.empty(nnz, np.int32); w = np.empty(nnz)
+    _check(ctx, ctx.lib.topt_b200_filter_csr(h, _ptr(rp), _ptr(col), _ptr(w)))
+    return FilterKernel(n, radius, rp, col, w, grid, h, ctx)
+
+
+def _filter_product(kernel: FilterKernel, v, transpose: bool, what: str):
+    n = kernel.size
+    dev = _is_torch_cuda(v)
+    size = v.numel() if dev else np.asarray(v).size
+    if size != n:
+        raise DomainError(f"{what}: field size does not match kernel")
+    ctx = kernel._ctx or L.context(0)
+    if dev:
+        if kernel._h is None:
+            raise DomainError(f"{what}: device fields need a kernel from build_filter")
+        v = _dev_f64(v, what, n)
+        import torch
+        out = torch.empty_like(v)
+        _check(ctx, ctx.lib.topt_b200_filter_apply_dev(ctx.h, kernel._h, int(transpose),
+                                                       v.data_ptr(), out.data_ptr()))
+        return out
+    v = np.ascontiguousarray(v, np.float64)
+    out = np.empty(n)
+    if kernel._h is not None:
+        _check(ctx, ctx.lib.topt_b200_filter_apply(ctx.h, kernel._h, int(transpose), _ptr(v),
+                                                   _ptr(out)))
+    else:
+        rp = np.ascontiguousarray(kernel.row_ptr, np.int32)
+        col = np.ascontiguousarray(kernel.col, np.int32)
+        w = np.ascontiguousarray(kernel.weight, np.float64)
+        _check(ctx, ctx.lib.topt_b200_csr_apply(ctx.h, n, _ptr(rp), _ptr(col), _ptr(w),
+                                                int(transpose), _ptr(v), _ptr(out)))
+    return out
+
+
+def apply_filter(kernel: FilterKernel, raw):
+    """filtered = W raw (filter.cpp:45-56)."""
+    return _filter_product(kernel, raw, False, "apply_filter")
+
+
+def filter_chain_rule(kernel: FilterKernel, grad_wrt_filtered):
+    """W^T grad (filter.cpp:58-69)."""
+    return _filter_product(kernel, grad_wrt_filtered, True, "filter_chain_rule")
+
+
+@dataclasses.dataclass
+class MaterialModel:
+    """material.hpp:13-24 (SIMP)."""
+    young_moduli: Sequence[float] = (1.0,)
+    e_min: float = 1e-9
+    poisson: float = 0.3
+    penalty: float = 3.0
+
+    def num_materials(self) -> int:
+        return len(self.young_moduli)
+
+    def validate(self):   # material.cpp:9-17
+        if not len(self.young_moduli):
+            raise ParameterError("material: no young moduli")
+        if not (self.e_min > 0.0):
+            raise ParameterError("material: e_min must be > 0")
+        for e in self.young_moduli:
+            if not (e > self.e_min):
+                raise ParameterError("material: every E_j must exceed e_min")
+        if not (0.0 < self.poisson < 0.5):
+            raise ParameterError("material: poisson must lie in (0, 0.5)")
+        if not (self.penalty >= 1.0):
+            raise ParameterError("material: penalty must be >= 1")
+
+
+@dataclasses.dataclass
+class StiffnessInterpolation:
+    moduli: object       # N
+    derivative: object   # N*K channel-major
+
+
+def interpolate_stiffness(densities, num_elements: int, model: MaterialModel,
+                          device: int = 0) -> StiffnessInterpolation:
+    """interpolate_stiffness (material.cpp:19-46) on the GPU.  Host arrays are
+    copied in and out; torch CUDA tensors stay on the device."""
+    import torch
+    model.validate()
+    k = model.num_materials()
+    dev = _is_torch_cuda(densities)
+    d = (_dev_f64(densities, "densities") if dev
+         else torch.from_numpy(np.ascontiguousarray(densities, np.float64)).cuda(device))
+    if d.numel() != num_elements * k:
+        raise DomainError("interpolate_stiffness: density vector size mismatch")
+    ctx = L.context(device)
+    mod = torch.empty(num_elements, dtype=torch.float64, device=d.device)
+    der = torch.empty(num_elements * k, dtype=torch.float64, device=d.device)
+    young = np.ascontiguousarray(model.young_moduli, np.float64)
+    rc = ctx.lib.topt_b200_interpolate_stiffness_dev(
+        ctx.h, num_elements, k, _ptr(young), model.e_min, model.poisson, model.penalty,
+        d.data_ptr(), mod.data_ptr(), der.data_ptr())
+    if rc == L.ERR_DOMAIN:
+        raise DomainError("interpolate_stiffness: density outside [0,1]")
+    _check(ctx, rc)
+    torch.cuda.synchronize(d.device)
+    if dev:
+        return StiffnessInterpolation(mod, der)
+    return StiffnessInterpolation(mod.cpu().numpy(), der.cpu().numpy())
+
+
+def element_stiffness_q4(poisson: float, element_size: float) -> np.ndarray:
+    """element_stiffness_q4 (fea.cpp:20-58): the unit-modulus plane-stress Q4
+    element matrix (8 x 8)."""
+    lib = L.load()
+    ke = np.empty(64)
+    if lib.topt_b200_element_stiffness_q4(float(poisson), float(element_size), _ptr(ke)):
+        raise ParameterError("element_stiffness_q4: poisson must lie in (0, 0.5) and "
+                             "element_size > 0")
+    return ke.reshape(8, 8)
+
+
+def compliance_gradient(grid: StructuredGrid, displacement, derivative, model: MaterialModel,
+                        device: int = 0):
+    """Element energies u_e^T k0 u_e and the compliance gradient -dE * energy
+    (fea.cpp:162-181) from a displacement field (all 2 (nx+1)(ny+1) dofs) and
+    interpolate_stiffness's derivative.  Returns (energy, gradient)."""
+    import torch
+    k = model.num_materials()
+    n = grid.num_elements()
+    dev = _is_torch_cuda(displacement)
+    cu = (lambda a, nm, sz: _dev_f64(a, nm, sz)) if dev else \
+        (lambda a, nm, sz: torch.from_numpy(np.ascontiguousarray(a, np.float64)).cuda(device))
+    u = cu(displacement, "displacement", grid.num_dofs())
+    der = cu(derivative, "derivative", n * k)
+    if u.numel() != grid.num_dofs() or der.numel() != n * k:
+        raise DomainError("compliance_gradient: size mismatch")
+    ctx = L.context(device)
+    energy = torch.empty(n, dtype=torch.float64, device=u.device)
+    grad = torch.empty(n * k, dtype=torch.float64, device=u.device)
+    _check(ctx, ctx.lib.topt_b200_compliance_gradient_dev(
+        ctx.h, grid.nx, grid.ny, grid.element_size, model.poisson, u.data_ptr(), k,
+        der.data_ptr(), energy.data_ptr(), grad.data_ptr()))
+    torch.cuda.synchronize(u.device)
+    if dev:
+        return energy, grad
+    return energy.cpu().numpy(), grad.cpu().numpy()
+
+
+def pgd_step_lockstep(slabs, n_global: int, settings: PgdSettings = None, device: int = 0,
+                      row_counts=None):
+    """One PGD step over element slabs, one lockstep rank per slab in this
+    process (topt_b200_pgd_step_lockstep): the multi-rank data plane -- rank
+    slabs, per-rank pass kernels, rank-order combine of the exchanged totals,
+    replicated control -- with device copies instead of NCCL.  `slabs`: per
+    rank a dict of torch CUDA tensors x, x_prev, g, g_prev, d_prev, grad (m x
+    slab) and the shared g_values, bounds_g, is_equality, t, violation.
+    Returns per-rank StepResults."""
+    import torch
+    world = len(slabs)
+    settings = settings or PgdSettings()
+    ctxs = [L.Context(device, r, world, lockstep=True) for r in range(world)]
+    probs = (L.StepProblem * world)()
+    outs = (L.StepOutputs * world)()
+    metas = (L.ProjMeta * world)()
+    keep, res_bufs = [], []
+    for r, s in enumerate(slabs):
+        n = int(s["x"].numel())
+        m = int(len(s["g_values"]))
+        pr = probs[r]
+        pr.n, pr.m, pr.t, pr.violation = n, m, int(s.get("t", 1)), float(s.get("violation", 0.0))
+        pr.lower, pr.upper = float(s.get("lower", 0.0)), float(s.get("upper", 1.0))
+        arrs = {k: _dev_f64(s[k], k, n) for k in ("x", "x_prev", "g", "g_prev", "d_prev")}
+        arrs["grad"] = _dev_f64(s["grad"], "grad", m * n)
+        for k, a in arrs.items():
+            setattr(pr, k, a.data_ptr())
+        gv = np.ascontiguousarray(s["g_values"], np.float64)
+        bg = np.ascontiguousarray(s["bounds_g"], np.float64)
+        ie = (None if s.get("is_equality") is None
+              else np.ascontiguousarray(s["is_equality"], np.uint8))
+        pr.g_values, pr.bounds_g, pr.is_equality = _ptr(gv), _ptr(bg), _ptr(ie)
+        pr.part_offsets = pr.part_indices = pr.owner = None
+        b = {k: torch.empty(n, dtype=torch.float64, device=arrs["x"].device)
+             for k in ("x_new", "d", "rho_tilde")}
+        b.update(y=np.zeros(m), sl=np.zeros(m), gh=np.zeros(m))
+        o = outs[r]
+        o.x_new, o.d, o.rho_tilde = b["x_new"].data_ptr(), b["d"].data_ptr(), b["rho_tilde"].data_ptr()
+        o.delta = o.mask = None
+        o.y, o.slacks, o.g_hat = _ptr(b["y"]), _ptr(b["sl"]), _ptr(b["gh"])
+        keep += [arrs, gv, bg, ie]
+        res_bufs.append(b)
+    handles = (C.c_void_p * world)(*[c.h for c in ctxs])
+    rc_arr = None if row_counts is None else np.ascontiguousarray(row_counts, np.int64)
+    opts = settings.options()._c()
+    sc = settings._c()
+    rc = ctxs[0].lib.topt_b200_pgd_step_lockstep(world, handles, probs, int(n_global), _ptr(rc_arr),
+                                                 C.byref(sc), C.byref(opts), outs, metas)
+    if rc != L.OK:
+        msg = "; ".join(c.last_error() for c in ctxs if c.last_error())
+        raise _ERRMAP.get(rc, RuntimeError)(msg)
+    out = []
+    for r in range(world):
+        b, meta = res_bufs[r], metas[r]
+        m = len(b["y"])
+        proj = _meta_to_result(meta, None, b["y"].copy(), b["sl"].copy(), m)
+        out.append(StepResult(x_new=b["x_new"], d=b["d"], rho_tilde=b["rho_tilde"], delta=None,
+                              y=b["y"].copy(), slacks=b["sl"].copy(), g_hat=b["gh"].copy(),
+                              alpha=meta.alpha, beta=meta.beta, fallback=bool(meta.fallback),
+                              projection=proj))
+    for c in ctxs:
+        c.close()
+    return out

@@ -497,6 +497,9 @@ struct topt_b200_ctx {
   uint32_t epoch = 0;
   int stream_inputs = 1;           // TOPT_B200_STREAM=0 disables
   int parity = 0;                  // 0 certified, 1 strict (TOPT_B200_PARITY=strict)
+  int lockstep = 0;                // rank of a single-process lockstep job (no NCCL)
+  int defer = 0;                   // run_plan_ranks: prepare only (the lockstep driver)
+  cudaEvent_t ev_pass = nullptr, ev_copied = nullptr;
   int ex_debug = 0;
   const int32_t* last_pidx = nullptr;   // device partition indices of the last owner map
   int64_t last_poff[MAX_M + 1] = {};
@@ -690,7 +693,7 @@ void plan_results_take(topt_b200_ctx* ctx, Plan& hp) {
 }
 
 int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
-  if (ctx->comm) return run_plan_ranks(ctx, hp);
+  if (ctx->comm || ctx->lockstep) return run_plan_ranks(ctx, hp);
   const bool persistent = ctx->persistent && ctx->coop_grid > 0;
   const int grid = persistent ? ctx->coop_grid : ctx->grid;
   const int64_t per_thread = (hp.P.n + (int64_t)grid * BLOCK - 1) / ((int64_t)grid * BLOCK);
@@ -816,7 +819,10 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
 // combines them in rank order and runs the controller -- identical decisions
 // everywhere, no host arithmetic.  The host only sequences the launches and
 // polls the next phase.
-int run_plan_ranks(topt_b200_ctx* ctx, Plan& hp) {
+constexpr int TOPT_DEFERRED = 100;   // internal: plan prepared, passes driven by the caller
+constexpr int RANK_BATCH = 4;        // passes enqueued per host synchronization (rank mode)
+
+int ranks_setup(topt_b200_ctx* ctx, Plan& hp) {
   if (hp.P.strict)   // a reference-order sum is sequential across the ranks' slabs
     return fail(ctx, TOPT_ERR_UNSUPPORTED, "strict parity is single-GPU only");
   const int grid = ctx->grid;
@@ -824,22 +830,56 @@ int run_plan_ranks(topt_b200_ctx* ctx, Plan& hp) {
   hp.P.ours_len = 2.0 * (double)per_thread + (double)grid + 64.0 + (double)ctx->world;
   hp.P.compact_cap = 0;
   plan_start(hp);
-  if (int rc = plan_upload(ctx, hp)) return rc;
+  return plan_upload(ctx, hp);
+}
+
+int ranks_pass_kernel(topt_b200_ctx* ctx, const Plan& hp) {
+  k_pass<<<ctx->grid, BLOCK, KPASS_SMEM + sizeof(double) * (size_t)hp.P.n_tab, ctx->stream>>>(
+      ctx->d_plan, ctx->d_part, ctx->d_counter, ctx->d_rank_tot);
+  ctx->launches++;
+  CUDA_TRY(ctx, cudaGetLastError());
+  return TOPT_OK;
+}
+
+int ranks_control_kernel(topt_b200_ctx* ctx) {
+  k_control<<<1, BLOCK, sizeof(Plan), ctx->stream>>>(ctx->d_plan, ctx->d_gathered, ctx->world);
+  ctx->launches++;
+  CUDA_TRY(ctx, cudaGetLastError());
+  return TOPT_OK;
+}
+
+int ranks_finish(topt_b200_ctx* ctx, Plan& hp, int phase) {
+  if (int rc = plan_results_async(ctx)) return rc;
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  plan_results_take(ctx, hp);
+  if (phase != PH_DONE) return fail(ctx, TOPT_ERR_INTERNAL, "plan did not terminate");
+  if (hp.res.status != ST_OK) return fail(ctx, hp.res.status, status_msg(hp.res.status));
+  return TOPT_OK;
+}
+
+// Multi-rank over NCCL: per pass every rank reduces its slab's partials on
+// its GPU (k_pass), the rank totals are all-gathered (NVLink), and every rank
+// combines them in rank order and runs the controller (k_control) --
+// identical decisions everywhere, no host arithmetic.  Passes are enqueued
+// RANK_BATCH at a time between host reads of the phase: a pass after the
+// last one is a no-op (k_pass / k_control return at PH_DONE, the all-gather
+// moves stale bytes), and every rank enqueues the same count.
+int run_plan_ranks(topt_b200_ctx* ctx, Plan& hp) {
+  if (int rc = ranks_setup(ctx, hp)) return rc;
+  if (ctx->defer) return TOPT_DEFERRED;
   int phase = hp.cmd.phase;
   NcclApi& api = nccl();
-  for (int it = 0; phase != PH_DONE && it < 4096; ++it) {
+  for (int it = 0; phase != PH_DONE && it < 4096; it += RANK_BATCH) {
     if (ctx->profile) cudaEventRecord(ctx->ev0, ctx->stream);
-    k_pass<<<grid, BLOCK, KPASS_SMEM + sizeof(double) * (size_t)hp.P.n_tab, ctx->stream>>>(ctx->d_plan, ctx->d_part, ctx->d_counter,
-                                                       ctx->d_rank_tot);
-    CUDA_TRY(ctx, cudaGetLastError());
-    const ncclResult_t nr = api.AllGather(ctx->d_rank_tot, ctx->d_gathered, PMAX, ncclDouble,
-                                          (ncclComm_t)ctx->comm, ctx->stream);
-    if (nr != ncclSuccess)
-      return fail(ctx, TOPT_ERR_CUDA, std::string("ncclAllGather: ") +
-                                          (api.GetErrorString ? api.GetErrorString(nr) : "?"));
-    k_control<<<1, BLOCK, sizeof(Plan), ctx->stream>>>(ctx->d_plan, ctx->d_gathered, ctx->world);
-    ctx->launches += 2;
-    CUDA_TRY(ctx, cudaGetLastError());
+    for (int b = 0; b < RANK_BATCH; ++b) {
+      if (int rc = ranks_pass_kernel(ctx, hp)) return rc;
+      const ncclResult_t nr = api.AllGather(ctx->d_rank_tot, ctx->d_gathered, PMAX, ncclDouble,
+                                            (ncclComm_t)ctx->comm, ctx->stream);
+      if (nr != ncclSuccess)
+        return fail(ctx, TOPT_ERR_CUDA, std::string("ncclAllGather: ") +
+                                            (api.GetErrorString ? api.GetErrorString(nr) : "?"));
+      if (int rc = ranks_control_kernel(ctx)) return rc;
+    }
     if (ctx->profile) cudaEventRecord(ctx->ev1, ctx->stream);
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_phase, &ctx->d_plan->cmd.phase, sizeof(int),
                                   cudaMemcpyDeviceToHost, ctx->stream));
@@ -849,17 +889,11 @@ int run_plan_ranks(topt_b200_ctx* ctx, Plan& hp) {
       cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
       ctx->prof_ms += ms;
       ctx->prof_max = std::max(ctx->prof_max, (double)ms);
-      ctx->prof_n++;
+      ctx->prof_n += RANK_BATCH;
     }
     phase = *ctx->h_phase;
-    if (getenv("TOPT_B200_DEBUG_PHASES") && it < 64) fprintf(stderr, "[topt] pass %d -> phase %d\n", it, phase);
   }
-  if (int rc = plan_results_async(ctx)) return rc;
-  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  plan_results_take(ctx, hp);
-  if (phase != PH_DONE) return fail(ctx, TOPT_ERR_INTERNAL, "plan did not terminate");
-  if (hp.res.status != ST_OK) return fail(ctx, hp.res.status, status_msg(hp.res.status));
-  return TOPT_OK;
+  return ranks_finish(ctx, hp, phase);
 }
 
 void fill_meta(const Plan& hp, topt_proj_meta* meta) {
@@ -1202,6 +1236,8 @@ void topt_b200_ctx_destroy(topt_b200_ctx* ctx) {
   if (ctx->h_timed_out) cudaFreeHost(ctx->h_timed_out);
   if (ctx->hp_pin) cudaFreeHost(ctx->hp_pin);
   if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
+  if (ctx->ev_pass) cudaEventDestroy(ctx->ev_pass);
+  if (ctx->ev_copied) cudaEventDestroy(ctx->ev_copied);
   if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -1560,7 +1596,8 @@ int topt_b200_pgd_step_ranks(topt_b200_ctx* ctx, const topt_step_problem* prob,
                              int64_t n_global, const int64_t* row_counts,
                              const topt_pgd_settings* settings, const topt_proj_options* opts,
                              const topt_step_outputs* out, topt_proj_meta* meta) {
-  if (!ctx->comm) return fail(ctx, TOPT_ERR_PARAMETER, "context has no NCCL communicator");
+  if (!ctx->comm && !ctx->lockstep)
+    return fail(ctx, TOPT_ERR_PARAMETER, "context has no NCCL communicator");
   ctx->n_global_override = n_global;
   ctx->row_counts_override = row_counts;
   const int rc = topt_b200_pgd_step_dev(ctx, prob, settings, opts, out, meta);
@@ -1754,6 +1791,96 @@ int topt_b200_step_direction(topt_b200_ctx* ctx, int64_t n, const double* x,
   if (alpha_out) *alpha_out = hp.res.alpha;
   if (beta_out) *beta_out = hp.res.beta;
   if (fallback_out) *fallback_out = hp.res.fallback;
+  return TOPT_OK;
+}
+
+// ---- single-process lockstep ranks (the multi-rank data plane without NCCL) ----
+int topt_b200_ctx_create_lockstep(int device, int rank, int world, topt_b200_ctx** out) {
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) return TOPT_ERR_PARAMETER;
+  topt_b200_ctx* ctx = nullptr;
+  int rc = topt_b200_ctx_create(device, &ctx);
+  if (rc) return rc;
+  ctx->rank = rank;
+  ctx->world = world;
+  ctx->lockstep = 1;
+  bool ok = cudaMalloc(&ctx->d_rank_tot, sizeof(double) * PMAX) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->d_gathered, sizeof(double) * PMAX * world) == cudaSuccess;
+  ok = ok && cudaMemset(ctx->d_rank_tot, 0, sizeof(double) * PMAX) == cudaSuccess;
+  ok = ok && cudaEventCreateWithFlags(&ctx->ev_pass, cudaEventDisableTiming) == cudaSuccess;
+  ok = ok && cudaEventCreateWithFlags(&ctx->ev_copied, cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) { topt_b200_ctx_destroy(ctx); return TOPT_ERR_CUDA; }
+  *out = ctx;
+  return TOPT_OK;
+}
+
+int topt_b200_pgd_step_lockstep(int world, topt_b200_ctx* const* ctxs,
+                                const topt_step_problem* probs, int64_t n_global,
+                                const int64_t* row_counts, const topt_pgd_settings* settings,
+                                const topt_proj_options* opts, const topt_step_outputs* outs,
+                                topt_proj_meta* metas) {
+  if (world < 1 || !ctxs) return TOPT_ERR_PARAMETER;
+  for (int r = 0; r < world; ++r)
+    if (!ctxs[r] || !ctxs[r]->lockstep || ctxs[r]->rank != r || ctxs[r]->world != world)
+      return TOPT_ERR_PARAMETER;
+  // every rank's plan: the ranks entry prepares it and stops before the passes
+  for (int r = 0; r < world; ++r) {
+    topt_b200_ctx* c = ctxs[r];
+    c->defer = 1;
+    const int rc = topt_b200_pgd_step_ranks(c, &probs[r], n_global, row_counts, settings, opts,
+                                            &outs[r], metas ? &metas[r] : nullptr);
+    c->defer = 0;
+    if (rc != TOPT_DEFERRED) return rc ? rc : TOPT_ERR_INTERNAL;
+  }
+  int phase = ctxs[0]->h_plan.cmd.phase;
+  for (int it = 0; phase != PH_DONE && it < 4096; it += RANK_BATCH) {
+    for (int b = 0; b < RANK_BATCH; ++b) {
+      for (int q = 0; q < world; ++q) {   // pass kernels (after last pass's copies of q's totals)
+        topt_b200_ctx* c = ctxs[q];
+        cudaSetDevice(c->device);
+        if (it + b > 0)
+          for (int r = 0; r < world; ++r) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, ctxs[r]->ev_copied, 0));
+        if (int rc = ranks_pass_kernel(c, c->h_plan)) return rc;
+        CUDA_TRY(c, cudaEventRecord(c->ev_pass, c->stream));
+      }
+      for (int r = 0; r < world; ++r) {   // the all-gather, as device copies
+        topt_b200_ctx* c = ctxs[r];
+        cudaSetDevice(c->device);
+        for (int q = 0; q < world; ++q) {
+          CUDA_TRY(c, cudaStreamWaitEvent(c->stream, ctxs[q]->ev_pass, 0));
+          CUDA_TRY(c, cudaMemcpyPeerAsync(c->d_gathered + (size_t)q * PMAX, c->device,
+                                          ctxs[q]->d_rank_tot, ctxs[q]->device,
+                                          sizeof(double) * PMAX, c->stream));
+        }
+        CUDA_TRY(c, cudaEventRecord(c->ev_copied, c->stream));
+        if (int rc = ranks_control_kernel(c)) return rc;
+      }
+    }
+    int ph0 = -1;
+    for (int r = 0; r < world; ++r) {
+      topt_b200_ctx* c = ctxs[r];
+      cudaSetDevice(c->device);
+      CUDA_TRY(c, cudaMemcpyAsync(c->h_phase, &c->d_plan->cmd.phase, sizeof(int),
+                                  cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      if (r == 0) ph0 = *c->h_phase;
+      else if (*c->h_phase != ph0)
+        return fail(c, TOPT_ERR_INTERNAL, "lockstep ranks diverged");
+    }
+    phase = ph0;
+  }
+  for (int r = 0; r < world; ++r) {
+    topt_b200_ctx* c = ctxs[r];
+    cudaSetDevice(c->device);
+    Plan& hp = c->h_plan;
+    if (int rc = ranks_finish(c, hp, phase)) return rc;
+    for (int j = 0; j < hp.P.m; ++j) {
+      if (outs[r].y) outs[r].y[j] = hp.res.y[j];
+      if (outs[r].slacks) outs[r].slacks[j] = hp.res.slacks[j];
+      if (outs[r].g_hat) outs[r].g_hat[j] = hp.res.ghat[j];
+    }
+    if (metas) fill_meta(hp, &metas[r]);
+  }
   return TOPT_OK;
 }
 

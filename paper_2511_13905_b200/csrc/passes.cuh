@@ -1033,17 +1033,17 @@ __device__ __forceinline__ void sweep_elem(double a, double r, const double* y, 
   const bool pos = a > 0.0;
   const double bl = pos ? b1 : b2, bh = pos ? b2 : b1;
   const double cl = a * (pos ? lo : hi), ch = a * (pos ? hi : lo), aa = a * a;
-  int p1 = 0, p2 = 0;   // p1 = #{y_k < bl}, p2 = #{y_k <= bh}
-#pragma unroll
-  for (int s = (KC >= 16 ? 16 : pow2_at_least(KC)); s > 0; s >>= 1) {
-    if (p1 + s <= cnt && y[p1 + s - 1] < bl) p1 += s;
-    if (p2 + s <= cnt && y[p2 + s - 1] <= bh) p2 += s;
-  }
+  // the candidates are ascending: k < p1 = #{y_k < bl} below the free window,
+  // k >= p2 = #{y_k <= bh} above it -- one compare pair per candidate
+  // (independent, no search chain through shared memory)
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
-    C[k] += (k < p1) ? cl : ((k >= p2) ? ch : 0.0);
-    S[k] += (k >= p1 && k < p2) ? aa : 0.0;
+    const double yk = y[k];
+    const bool below = yk < bl, above = !(yk <= bh);
+    C[k] += below ? cl : (above ? ch : 0.0);
+    S[k] += (below || above) ? 0.0 : aa;
   }
+  (void)cnt;
 }
 
 // Most elements have no candidate inside their free window [bl, bh] (p1 ==
@@ -1058,6 +1058,7 @@ struct SweepAcc {
   double C[KC], S[KC];
   double Sall;   // slopes of elements free at every candidate (p1 = 0, p2 = cnt)
   double Clo, Chi;   // constants of elements clipped alike at every candidate
+  double y0, yl;     // the row's first and last candidate
   double* qa;    // this warp's queue (shared memory, SQ_CAP entries)
   double* qr;
   int qn;
@@ -1070,6 +1071,7 @@ struct SweepAcc {
     for (int k = 0; k < KC; ++k) { C[k] = 0.0; S[k] = 0.0; }
     Sall = 0.0; Clo = 0.0; Chi = 0.0;
     qa = qa_; qr = qr_; qn = 0; y = y_; cnt = cnt_; L = L_; U = U_;
+    y0 = y_[0]; yl = y_[cnt_ - 1];
   }
   // all 32 lanes call push together (valid = this lane holds an element)
   __device__ __forceinline__ void push(bool valid, double a, double r) {
@@ -1081,13 +1083,19 @@ struct SweepAcc {
       const double b1 = lo * ra, b2 = hi * ra;
       const bool pos = a > 0.0;
       const double bl = pos ? b1 : b2, bh = pos ? b2 : b1;
+      // window endpoints decide most elements without a search: both
+      // breakpoints outside (y_0, y_last] means p1, p2 in {0, cnt}
+      const bool outl = bl <= y0 || bl > yl, outh = bh < y0 || bh >= yl;
       int p1 = 0, p2 = 0;
-#pragma unroll
-      for (int s = (KC >= 16 ? 16 : pow2_at_least(KC)); s > 0; s >>= 1) {
-        if (p1 + s <= cnt && y[p1 + s - 1] < bl) p1 += s;
-        if (p2 + s <= cnt && y[p2 + s - 1] <= bh) p2 += s;
+      if (outl && outh) {
+        p1 = bl > yl ? cnt : 0;
+        p2 = bh >= yl ? cnt : 0;
+      } else {
+        p1 = -1;   // a breakpoint inside the window: the full per-candidate loop
       }
-      if (p1 == p2) {
+      if (p1 < 0) {
+        need = true;
+      } else if (p1 == p2) {
         const double cl = a * (pos ? lo : hi), ch = a * (pos ? hi : lo);
         // the walk window is narrow after the first sweep: nearly every
         // element is clipped alike at every candidate -- one sum, added to
@@ -1946,7 +1954,9 @@ __device__ __noinline__ void pass_newton_pat7(const PassCtx& c) {
   for (int k = 0; k < NB; ++k) h[k] = 0.0;
 #pragma unroll
   for (int k = 0; k < NB * (NB + 1) / 2; ++k) G[k] = 0.0;
-  const volatile double* ys = cmd.y;
+  double ys[M];   // duals in registers (14 of the 28 doubles the dense kernel keeps)
+#pragma unroll
+  for (int k = 0; k < M; ++k) ys[k] = cmd.y[k];
   const double2* __restrict__ R2 = reinterpret_cast<const double2*>(P.rho);
   const double2* __restrict__ A2 = reinterpret_cast<const double2*>(P.grad);
   const int64_t n2 = P.n >> 1, st = c.stride, ld2 = P.ld >> 1;
@@ -2019,10 +2029,15 @@ __device__ __noinline__ void pass_feas_pat7(const PassCtx& c) {
   const int64_t n2 = P.n >> 1, st = c.stride, ld2 = P.ld >> 1;
   const double2* __restrict__ R2 = reinterpret_cast<const double2*>(P.rho);
   const double2* __restrict__ A2 = reinterpret_cast<const double2*>(P.grad);
-  const volatile int* frow = cmd.feas_row;
-  const volatile double* fy = cmd.feas_y;
   for (int f0 = 0; f0 < cmd.nfeas; f0 += FEAS_GROUP) {
     const int ng = cmd.nfeas - f0 < FEAS_GROUP ? cmd.nfeas - f0 : FEAS_GROUP;
+    int frow[FEAS_GROUP];     // the group's candidates in registers
+    double fy[FEAS_GROUP];
+#pragma unroll
+    for (int g = 0; g < FEAS_GROUP; ++g) {
+      frow[g] = g < ng ? cmd.feas_row[f0 + g] : -1;
+      fy[g] = g < ng ? cmd.feas_y[f0 + g] : 0.0;
+    }
     double acc[FEAS_GROUP][NB];
 #pragma unroll
     for (int g = 0; g < FEAS_GROUP; ++g)
@@ -2034,8 +2049,8 @@ __device__ __noinline__ void pass_feas_pat7(const PassCtx& c) {
       const double lo = L - r, hi = U - r;
 #pragma unroll
       for (int g = 0; g < FEAS_GROUP; ++g) {
-        const int rj = g < ng ? frow[f0 + g] : -1;
-        const double yj = g < ng ? fy[f0 + g] : 0.0;
+        const int rj = frow[g];
+        const double yj = fy[g];
         double z = 0.0;
         if (rj >= 0 && yj != 0.0) {
           double arj = 0.0;
