@@ -657,7 +657,9 @@ __device__ __forceinline__ void prep_group(const PassCtx& c, int j0, int64_t n, 
     if (!detect || r == 0) A[r].v[PS_NNEG] = 1.0;
     if (detect && c.i0 == 0) A[r].v[PS_AREF] = aref[r];
   }
-  constexpr int UP = 2;   // pairs in flight per thread
+  // pairs in flight per thread: enough bytes per SM to cover HBM latency
+  // (Little's law) without spilling the G rows' accumulators
+  constexpr int UP = G == 1 ? 3 : 2;
   for (int64_t qb = c.i0 - lane; qb < n2; qb += UP * st) {   // warp-uniform trip count
     double2 a2[UP][G], r2[UP], d2[UP];
     const double2 z2 = make_double2(0.0, 0.0);
@@ -2262,14 +2264,17 @@ __device__ __noinline__ void pass_final_m(const PassCtx& c) {
         }
       };
       int64_t q = c.i0;
-      for (; q + st < n2; q += 2 * st) {   // two pairs' loads in flight per thread
-        double2 r2, r3, a2[M], a3[M];
-        load(q, r2, a2);
-        load(q + st, r3, a3);
-        finish(q, r2, a2);
-        finish(q + st, r3, a3);
-      }
-      if (q < n2) {
+      // two pairs' loads in flight per thread where the registers allow it
+      // (m = 7 / 8 would spill: pass_final_pat7 covers the C4/C5 layout)
+      if (M <= 4)
+        for (; q + st < n2; q += 2 * st) {
+          double2 r2, r3, a2[M], a3[M];
+          load(q, r2, a2);
+          load(q + st, r3, a3);
+          finish(q, r2, a2);
+          finish(q + st, r3, a3);
+        }
+      for (; q < n2; q += st) {
         double2 r2, a2[M];
         load(q, r2, a2);
         finish(q, r2, a2);
@@ -2316,6 +2321,76 @@ __device__ __noinline__ void pass_final_m(const PassCtx& c) {
     }
   }
   if (resid) block_reduce_store<M>(acc, m, PH_FINAL, 0, c.out, c.smem);
+}
+
+// FINAL for the P.pat7 layout (see pass_newton_pat7): rho and rows 1, 3, 5
+// (the rows of the dual's non-zero entries only, unless residuals are
+// wanted); x_{t+1} / delta / mask as 16-byte pairs, two pairs in flight.
+__device__ __noinline__ void pass_final_pat7(const PassCtx& c) {
+  constexpr int M = 7;
+  const Plan& pl = *c.plan;
+  const Problem& P = pl.P;
+  const Cmd& cmd = *c.cmd;
+  const double L = P.lower, Up = P.upper;
+  const double a0 = P.alias_c[0];
+  const int64_t n2 = P.n >> 1, st = c.stride, ld2 = P.ld >> 1;
+  const double2* __restrict__ R2 = reinterpret_cast<const double2*>(P.rho);
+  const double2* __restrict__ A2 = reinterpret_cast<const double2*>(P.grad);
+  double2* __restrict__ DO = cmd.write_delta ? reinterpret_cast<double2*>(P.delta_out) : nullptr;
+  double2* __restrict__ XO = cmd.write_x ? reinterpret_cast<double2*>(P.x_out) : nullptr;
+  uchar2* __restrict__ MO = cmd.write_mask ? reinterpret_cast<uchar2*>(P.mask_out) : nullptr;
+  const bool resid = cmd.resid_rows;
+  double yv[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) yv[k] = cmd.y[k];
+  // base rows 1, 3, 5 are read when their pair has a non-zero dual
+  const bool nu = resid || yv[1] != 0.0 || yv[2] != 0.0;
+  const bool nv = resid || yv[3] != 0.0 || yv[4] != 0.0;
+  const bool nw = resid || yv[5] != 0.0 || yv[6] != 0.0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  auto one = [&](double r, double u, double v, double w, bool& below, bool& above) {
+    const double a[M] = {a0, u, -u, v, -v, w, -w};
+    double z = 0.0;
+#pragma unroll
+    for (int k = 0; k < M; ++k)
+      if (yv[k] != 0.0) z += yv[k] * a[k];
+    const double lo = L - r, hi = Up - r;
+    below = z < lo; above = z > hi;
+    const double dl = below ? lo : (above ? hi : z);
+    if (resid) {
+      acc[0] += a0 * dl; acc[1] += u * dl; acc[2] += v * dl; acc[3] += w * dl;
+    }
+    return dl;
+  };
+  auto put = [&](int64_t q, double2 r2, double2 u2, double2 v2, double2 w2) {
+    bool b0, o0, b1, o1;
+    const double d0 = one(r2.x, u2.x, v2.x, w2.x, b0, o0);
+    const double d1 = one(r2.y, u2.y, v2.y, w2.y, b1, o1);
+    if (DO) DO[q] = make_double2(d0, d1);
+    if (XO) XO[q] = make_double2(r2.x + d0, r2.y + d1);
+    if (MO) {
+      uchar2 mk;
+      mk.x = b0 ? 1 : (o0 ? 2 : 0);
+      mk.y = b1 ? 1 : (o1 ? 2 : 0);
+      MO[q] = mk;
+    }
+  };
+  const double2 z2 = make_double2(0.0, 0.0);
+  int64_t q = c.i0;
+  for (; q + st < n2; q += 2 * st) {
+    const double2 r2 = R2[q], r3 = R2[q + st];
+    const double2 u2 = nu ? A2[ld2 + q] : z2, u3 = nu ? A2[ld2 + q + st] : z2;
+    const double2 v2 = nv ? A2[3 * ld2 + q] : z2, v3 = nv ? A2[3 * ld2 + q + st] : z2;
+    const double2 w2 = nw ? A2[5 * ld2 + q] : z2, w3 = nw ? A2[5 * ld2 + q + st] : z2;
+    put(q, r2, u2, v2, w2);
+    put(q + st, r3, u3, v3, w3);
+  }
+  if (q < n2)
+    put(q, R2[q], nu ? A2[ld2 + q] : z2, nv ? A2[3 * ld2 + q] : z2, nw ? A2[5 * ld2 + q] : z2);
+  if (resid) {
+    double vv[M] = {acc[0], acc[1], -acc[1], acc[2], -acc[2], acc[3], -acc[3]};
+    block_reduce_store<M>(vv, M, PH_FINAL, 0, c.out, c.smem);
+  }
 }
 
 // FINAL for a contiguous-range partition: row j's range as 16-byte pairs
@@ -2392,7 +2467,16 @@ __device__ void pass_final(const PassCtx& c) {
   const int m = c.plan->P.m;
   const bool own = c.plan->P.owner != nullptr;
   if (own && c.plan->P.part_ranges) { pass_final_ranges(c); return; }
-  if (!own && m == 7) { pass_final_m<7, false>(c); return; }
+  if (!own && m == 7) {
+    const Problem& P = c.plan->P;
+    if (P.pat7 && (P.n & 1) == 0 && (P.ld & 1) == 0 && al16(P.rho) && al16(P.grad) &&
+        (!c.cmd->write_delta || al16(P.delta_out)) && (!c.cmd->write_x || al16(P.x_out)) &&
+        (!c.cmd->write_mask || (reinterpret_cast<uintptr_t>(P.mask_out) & 1u) == 0))
+      pass_final_pat7(c);
+    else
+      pass_final_m<7, false>(c);
+    return;
+  }
   if (own) {
     if (m <= 4) pass_final_m<4, true>(c);
     else if (m <= 8) pass_final_m<8, true>(c);

