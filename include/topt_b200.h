@@ -344,6 +344,20 @@ int topt_b200_compliance_gradient_dev(topt_b200_ctx* ctx, int32_t nx, int32_t ny
                                       int32_t kmat, const double* der_dev, double* energy_dev,
                                       double* grad_dev);
 
+/* FE solve (assemble_and_solve, fea.cpp:60-144):
+ * plane-stress Q4 elasticity on an nx x ny grid with element moduli E (device,
+ * nx ny), fixed dofs and point loads (host lists, BoundaryConditions of
+ * grid.hpp:36-41, validated as grid.cpp:26-38), solved matrix-free by Jacobi-
+ * preconditioned CG to ||K u - f|| / ||f|| <= rel_tol in at most 10 N_free
+ * iterations (the reference's Eigen ConjugateGradient settings).  u_dev: all
+ * 2 (nx+1)(ny+1) dofs, fixed ones 0.  Status: bad BCs -> TOPT_ERR_PARAMETER,
+ * no convergence -> TOPT_ERR_SINGULAR (SingularSystemError). */
+int topt_b200_fe_solve_dev(topt_b200_ctx* ctx, int32_t nx, int32_t ny, double element_size,
+                           double poisson, const double* moduli_dev, const int32_t* fixed_dofs,
+                           int64_t n_fixed, const int32_t* load_dofs, const double* load_values,
+                           int64_t n_loads, double rel_tol, double* u_dev, int64_t* iterations,
+                           double* residual);
+
 #ifdef __cplusplus
 }
 #endif

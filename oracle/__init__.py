@@ -305,6 +305,50 @@ def ref_interpolate(dens, n, young, e_min=1e-9, poisson=0.3, penalty=3.0):
     return mod, der
 
 
+def fe_system(nx, ny, moduli, fixed, loads, poisson=0.3, h=1.0):
+    """assemble_and_solve's free-dof system (fea.cpp:60-104) restated with
+    scipy.sparse: triplets E_e k0[i][j] over free dofs, summed duplicates;
+    the right-hand side from the point loads.  Returns (K_free, f_free,
+    free_dof_index)."""
+    import scipy.sparse as sp
+    nd = 2 * (nx + 1) * (ny + 1)
+    fixed_mask = np.zeros(nd, bool)
+    fixed_mask[np.asarray(fixed, np.int64)] = True
+    dof_map = -np.ones(nd, np.int64)
+    free = np.nonzero(~fixed_mask)[0]
+    dof_map[free] = np.arange(free.size)
+    ke = element_q4(poisson, h)
+    rows, cols, vals = [], [], []
+    for e in range(nx * ny):
+        ex, ey = e % nx, e // nx
+        n1 = ey * (nx + 1) + ex; n2 = n1 + 1; n3 = (ey + 1) * (nx + 1) + ex + 1; n4 = n3 - 1
+        dofs = [2 * n1, 2 * n1 + 1, 2 * n2, 2 * n2 + 1, 2 * n3, 2 * n3 + 1, 2 * n4, 2 * n4 + 1]
+        gi = dof_map[dofs]
+        for i in range(8):
+            if gi[i] < 0:
+                continue
+            for j in range(8):
+                if gi[j] < 0:
+                    continue
+                rows.append(gi[i]); cols.append(gi[j]); vals.append(moduli[e] * ke[i, j])
+    K = sp.csr_matrix((vals, (rows, cols)), shape=(free.size, free.size))
+    f = np.zeros(free.size)
+    for dof, val in loads.items():
+        if dof_map[dof] >= 0:
+            f[dof_map[dof]] += val
+    return K, f, free
+
+
+def fe_solve(nx, ny, moduli, fixed, loads, poisson=0.3, h=1.0):
+    """Direct sparse solve of the reference's free-dof system (the oracle for
+    the GPU's iterative solve): u on all dofs, fixed ones 0."""
+    import scipy.sparse.linalg as sla
+    K, f, free = fe_system(nx, ny, moduli, fixed, loads, poisson, h)
+    u = np.zeros(2 * (nx + 1) * (ny + 1))
+    u[free] = sla.spsolve(K.tocsc(), f)
+    return u
+
+
 def random_instance(rng, n, m, feasible=True, eq_rows=0):
     """A random projection instance (rho_tilde, A, g_hat): rho in (-0.3, 1.3),
     rows ~ N(0, 1); feasible ones get g_hat = A (x0 - rho) + slack for a random

@@ -83,7 +83,7 @@ EXPORTS = [
     "topt_b200_filter_csr", "topt_b200_filter_apply", "topt_b200_filter_apply_dev",
     "topt_b200_csr_apply", "topt_b200_interpolate_stiffness_dev",
     "topt_b200_element_stiffness_q4", "topt_b200_compliance_gradient_dev",
-    "topt_b200_ctx_create_lockstep", "topt_b200_pgd_step_lockstep",
+    "topt_b200_ctx_create_lockstep", "topt_b200_pgd_step_lockstep", "topt_b200_fe_solve_dev",
 ]
 
 _lib = None
@@ -143,6 +143,7 @@ def load():
         "topt_b200_compliance_gradient_dev": [vp, i32, i32, d, d, vp, i32, vp, vp, vp],
         "topt_b200_ctx_create_lockstep": [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)],
         "topt_b200_pgd_step_lockstep": [C.c_int, vp, vp, i64, vp, vp, vp, vp, vp],
+        "topt_b200_fe_solve_dev": [vp, i32, i32, d, d, vp, vp, i64, vp, vp, i64, d, vp, vp, vp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

@@ -877,3 +877,104 @@ def pgd_step_lockstep(slabs, n_global: int, settings: PgdSettings = None, device
     for c in ctxs:
         c.close()
     return out
+
+
+# ---- FE solve and compliance sensitivities (fea.hpp:14-54, grid.hpp:36-45) -----
+@dataclasses.dataclass
+class BoundaryConditions:
+    """grid.hpp:36-41: fixed dofs (sorted, unique) and point loads {dof: force}."""
+    fixed_dofs: Sequence[int] = ()
+    loads: dict = dataclasses.field(default_factory=dict)
+
+
+def cantilever_bc(grid: StructuredGrid, load_magnitude: float = 1.0) -> BoundaryConditions:
+    """grid.cpp:40-51: left edge clamped, downward unit load at the midpoint of
+    the right edge (iy = ny / 2, rounded down)."""
+    fixed = []
+    for iy in range(grid.ny + 1):
+        nd = iy * (grid.nx + 1)
+        fixed += [2 * nd, 2 * nd + 1]
+    tip = (grid.ny // 2) * (grid.nx + 1) + grid.nx
+    return BoundaryConditions(sorted(fixed), {2 * tip + 1: -load_magnitude})
+
+
+@dataclasses.dataclass
+class SolveOptions:
+    """fea.hpp:20-25.  The GPU solve is always the matrix-free PCG (the
+    reference switches to a dense LDLT below dense_threshold free dofs; both
+    meet the same relative-residual contract)."""
+    rel_tolerance: float = 1e-8
+    dense_threshold: int = 200
+    force_iterative: bool = False
+
+
+@dataclasses.dataclass
+class LinearSystem:
+    """fea.hpp:27-34 without the assembled matrix (the GPU never forms it)."""
+    solution: object
+    free_dofs: np.ndarray
+    iterations: int
+    residual: float
+
+
+def assemble_and_solve(grid: StructuredGrid, bc: BoundaryConditions, element_moduli,
+                       poisson: float = 0.3, options: SolveOptions = None,
+                       device: int = 0) -> LinearSystem:
+    """assemble_and_solve (fea.cpp:60-144) on the GPU: matrix-free Jacobi-PCG."""
+    import torch
+    options = options or SolveOptions()
+    n = grid.num_elements()
+    dev = _is_torch_cuda(element_moduli)
+    E = (_dev_f64(element_moduli, "element_moduli") if dev
+         else torch.from_numpy(np.ascontiguousarray(element_moduli, np.float64)).cuda(device))
+    if E.numel() != n:
+        raise DomainError("assemble_and_solve: element_moduli size mismatch")
+    ctx = L.context(device)
+    fixed = np.ascontiguousarray(sorted(bc.fixed_dofs), np.int32)
+    ld = np.ascontiguousarray(list(bc.loads.keys()), np.int32)
+    lv = np.ascontiguousarray(list(bc.loads.values()), np.float64)
+    u = torch.empty(grid.num_dofs(), dtype=torch.float64, device=E.device)
+    its = C.c_int64(0)
+    res = C.c_double(0.0)
+    rc = ctx.lib.topt_b200_fe_solve_dev(ctx.h, grid.nx, grid.ny, grid.element_size, poisson,
+                                        E.data_ptr(), _ptr(fixed), len(fixed), _ptr(ld), _ptr(lv),
+                                        len(ld), options.rel_tolerance, u.data_ptr(),
+                                        C.byref(its), C.byref(res))
+    if rc == L.ERR_PARAMETER:
+        raise ParameterError("bc: invalid boundary conditions (no fixed dofs, out of range, "
+                             "or a load on a fixed dof)")
+    if rc == L.ERR_SINGULAR:
+        raise SingularSystemError(f"assemble_and_solve: cg stalled at relative residual "
+                                  f"{res.value:g} (system may be near-singular; check e_min)")
+    _check(ctx, rc)
+    mask = np.ones(grid.num_dofs(), bool)
+    mask[fixed] = False
+    sol = u if dev else u.cpu().numpy()
+    return LinearSystem(sol, np.nonzero(mask)[0].astype(np.int32), int(its.value), float(res.value))
+
+
+@dataclasses.dataclass
+class ComplianceResult:
+    compliance: float
+    gradient: object
+    solver_iterations: int
+
+
+def compliance_and_gradient(grid: StructuredGrid, bc: BoundaryConditions, densities,
+                            model: MaterialModel, options: SolveOptions = None,
+                            device: int = 0) -> ComplianceResult:
+    """compliance_and_gradient (fea.cpp:146-182), every stage on the GPU:
+    SIMP interpolation, the FE solve, f.u and -dE * u_e^T k0 u_e."""
+    import torch
+    dev = _is_torch_cuda(densities)
+    d = densities if dev else torch.from_numpy(np.ascontiguousarray(densities, np.float64)).cuda(device)
+    interp = interpolate_stiffness(d, grid.num_elements(), model, device)
+    sys_ = assemble_and_solve(grid, bc, interp.moduli, model.poisson, options, device)
+    u = sys_.solution
+    uh = u.cpu().numpy()
+    comp = 0.0
+    for dof, val in bc.loads.items():   # fea.cpp:157
+        comp += val * uh[dof]
+    _, grad = compliance_gradient(grid, u, interp.derivative, model, device)
+    return ComplianceResult(comp, grad if dev else grad.cpu().numpy() if hasattr(grad, "cpu") else grad,
+                            sys_.iterations)

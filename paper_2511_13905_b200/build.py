@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libtopt_b200.so")
-SOURCES = ["capi.cu", "upstream.cu", "dropin.cpp"]
+SOURCES = ["capi.cu", "upstream.cu", "fea.cu", "dropin.cpp"]
 HEADERS = ["topt_core.h", "controller.h", "passes.cuh"]
 
 NVCC_FLAGS = [

@@ -1032,7 +1032,7 @@ TOPT_NOINLINE void consume_prep_core(Plan& pl, const double* t) {
 // projection.cpp:140-145, :151-155) in the reference's order before any
 // decision uses it; the PREP totals wait in the plan meanwhile.
 TOPT_HD bool prep_needs_exact(const Plan& pl) {
-  return pl.P.strict && !pl.ghat_ex_ok &&
+  return pl.P.strict && !pl.ghat_ex_ok && pl.P.m > 0 &&
          (pl.dot_mode || (pl.cmd.validate_part && pl.P.gd_step != nullptr));
 }
 TOPT_NOINLINE void schedule_exact_ghat(Plan& pl, const double* t) {

@@ -250,6 +250,22 @@ __device__ __forceinline__ bool al16(const void* p) {
   return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
 }
 
+// L2 prefetch of a CTA's upcoming slice of a streamed array: one bulk
+// prefetch instruction (TMA unit) per array and step, issued PF_AHEAD loop
+// steps ahead by one thread, so the vector loads of that step hit L2 instead
+// of waiting a full HBM round trip -- the passes are latency-limited with 16
+// warps per SM (ncu: long_scoreboard on the loads).  Clamped to the array.
+constexpr int PF_AHEAD = 3;
+__device__ __forceinline__ void prefetch_l2(const void* base, int64_t off_bytes, int64_t bytes,
+                                            int64_t limit_bytes) {
+  if (off_bytes >= limit_bytes || bytes <= 0) return;
+  if (off_bytes + bytes > limit_bytes) bytes = limit_bytes - off_bytes;
+  bytes &= ~int64_t(15);
+  if (bytes <= 0) return;
+  const char* p = reinterpret_cast<const char*>(base) + off_bytes;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((unsigned)bytes) : "memory");
+}
+
 // ---- Row-pair streaming -------------------------------------------------------
 // Passes that read several element-aligned rows (rho, A rows, x, g, ...) for
 // every element load them as 16-byte pairs: each thread takes element pairs
@@ -660,7 +676,25 @@ __device__ __forceinline__ void prep_group(const PassCtx& c, int j0, int64_t n, 
   // pairs in flight per thread: enough bytes per SM to cover HBM latency
   // (Little's law) without spilling the G rows' accumulators
   constexpr int UP = G == 1 ? 3 : 2;
+  const int64_t cta0 = c.i0 - threadIdx.x;   // this CTA's first pair of a step
   for (int64_t qb = c.i0 - lane; qb < n2; qb += UP * st) {   // warp-uniform trip count
+    if (threadIdx.x == 0) {   // L2 prefetch PF_AHEAD steps ahead (16-byte pairs)
+      const int64_t lim = n2 * 16;
+#pragma unroll
+      for (int u = 0; u < UP; ++u) {
+        const int64_t off = (cta0 + (qb - (c.i0 - lane)) + (int64_t)PF_AHEAD * UP * st + u * st) * 16;
+#pragma unroll
+        for (int r = 0; r < G; ++r) prefetch_l2(A2[r], off, BLOCK * 16, lim);
+        if (FUSE) {
+          prefetch_l2(G2, off, BLOCK * 16, lim);
+          prefetch_l2(X2, off, BLOCK * 16, lim);
+          if (use_dp) prefetch_l2(P2, off, BLOCK * 16, lim);
+        } else {
+          prefetch_l2(R2, off, BLOCK * 16, lim);
+          if (dot) prefetch_l2(D2, off, BLOCK * 16, lim);
+        }
+      }
+    }
     double2 a2[UP][G], r2[UP], d2[UP];
     const double2 z2 = make_double2(0.0, 0.0);
 #pragma unroll
@@ -1987,7 +2021,19 @@ __device__ __noinline__ void pass_newton_pat7(const PassCtx& c) {
   // two pairs per thread in flight (8 x 16-byte loads): the pass is HBM-bound
   // only with enough bytes in flight per SM; same per-thread element order
   int64_t q = c.i0;
+  const int64_t cta0 = c.i0 - threadIdx.x;
   for (; q + st < n2; q += 2 * st) {
+    if (threadIdx.x == 0) {   // L2 prefetch of rho and rows 1, 3, 5, PF_AHEAD steps ahead
+      const int64_t lim = n2 * 16;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t off = (cta0 + (q - c.i0) + (int64_t)PF_AHEAD * 2 * st + u * st) * 16;
+        prefetch_l2(R2, off, BLOCK * 16, lim);
+        prefetch_l2(A2 + ld2, off, BLOCK * 16, lim);
+        prefetch_l2(A2 + 3 * ld2, off, BLOCK * 16, lim);
+        prefetch_l2(A2 + 5 * ld2, off, BLOCK * 16, lim);
+      }
+    }
     const double2 r2 = R2[q], u2 = A2[ld2 + q], v2 = A2[3 * ld2 + q], w2 = A2[5 * ld2 + q];
     const double2 r3 = R2[q + st], u3 = A2[ld2 + q + st], v3 = A2[3 * ld2 + q + st],
                   w3 = A2[5 * ld2 + q + st];
@@ -2067,7 +2113,19 @@ __device__ __noinline__ void pass_feas_pat7(const PassCtx& c) {
       }
     };
     int64_t q = c.i0;
+    const int64_t cta0 = c.i0 - threadIdx.x;
     for (; q + st < n2; q += 2 * st) {   // two pairs in flight (see pass_newton_pat7)
+      if (threadIdx.x == 0) {
+        const int64_t lim = n2 * 16;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int64_t off = (cta0 + (q - c.i0) + (int64_t)PF_AHEAD * 2 * st + u * st) * 16;
+          prefetch_l2(R2, off, BLOCK * 16, lim);
+          prefetch_l2(A2 + ld2, off, BLOCK * 16, lim);
+          prefetch_l2(A2 + 3 * ld2, off, BLOCK * 16, lim);
+          prefetch_l2(A2 + 5 * ld2, off, BLOCK * 16, lim);
+        }
+      }
       const double2 r2 = R2[q], u2 = A2[ld2 + q], v2 = A2[3 * ld2 + q], w2 = A2[5 * ld2 + q];
       const double2 r3 = R2[q + st], u3 = A2[ld2 + q + st], v3 = A2[3 * ld2 + q + st],
                     w3 = A2[5 * ld2 + q + st];
@@ -2638,6 +2696,7 @@ __device__ __noinline__ void pass_exact(const PassCtx& c) {
   const Cmd& cmd = *c.cmd;
   cg::grid_group grid = cg::this_grid();
   const int nc = cmd.ex_n;
+  if (nc <= 0) return;                           // (uniform: no barrier skipped)
   const int NCp = (nc + 1) & ~1;                 // 16-byte rows
   const int seq = cmd.ex_seq;
   const int64_t L = ex_len(P, seq);
