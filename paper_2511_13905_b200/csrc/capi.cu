@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass(Plan* plan, double* partials,
   c.list_cap = 0;
   c.timed_out = nullptr;   // never streamed
   c.ex_smem = nullptr;     // (strict parity runs in the persistent kernel only)
+  c.ms_smem = nullptr;
   double* s_rtab = reinterpret_cast<double*>(reinterpret_cast<char*>(s_dyn) + PLAN_SMEM);
   c.rtab = s_rtab;
   build_row_tables(plan->P, s_rtab);
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     c.timed_out = gb.timed_out;
     c.rtab = s_rtab;
     c.ex_smem = reinterpret_cast<char*>(s_dyn) + sp.P.ex_smem;
+    c.ms_smem = sp.P.ms_smem ? reinterpret_cast<char*>(s_dyn) + sp.P.ms_smem : nullptr;
     if (sp.cmd.phase == PH_SWEEP && sp.cmd.local) {   // CTA-local sweep: no barrier
       local_sweep(c, s_tot);
       if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -717,6 +719,17 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
   // the work area holds the structured rows' tables instead (no active
   // lists in that case)
   dyn_smem = std::max(dyn_smem, PLAN_SMEM + sizeof(double) * (size_t)hp.P.n_tab);
+  // dense multi-row problems without a partition: the fused multi-row sweep's
+  // queues and accumulators (pass_sweep_multi)
+  hp.P.ms_smem = 0;
+  if (persistent && hp.P.m > 1 && !hp.P.has_part && !hp.P.structured) {
+    const size_t off = (dyn_smem + 127) & ~size_t(127);
+    // (leaves room for the strict-parity chain ring: >= 2 stages of 16 KB)
+    if (off + multi_sweep_bytes() + 2 * EX_CHUNK_BYTES + 256 <= (size_t)ctx->max_dyn_smem) {
+      hp.P.ms_smem = (int32_t)off;
+      dyn_smem = off + multi_sweep_bytes();
+    }
+  }
   if (hp.P.strict) {
     // strict parity: chain passes (PH_EXACT) run inside the persistent kernel
     Problem& P = hp.P;

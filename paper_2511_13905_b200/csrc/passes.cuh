@@ -144,6 +144,7 @@ struct PassCtx {
   int* timed_out;      // global flag: a streamed input chunk never arrived
   const double* rtab;  // shared centroid tables of structured rows (P.n_tab entries)
   void* ex_smem;       // chain ring + mbarriers in dynamic shared memory (strict parity)
+  void* ms_smem;       // fused multi-row sweep queues / accumulators (or null)
 };
 
 // ---- Structured constraint rows ------------------------------------------------
@@ -676,25 +677,7 @@ __device__ __forceinline__ void prep_group(const PassCtx& c, int j0, int64_t n, 
   // pairs in flight per thread: enough bytes per SM to cover HBM latency
   // (Little's law) without spilling the G rows' accumulators
   constexpr int UP = G == 1 ? 3 : 2;
-  const int64_t cta0 = c.i0 - threadIdx.x;   // this CTA's first pair of a step
   for (int64_t qb = c.i0 - lane; qb < n2; qb += UP * st) {   // warp-uniform trip count
-    if (threadIdx.x == 0) {   // L2 prefetch PF_AHEAD steps ahead (16-byte pairs)
-      const int64_t lim = n2 * 16;
-#pragma unroll
-      for (int u = 0; u < UP; ++u) {
-        const int64_t off = (cta0 + (qb - (c.i0 - lane)) + (int64_t)PF_AHEAD * UP * st + u * st) * 16;
-#pragma unroll
-        for (int r = 0; r < G; ++r) prefetch_l2(A2[r], off, BLOCK * 16, lim);
-        if (FUSE) {
-          prefetch_l2(G2, off, BLOCK * 16, lim);
-          prefetch_l2(X2, off, BLOCK * 16, lim);
-          if (use_dp) prefetch_l2(P2, off, BLOCK * 16, lim);
-        } else {
-          prefetch_l2(R2, off, BLOCK * 16, lim);
-          if (dot) prefetch_l2(D2, off, BLOCK * 16, lim);
-        }
-      }
-    }
     double2 a2[UP][G], r2[UP], d2[UP];
     const double2 z2 = make_double2(0.0, 0.0);
 #pragma unroll
@@ -862,7 +845,7 @@ __device__ __noinline__ void pass_prep(const PassCtx& c) {
   // 16-byte pairs (a range row only over its own range; outside it only a_j
   // is read, for the validation count), same per-element arithmetic
   if ((!owner || P.part_ranges) && P.chunk <= 0) {
-    if (dir && !owner && !P.structured && (n & 1) == 0 && (ld & 1) == 0 && al16(P.grad) &&
+    if (dir && m >= 1 && !owner && !P.structured && (n & 1) == 0 && (ld & 1) == 0 && al16(P.grad) &&
         al16(g) && al16(x) && al16(dout) && al16(rho) && (!use_dp || al16(dp))) {
       prep_dense_grouped(c, m, n, dir, dot, use_dp, beta, wa, L, U_);
       compact_init(c);
@@ -1382,9 +1365,175 @@ __device__ __noinline__ void pass_sweep_row_compact(const PassCtx& c, int j, int
   __syncthreads();
 }
 
+// ---- fused multi-row sweep (rows found structured by PREP) ------------------
+// The stage-1 sweeps of C4/C5 walk up to 4 rows at once.  pass_sweep_row
+// reads rho and the row once PER ROW; here one pass over the elements reads
+// rho and each walking row's data once (a constant row -- the volume row --
+// not at all; a negated row as its base) and serves every walking row.  Per
+// element and row the classification is SweepAcc's: both breakpoints outside
+// the row's candidate window -> one of three running sums; otherwise the
+// element is queued per (warp, row) and, 32 at a time, run through the full
+// per-candidate loop (sweep_elem), whose per-lane sums are folded into the
+// warp's shared-memory accumulators by a fixed shuffle tree.  Deterministic;
+// the sums differ from the per-row sweep only in (certified) rounding.
+constexpr int MS_ROWS = 4;      // walking rows per fused sweep
+constexpr int MS_Q = 64;        // queue entries per (warp, row)
+__host__ __device__ constexpr size_t multi_sweep_bytes() {
+  return sizeof(double) * (size_t)NWARP * MS_ROWS * (2 * MAX_K + 2 * MS_Q);
+}
+
+template <int KC>
+__device__ __noinline__ void pass_sweep_multi(const PassCtx& c, int nw, const int* wrow) {
+  const Problem& P = c.plan->P;
+  const Cmd& cmd = *c.cmd;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double L = P.lower, U = P.upper;
+  const int64_t n2 = P.n >> 1, st = c.stride, ld2 = P.ld >> 1;
+  const double2* __restrict__ R2 = reinterpret_cast<const double2*>(P.rho);
+  const double2* __restrict__ A2 = reinterpret_cast<const double2*>(P.grad);
+  double* wacc = reinterpret_cast<double*>(c.ms_smem) + (size_t)warp * MS_ROWS * 2 * MAX_K;
+  double* qbase = reinterpret_cast<double*>(c.ms_smem) + (size_t)NWARP * MS_ROWS * 2 * MAX_K +
+                  (size_t)warp * MS_ROWS * 2 * MS_Q;
+  // per walking row: data source, candidate window, running sums
+  int64_t off[MS_ROWS];
+  int kind[MS_ROWS], cb[MS_ROWS], cn[MS_ROWS], qn[MS_ROWS];
+  double cst[MS_ROWS], y0[MS_ROWS], yl[MS_ROWS], Sall[MS_ROWS], Clo[MS_ROWS], Chi[MS_ROWS];
+#pragma unroll
+  for (int w = 0; w < MS_ROWS; ++w) {
+    const int j = w < nw ? wrow[w] : 0;
+    const int ak = P.alias_kind[j];
+    kind[w] = ak;
+    off[w] = (int64_t)(ak == AK_NEG ? j - 1 : j) * ld2;
+    cst[w] = P.alias_c[j];
+    cb[w] = cmd.row_start[j];
+    cn[w] = w < nw ? cmd.row_start[j + 1] - cmd.row_start[j] : 0;
+    y0[w] = cmd.cand_y[cb[w]];
+    yl[w] = cmd.cand_y[cb[w] + (cn[w] > 0 ? cn[w] - 1 : 0)];
+    Sall[w] = Clo[w] = Chi[w] = 0.0;
+    qn[w] = 0;
+  }
+  for (int k = lane; k < MS_ROWS * 2 * MAX_K; k += 32) wacc[k] = 0.0;
+  __syncwarp();
+  // the per-candidate loop over one (warp, row) queue; lanes < cntq hold items
+  auto flush = [&](int w, int from, int cntq) {
+    double C[KC], S[KC];
+#pragma unroll
+    for (int k = 0; k < KC; ++k) { C[k] = 0.0; S[k] = 0.0; }
+    double* qa = qbase + (size_t)w * 2 * MS_Q;
+    double* qr = qa + MS_Q;
+    if (lane < cntq)
+      sweep_elem<KC>(qa[from + lane], qr[from + lane], cmd.cand_y + cb[w], cn[w], L, U, C, S);
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        C[k] += __shfl_down_sync(0xffffffffu, C[k], o);
+        S[k] += __shfl_down_sync(0xffffffffu, S[k], o);
+      }
+    }
+    if (lane == 0) {
+      double* acc = wacc + (size_t)w * 2 * MAX_K;
+#pragma unroll
+      for (int k = 0; k < KC; ++k) { acc[2 * k] += C[k]; acc[2 * k + 1] += S[k]; }
+    }
+    __syncwarp();
+  };
+  auto elem = [&](int w, bool valid, double v, double r) {
+    const double a = kind[w] == AK_CONST ? cst[w] : (kind[w] == AK_NEG ? -v : v);
+    bool need = false;
+    if (valid && a != 0.0) {
+      const double lo = L - r, hi = U - r;
+      const double ra = rcp_full(a);
+      const double b1 = lo * ra, b2 = hi * ra;
+      const bool pos = a > 0.0;
+      const double bl = pos ? b1 : b2, bh = pos ? b2 : b1;
+      const bool outl = bl <= y0[w] || bl > yl[w], outh = bh < y0[w] || bh >= yl[w];
+      if (outl && outh) {
+        const bool above = !(bl > yl[w]);   // p1 == 0
+        const bool freeall = above && bh >= yl[w];
+        if (freeall) Sall[w] += a * a;
+        else if (above) Chi[w] += a * (pos ? hi : lo);
+        else Clo[w] += a * (pos ? lo : hi);
+      } else {
+        need = true;
+      }
+    }
+    const unsigned nm = __ballot_sync(0xffffffffu, need);
+    if (nm) {
+      double* qa = qbase + (size_t)w * 2 * MS_Q;
+      if (need) {
+        const int slot = qn[w] + __popc(nm & ((1u << lane) - 1u));
+        qa[slot] = a;
+        qa[MS_Q + slot] = r;
+      }
+      qn[w] += __popc(nm);
+      __syncwarp();
+      if (qn[w] >= 32) {
+        flush(w, qn[w] - 32, 32);
+        qn[w] -= 32;
+      }
+    }
+  };
+  for (int64_t q0 = c.i0 - lane; q0 < n2; q0 += st) {   // warp-uniform trip count
+    const int64_t q = q0 + lane;
+    const bool ok = q < n2;
+    const double2 r2 = ok ? R2[q] : make_double2(0.0, 0.0);
+    double2 v2[MS_ROWS];
+#pragma unroll
+    for (int w = 0; w < MS_ROWS; ++w)
+      v2[w] = (ok && w < nw && kind[w] != AK_CONST) ? A2[off[w] + q] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int w = 0; w < MS_ROWS; ++w) {
+      if (w < nw) {
+        elem(w, ok, v2[w].x, r2.x);
+        elem(w, ok, v2[w].y, r2.y);
+      }
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < MS_ROWS; ++w)
+    if (w < nw && qn[w] > 0) flush(w, 0, qn[w]);
+  __syncthreads();   // the reduction scratch is reused below
+  // per row: thread sums + (lane 0) the warp's queued sums, then the CTA reduction
+#pragma unroll
+  for (int w = 0; w < MS_ROWS; ++w) {
+    if (w >= nw) continue;
+    const double* acc = wacc + (size_t)w * 2 * MAX_K;
+    double v[2 * KC];
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+      double Ck = Chi[w] + Clo[w], Sk = Sall[w];
+      if (lane == 0) { Ck = Ck + acc[2 * k]; Sk = Sk + acc[2 * k + 1]; }
+      const double yk = k < cn[w] ? cmd.cand_y[cb[w] + k] : 0.0;
+      v[2 * k] = Ck + yk * Sk;
+      v[2 * k + 1] = Sk;
+    }
+    block_reduce_store<2 * KC>(v, 2 * cn[w], PH_SWEEP, 2 * cb[w], c.out, c.smem);
+  }
+}
+
 __device__ void pass_sweep(const PassCtx& c) {
   const Cmd& cmd = *c.cmd;
   const int m = c.plan->P.m;
+  {   // rows with detected structure: one fused pass for all walking rows
+    const Problem& P = c.plan->P;
+    int wrow[MS_ROWS], nw = 0, kmax = 0;
+    bool fit = !cmd.compact && c.ms_smem && P.n_alias && !P.owner && !P.structured &&
+               (P.n & 1) == 0 && (P.ld & 1) == 0 && al16(P.rho) && al16(P.grad);
+    for (int j = 0; j < m && fit; ++j) {
+      const int cnt = cmd.row_start[j + 1] - cmd.row_start[j];
+      if (cnt <= 0) continue;
+      if (nw == MS_ROWS) { fit = false; break; }
+      wrow[nw++] = j;
+      kmax = cnt > kmax ? cnt : kmax;
+    }
+    if (fit && nw >= 2) {
+      if (kmax <= 8) pass_sweep_multi<8>(c, nw, wrow);
+      else if (kmax <= 12) pass_sweep_multi<12>(c, nw, wrow);
+      else pass_sweep_multi<MAX_K>(c, nw, wrow);
+      return;
+    }
+  }
   for (int j = 0; j < m; ++j) {
     const int b = cmd.row_start[j], cnt = cmd.row_start[j + 1] - b;
     if (cnt <= 0) continue;
@@ -2113,19 +2262,7 @@ __device__ __noinline__ void pass_feas_pat7(const PassCtx& c) {
       }
     };
     int64_t q = c.i0;
-    const int64_t cta0 = c.i0 - threadIdx.x;
     for (; q + st < n2; q += 2 * st) {   // two pairs in flight (see pass_newton_pat7)
-      if (threadIdx.x == 0) {
-        const int64_t lim = n2 * 16;
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int64_t off = (cta0 + (q - c.i0) + (int64_t)PF_AHEAD * 2 * st + u * st) * 16;
-          prefetch_l2(R2, off, BLOCK * 16, lim);
-          prefetch_l2(A2 + ld2, off, BLOCK * 16, lim);
-          prefetch_l2(A2 + 3 * ld2, off, BLOCK * 16, lim);
-          prefetch_l2(A2 + 5 * ld2, off, BLOCK * 16, lim);
-        }
-      }
       const double2 r2 = R2[q], u2 = A2[ld2 + q], v2 = A2[3 * ld2 + q], w2 = A2[5 * ld2 + q];
       const double2 r3 = R2[q + st], u3 = A2[ld2 + q + st], v3 = A2[3 * ld2 + q + st],
                     w3 = A2[5 * ld2 + q + st];

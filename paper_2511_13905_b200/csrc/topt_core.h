@@ -250,6 +250,8 @@ struct Problem {
   int32_t ex_nst;               // ring stages of the chain consumer (16 KB each)
   int32_t ex_smem;              // byte offset of the chain ring in dynamic shared memory
   int32_t ex_debug;             // print each chain pass's first results (TOPT_B200_EXDEBUG)
+  int32_t ms_smem;              // byte offset of the fused-sweep area (0: none)
+  int32_t pad4_;
   double* ex_buf;               // 2 x ex_seg x MAX_EX doubles (term staging)
   int64_t ex_seg;               // elements per staged segment
   const int32_t* part_idx;      // device partition indices (CSR; for subset chains)
