@@ -6,6 +6,7 @@ if the library or a CUDA device is missing every call raises.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 
@@ -233,6 +234,26 @@ class Context:
 
     def set_stream(self, stream_ptr: int):
         self.lib.topt_b200_set_stream(self.h, C.c_void_p(stream_ptr))
+
+    @contextlib.contextmanager
+    def ordered_with_torch(self):
+        """Device-tensor calls: this context's stream waits for the work torch
+        has queued on its current stream (the tensors' producers), and torch's
+        stream then waits for ours (the consumers of the outputs) -- event
+        waits on the device, no host synchronisation.  A no-op when the
+        context already runs on torch's current stream (set_stream)."""
+        import torch
+        cur = torch.cuda.current_stream(self.device)
+        mine = self.stream
+        if mine == int(cur.cuda_stream):
+            yield
+            return
+        ext = torch.cuda.ExternalStream(mine, device=self.device)
+        ext.wait_stream(cur)
+        try:
+            yield
+        finally:
+            cur.wait_stream(ext)
 
     def set_structured_rows(self, rows, grid=None, index_offset: int = 0):
         """Structured constraint rows for the following device steps (None

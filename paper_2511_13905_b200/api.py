@@ -368,10 +368,11 @@ def _project(which, rho_tilde, lin, lower, upper, options: ProjectionOptions,
                                                         _ptr(lc.off), _ptr(lc.idx),
                                                         C.c_void_p(lin._owner.data_ptr())))
             lc.s.owner = None if lin._owner is None else lin._owner.data_ptr()
-            _check(ctx, ctx.lib.topt_b200_project_dev(
-                ctx.h, which, rho.data_ptr(), C.byref(lc.s), lower, upper, C.byref(opts),
-                delta.data_ptr(), mask.data_ptr() if mask is not None else None, _ptr(y),
-                _ptr(sl), C.byref(meta)))
+            with ctx.ordered_with_torch():
+                _check(ctx, ctx.lib.topt_b200_project_dev(
+                    ctx.h, which, rho.data_ptr(), C.byref(lc.s), lower, upper, C.byref(opts),
+                    delta.data_ptr(), mask.data_ptr() if mask is not None else None, _ptr(y),
+                    _ptr(sl), C.byref(meta)))
             return _meta_to_result(meta, delta, y, sl, m, mask)
         delta = np.empty(n)
         _check(ctx, ctx.lib.topt_b200_project(ctx.h, which, _ptr(rho), C.byref(lc.s),
@@ -445,16 +446,21 @@ class PreparedStep:
     loop, the benchmark) pay only the library call.  `run()` executes the
     step; `result()` wraps the last outputs like pgd_step's return value."""
 
-    def __init__(self, ctx, fn, args, keep, m, outs, rows=None):
+    def __init__(self, ctx, fn, args, keep, m, outs, rows=None, dev=False):
         self.ctx, self._fn, self._args, self._keep, self.m = ctx, fn, args, keep, m
         self._outs = outs
         self._rows = rows   # (RowDesc list, grid, index_offset) or None
+        self._dev = dev     # device tensors: order the call with torch's stream
 
     def run(self):
         if self._rows is not None:
             self.ctx.set_structured_rows(*self._rows)
         try:
-            _check(self.ctx, self._fn(*self._args))
+            if self._dev:
+                with self.ctx.ordered_with_torch():
+                    _check(self.ctx, self._fn(*self._args))
+            else:
+                _check(self.ctx, self._fn(*self._args))
         finally:
             if self._rows is not None:
                 self.ctx.set_structured_rows(None)
@@ -610,7 +616,7 @@ def prepare_pgd_step(x, x_prev, g, g_prev, d_prev, grad, g_values, bounds_g, is_
                            float(r.get("center", 0.0)), float(r.get("scale", 1.0)),
                            float(r.get("sign", 1.0))) for r in rows]
         srows = (descs, grid, index_offset)
-    return PreparedStep(ctx, fn, args, keep, m, outs, srows)
+    return PreparedStep(ctx, fn, args, keep, m, outs, srows, dev)
 
 
 
@@ -690,8 +696,9 @@ def _filter_product(kernel: FilterKernel, v, transpose: bool, what: str):
         v = _dev_f64(v, what, n)
         import torch
         out = torch.empty_like(v)
-        _check(ctx, ctx.lib.topt_b200_filter_apply_dev(ctx.h, kernel._h, int(transpose),
-                                                       v.data_ptr(), out.data_ptr()))
+        with ctx.ordered_with_torch():
+            _check(ctx, ctx.lib.topt_b200_filter_apply_dev(ctx.h, kernel._h, int(transpose),
+                                                           v.data_ptr(), out.data_ptr()))
         return out
     v = np.ascontiguousarray(v, np.float64)
     out = np.empty(n)
@@ -764,9 +771,10 @@ def interpolate_stiffness(densities, num_elements: int, model: MaterialModel,
     mod = torch.empty(num_elements, dtype=torch.float64, device=d.device)
     der = torch.empty(num_elements * k, dtype=torch.float64, device=d.device)
     young = np.ascontiguousarray(model.young_moduli, np.float64)
-    rc = ctx.lib.topt_b200_interpolate_stiffness_dev(
-        ctx.h, num_elements, k, _ptr(young), model.e_min, model.poisson, model.penalty,
-        d.data_ptr(), mod.data_ptr(), der.data_ptr())
+    with ctx.ordered_with_torch():
+        rc = ctx.lib.topt_b200_interpolate_stiffness_dev(
+            ctx.h, num_elements, k, _ptr(young), model.e_min, model.poisson, model.penalty,
+            d.data_ptr(), mod.data_ptr(), der.data_ptr())
     if rc == L.ERR_DOMAIN:
         raise DomainError("interpolate_stiffness: density outside [0,1]")
     _check(ctx, rc)
@@ -805,9 +813,10 @@ def compliance_gradient(grid: StructuredGrid, displacement, derivative, model: M
     ctx = L.context(device)
     energy = torch.empty(n, dtype=torch.float64, device=u.device)
     grad = torch.empty(n * k, dtype=torch.float64, device=u.device)
-    _check(ctx, ctx.lib.topt_b200_compliance_gradient_dev(
-        ctx.h, grid.nx, grid.ny, grid.element_size, model.poisson, u.data_ptr(), k,
-        der.data_ptr(), energy.data_ptr(), grad.data_ptr()))
+    with ctx.ordered_with_torch():
+        _check(ctx, ctx.lib.topt_b200_compliance_gradient_dev(
+            ctx.h, grid.nx, grid.ny, grid.element_size, model.poisson, u.data_ptr(), k,
+            der.data_ptr(), energy.data_ptr(), grad.data_ptr()))
     torch.cuda.synchronize(u.device)
     if dev:
         return energy, grad
@@ -860,6 +869,7 @@ def pgd_step_lockstep(slabs, n_global: int, settings: PgdSettings = None, device
     rc_arr = None if row_counts is None else np.ascontiguousarray(row_counts, np.int64)
     opts = settings.options()._c()
     sc = settings._c()
+    torch.cuda.current_stream(device).synchronize()   # the slabs' producers (own streams below)
     rc = ctxs[0].lib.topt_b200_pgd_step_lockstep(world, handles, probs, int(n_global), _ptr(rc_arr),
                                                  C.byref(sc), C.byref(opts), outs, metas)
     if rc != L.OK:
@@ -936,10 +946,11 @@ def assemble_and_solve(grid: StructuredGrid, bc: BoundaryConditions, element_mod
     u = torch.empty(grid.num_dofs(), dtype=torch.float64, device=E.device)
     its = C.c_int64(0)
     res = C.c_double(0.0)
-    rc = ctx.lib.topt_b200_fe_solve_dev(ctx.h, grid.nx, grid.ny, grid.element_size, poisson,
-                                        E.data_ptr(), _ptr(fixed), len(fixed), _ptr(ld), _ptr(lv),
-                                        len(ld), options.rel_tolerance, u.data_ptr(),
-                                        C.byref(its), C.byref(res))
+    with ctx.ordered_with_torch():
+        rc = ctx.lib.topt_b200_fe_solve_dev(ctx.h, grid.nx, grid.ny, grid.element_size, poisson,
+                                            E.data_ptr(), _ptr(fixed), len(fixed), _ptr(ld),
+                                            _ptr(lv), len(ld), options.rel_tolerance,
+                                            u.data_ptr(), C.byref(its), C.byref(res))
     if rc == L.ERR_PARAMETER:
         raise ParameterError("bc: invalid boundary conditions (no fixed dofs, out of range, "
                              "or a load on a fixed dof)")

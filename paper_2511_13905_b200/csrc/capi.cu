@@ -15,7 +15,9 @@
 #include <cstddef>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/topt_b200.h"
@@ -255,6 +257,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
   if (threadIdx.x == 0) g_ctl_marks = nullptr;
   for (int pass = 0; pass < 8192; ++pass) {
     if (sp.cmd.phase == PH_DONE) break;
+    progress_mark(0, ((unsigned long long)pass << 8) | (unsigned)sp.cmd.phase);
     unsigned long long* tr = (trace && pass < 64) ? trace + pass * 8 : nullptr;
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) { tr[0] = gtimer(); tr[5] = sp.cmd.phase; }
     // partials alternate between grid-synchronized passes only (a CTA-local
@@ -303,12 +306,14 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
       continue;
     }
     run_pass(c);
+    progress_mark(1, pass);
     if (tr && threadIdx.x == 0) {
       if (blockIdx.x == 0) tr[1] = gtimer();
       atomicMax(tr + 6, gtimer());
     }
     __threadfence();
     grid.sync();
+    progress_mark(2, pass);
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[2] = gtimer();
     if (sp.cmd.phase == PH_PREP && blockIdx.x == 0 && threadIdx.x == 0) signal_out(sp.P);
     if (sp.cmd.phase == PH_GATHER) gather_load(c, nb);
@@ -323,6 +328,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
     } else {
       finish_reduce(part, nb, sp.cmd.nslots, sp.cmd.phase, s_tot, s_red);
     }
+    progress_mark(3, pass);
     if (threadIdx.x == 0) sp.nglobal++;   // (read again only after the controller's barrier)
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
       tr[3] = gtimer();
@@ -347,6 +353,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
       if (threadIdx.x < 32) plan_consume_warp(sp, s_tot);
       __syncthreads();
     }
+    progress_mark(4, pass);
     if (sp.cmd.load_fused) {   // fused gather: the items were published by the sweep
       gather_load_fused(c, nb);
       if (threadIdx.x == 0) sp.cmd.load_fused = 0;
@@ -468,6 +475,12 @@ struct topt_b200_ctx {
   int persistent = 1;       // one cooperative launch per job when possible
   int coop_grid = 0;        // co-resident CTAs for k_step
   int compact = 1;          // active-set compaction of bisection sweeps
+  // fused multi-row sweep (pass_sweep_multi; TOPT_B200_FUSED_SWEEP=1).  Off by
+  // default: measured r02n, the per-row sweeps are faster on every sweep (C4
+  // 409 / 187 / 175 us against 3878 / 357 / 230 us; C5 7.9 / 3.5 / 3.2 ms
+  // against 48.6 / 6.6 / 6.4 ms) -- a wide first window sends nearly every
+  // element through the queued per-candidate loop and its shuffle folds.
+  int fused_sweep = 0;
   int* d_blk_cnt = nullptr;
   double* d_ga = nullptr;
   double* d_gr = nullptr;
@@ -722,7 +735,7 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
   // dense multi-row problems without a partition: the fused multi-row sweep's
   // queues and accumulators (pass_sweep_multi)
   hp.P.ms_smem = 0;
-  if (persistent && hp.P.m > 1 && !hp.P.has_part && !hp.P.structured) {
+  if (persistent && ctx->fused_sweep && hp.P.m > 1 && !hp.P.has_part && !hp.P.structured) {
     const size_t off = (dyn_smem + 127) & ~size_t(127);
     // (leaves room for the strict-parity chain ring: >= 2 stages of 16 KB)
     if (off + multi_sweep_bytes() + 2 * EX_CHUNK_BYTES + 256 <= (size_t)ctx->max_dyn_smem) {
@@ -1213,9 +1226,28 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   ok = ok && cudaMalloc(&ctx->d_probe, sizeof(int)) == cudaSuccess;
   ok = ok && cudaMallocHost(&ctx->h_timed_out, sizeof(int)) == cudaSuccess;
   ok = ok && cudaMallocHost(&ctx->hp_pin, sizeof(Plan)) == cudaSuccess;
+  if (getenv("TOPT_B200_PROGRESS")) {
+    static unsigned long long* hprog = nullptr;
+    if (!hprog && cudaHostAlloc(&hprog, 32 * sizeof(unsigned long long), cudaHostAllocMapped) == cudaSuccess) {
+      std::memset(hprog, 0, 32 * sizeof(unsigned long long));
+      unsigned long long* dprog = nullptr;
+      cudaHostGetDevicePointer(&dprog, hprog, 0);
+      cudaMemcpyToSymbol(g_progress, &dprog, sizeof(dprog));
+      std::thread([] {
+        for (;;) {
+          std::this_thread::sleep_for(std::chrono::seconds(2));
+          volatile unsigned long long* h = hprog;
+          fprintf(stderr, "[progress] pass %llu phase %llu | run %llu sync %llu red %llu ctl %llu | ctas: start %llu run %llu sync %llu red %llu ctl %llu | c5 %llu c6 %llu c7 %llu c8 %llu c9 %llu\n",
+                  h[0] >> 8, h[0] & 255, h[1], h[2], h[3], h[4], h[16], h[17], h[18], h[19], h[20],
+                  h[21], h[22], h[23], h[24], h[25]);
+        }
+      }).detach();
+    }
+  }
   if (const char* e = getenv("TOPT_B200_STREAM")) ctx->stream_inputs = atoi(e);
   if (const char* e = getenv("TOPT_B200_PARITY")) ctx->parity = (std::strcmp(e, "strict") == 0);
   if (const char* e = getenv("TOPT_B200_EXDEBUG")) ctx->ex_debug = atoi(e);
+  if (const char* e = getenv("TOPT_B200_FUSED_SWEEP")) ctx->fused_sweep = atoi(e);
   if (!ok) { topt_b200_ctx_destroy(ctx); return TOPT_ERR_CUDA; }
   *out = ctx;
   return TOPT_OK;

@@ -35,6 +35,16 @@ constexpr double kUnit = 1.1102230246251565e-16;  // 2^-53
 // Optional device-side timeline marks (debug builds of the trace only).
 #if defined(__CUDACC__)
 __device__ unsigned long long* g_ctl_marks = nullptr;
+// Debug progress words in mapped host memory (TOPT_B200_PROGRESS=1): a
+// watchdog thread prints them while a launch is stuck.
+__device__ unsigned long long* g_progress = nullptr;
+__device__ __forceinline__ void progress_mark(int slot, unsigned long long v) {
+  if (g_progress) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_progress[slot] = v;
+    if (threadIdx.x == 0) atomicAdd_system(g_progress + 16 + slot, 1ull);
+    __threadfence_system();
+  }
+}
 #if defined(TOPT_CTL_MARK_SMEM)   // microbenchmark builds: clock64 into shared memory
 __device__ __forceinline__ unsigned long long* ctl_marks_smem() {
   __shared__ unsigned long long m[16];
@@ -1813,7 +1823,12 @@ __device__ __noinline__ void consume_sweep_warp(Plan& pl, const double* t) {
 __device__ void plan_consume_warp(Plan& pl, const double* t) {
   const int lane = threadIdx.x & 31;
   __shared__ WarpPath s_wp2;
-  const int ph = pl.cmd.phase;
+  // One phase value for the whole warp, taken before any lane goes on: lane 0
+  // rewrites cmd.phase below, and a lane that read it late took a different
+  // branch to a different __syncwarp (hang seen with the very short m = 0
+  // PREP step of JOB_DIRECTION).
+  __syncwarp();
+  const int ph = __shfl_sync(0xffffffffu, (int)pl.cmd.phase, 0);
   if (ph == PH_SWEEP) {
     consume_sweep_warp(pl, t);
     return;
@@ -1875,6 +1890,7 @@ __device__ __noinline__ void plan_consume_cta(Plan& pl, const double* t) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int m = pl.P.m;
   const int ph = pl.cmd.phase;
+  __syncthreads();   // every thread has the phase before warp 0 may rewrite it
   const bool multi = m > 1 && m <= (int)(blockDim.x >> 5) && (ph == PH_SWEEP || ph == PH_PREP);
   if (!multi) {
     if (warp == 0) plan_consume_warp(pl, t);

@@ -166,7 +166,9 @@ struct Cmd {
   // both ends are folded into per-CTA fixed sums and dropped from the list.
   int32_t compact, local;        // local: sweep runs on the gathered items in each CTA
   int32_t load_fused;            // the items were published by the last global sweep:
-  int32_t pad_cmd_;              // every CTA loads them before the first local sweep
+                                 // every CTA loads them before the first local sweep
+  int32_t sample;                // > 0: a SKETCH sweep over every 2^sample-th step of each
+                                 // thread's elements; its sums only steer the candidates
   double wlo[MAX_M], whi[MAX_M];
   // PH_EXACT (strict parity)
   int32_t ex_n;                  // chains
@@ -262,6 +264,9 @@ struct Problem {
   int8_t alias_kind[MAX_M];
   int32_t n_alias, pat7;
   double alias_c[MAX_M];
+  // root sketch (controller.h: consume_sketch): problems with at least this
+  // many elements run sampled sweeps before the first full sweep (0: never)
+  int64_t sketch_min_n;
 };
 enum RowKind { RK_DENSE = 0, RK_CONST = 1, RK_CENTROID = 2 };
 // Row structure detected in the data by PREP (dense rows, single rank).
@@ -301,6 +306,7 @@ struct Plan {
   // root sketch from the PREP pass (candidate choice only, never a decision)
   double hint_y[MAX_M], hint_sig[MAX_M];
   int32_t hint_ok[MAX_M];
+  int32_t sketch_left, pad_sk_;       // sampled sweeps still to run before the full ones
   // strict parity
   int32_t ghat_ex_ok;                 // g_hat dots below are reference-order exact
   int32_t nglobal;                    // grid-synchronized passes so far (partials buffer parity)

@@ -23,7 +23,8 @@ import sys, time
 sys.path.insert(0, %r)
 import numpy as np
 import oracle as O
-from paper_2511_13905_b200 import api, synth
+from paper_2511_13905_b200 import _lib, api, synth
+_lib.context(0)   # CUDA initialisation and context creation are not what is timed below
 for name in ("C1", "C4p"):
     p = synth.SMALL[name](11)
     ref = O.pgd_step(p)

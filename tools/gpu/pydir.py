@@ -1,0 +1,17 @@
+"""m = 0 direction job (topt_b200_step_direction) on n random elements."""
+import ctypes as C, numpy as np, sys, os
+sys.path.insert(0, '.')
+from paper_2511_13905_b200 import _lib
+ctx = _lib.context(0)
+n = int(sys.argv[1])
+rng = np.random.default_rng(0)
+x = rng.random(n); xp = x + 0.01 * rng.standard_normal(n); g = -rng.random(n); gp = -rng.random(n)
+d = np.empty(n); rt = np.empty(n)
+a = C.c_double(); b = C.c_double(); fb = C.c_int32()
+class S(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("alpha_max", "alpha_fallback", "omega", "eps_alpha", "tol_n")] + [("t_warmup", C.c_int32)]
+s = S(1e2, 0.2, 1.0, 1e-6, 1e-6, 50)
+p = lambda v: v.ctypes.data_as(C.c_void_p)
+print("calling", n, flush=True)
+rc = ctx.lib.topt_b200_step_direction(ctx.h, n, p(x), p(xp), p(g), p(gp), p(gp), 1, 0.0, C.byref(s), p(d), p(rt), C.byref(a), C.byref(b), C.byref(fb))
+print("rc", rc, a.value, b.value, fb.value, flush=True)
