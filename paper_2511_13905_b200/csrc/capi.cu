@@ -481,6 +481,15 @@ struct topt_b200_ctx {
   // against 48.6 / 6.6 / 6.4 ms) -- a wide first window sends nearly every
   // element through the queued per-candidate loop and its shuffle folds.
   int fused_sweep = 0;
+  // root sketch (controller.h: consume_sketch): sampled sweeps before the first
+  // full sweep for problems of at least this many elements (0: never;
+  // TOPT_B200_SKETCH_MIN_N)
+  int64_t sketch_min_n = (int64_t)1 << 25;
+  // the last PGD step's PREP found the pat7 row layout on these buffers
+  // (Problem::pat_hint; TOPT_B200_PAT_HINT=0 disables)
+  int pat_hint_on = 1;
+  const double* pat_grad = nullptr;
+  int64_t pat_n = 0, pat_ld = 0;
   int* d_blk_cnt = nullptr;
   double* d_ga = nullptr;
   double* d_gr = nullptr;
@@ -707,8 +716,22 @@ void plan_results_take(topt_b200_ctx* ctx, Plan& hp) {
   }
 }
 
+static int run_plan_(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si);
 int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
   if (ctx->comm || ctx->lockstep) return run_plan_ranks(ctx, hp);
+  const bool step = hp.P.job == JOB_PGD_STEP && hp.P.m == 7;
+  hp.P.pat_hint = (step && ctx->pat_hint_on && ctx->pat_grad == hp.P.grad &&
+                   ctx->pat_n == hp.P.n && ctx->pat_ld == hp.P.ld) ? 1 : 0;
+  const int rc = run_plan_(ctx, hp, si);
+  if (step) {   // remember (or forget) the row layout PREP found on these buffers
+    const bool found = rc == TOPT_OK && hp.res.pat7;
+    ctx->pat_grad = found ? hp.P.grad : nullptr;
+    ctx->pat_n = hp.P.n;
+    ctx->pat_ld = hp.P.ld;
+  }
+  return rc;
+}
+static int run_plan_(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si) {
   const bool persistent = ctx->persistent && ctx->coop_grid > 0;
   const int grid = persistent ? ctx->coop_grid : ctx->grid;
   const int64_t per_thread = (hp.P.n + (int64_t)grid * BLOCK - 1) / ((int64_t)grid * BLOCK);
@@ -830,7 +853,25 @@ int run_plan(topt_b200_ctx* ctx, Plan& hp, const StreamIn* si = nullptr) {
       ctx->prof_n++;
     }
     phase = *ctx->h_phase;
-    if (getenv("TOPT_B200_DEBUG_PHASES") && it < 64) fprintf(stderr, "[topt1] pass %d -> phase %d\n", it, phase);
+    if (const char* dbg = getenv("TOPT_B200_DEBUG_PHASES")) {
+      if (it < 64) fprintf(stderr, "[topt1] pass %d -> phase %d\n", it, phase);
+      if (atoi(dbg) >= 2 && it < 64) {   // the next command's candidates and the walks' state
+        static Plan dp;
+        cudaMemcpy(&dp, ctx->d_plan, offsetof(Plan, sc), cudaMemcpyDeviceToHost);
+        if (dp.cmd.phase == PH_SWEEP) {
+          fprintf(stderr, "  sweep: sample %d compact %d ncand %d sketch_left %d\n", dp.cmd.sample,
+                  dp.cmd.compact, dp.cmd.ncand, dp.sketch_left);
+          for (int j = 0; j < dp.P.m; ++j) {
+            const Walk& w = dp.w[j];
+            fprintf(stderr, "  row %d status %d up %d feas %d lo %.6g hi %.6g hok %d hy %.9g hs %.3g E %.3g cand:", j,
+                    w.status, w.up, w.feas_done, w.lo, w.hi, w.hok, w.hy, w.hs, w.E);
+            for (int k = dp.cmd.row_start[j]; k < dp.cmd.row_start[j + 1]; ++k)
+              fprintf(stderr, " %.9g", dp.cmd.cand_y[k]);
+            fprintf(stderr, "\n");
+          }
+        }
+      }
+    }
   }
   if (int rc = plan_results_async(ctx)) return rc;
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
@@ -969,6 +1010,7 @@ int init_problem(topt_b200_ctx* ctx, Plan& hp, int64_t n, int m, const topt_proj
   for (int j = 0; j < m; ++j) P.row_count[j] = (double)n;
   P.strict = ctx->parity;
   P.ex_debug = ctx->ex_debug;
+  P.sketch_min_n = ctx->sketch_min_n;
   return TOPT_OK;
 }
 
@@ -1248,6 +1290,8 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   if (const char* e = getenv("TOPT_B200_PARITY")) ctx->parity = (std::strcmp(e, "strict") == 0);
   if (const char* e = getenv("TOPT_B200_EXDEBUG")) ctx->ex_debug = atoi(e);
   if (const char* e = getenv("TOPT_B200_FUSED_SWEEP")) ctx->fused_sweep = atoi(e);
+  if (const char* e = getenv("TOPT_B200_SKETCH_MIN_N")) ctx->sketch_min_n = atoll(e);
+  if (const char* e = getenv("TOPT_B200_PAT_HINT")) ctx->pat_hint_on = atoi(e);
   if (!ok) { topt_b200_ctx_destroy(ctx); return TOPT_ERR_CUDA; }
   *out = ctx;
   return TOPT_OK;

@@ -694,6 +694,91 @@ TOPT_NOINLINE bool schedule_exact_walks(Plan& pl) {
   return true;
 }
 
+// ---- root sketch ------------------------------------------------------------
+// Before the first full sweep of a large problem, SKETCH_PASSES sampled sweeps
+// (cmd.sample = s: every 2^s-th step of each thread's element loop, about
+// n / 2^s elements spread over the whole index range) evaluate the walks'
+// candidates approximately.  Their sums are never evidence -- no bracket, no
+// certificate, no walk decision uses them: they only place the root estimate
+// (Walk::hy, hs) the candidate choice starts from.  The first full sweep's
+// candidates, and with them the window [y_first, y_last] outside which an
+// element costs three running sums instead of a per-candidate loop, are then
+// already narrow (C5 first sweep: 7.9 ms with the r(0) Newton estimate).
+constexpr int SKETCH_PASSES = 4;   // at most; the sketch stops at its sampling-noise floor
+TOPT_HD int sketch_shift(const Plan& pl) {   // 1/16 of the elements, 1/64 from 2^28 on
+  const int64_t n = pl.P.n_global;
+  return 4 + (n >= ((int64_t)1 << 26) ? 1 : 0) + (n >= ((int64_t)1 << 28) ? 1 : 0);
+}
+
+TOPT_HD bool sketch_wanted(const Plan& pl) {
+  const Problem& P = pl.P;
+  return P.sketch_min_n > 0 && P.n_global >= P.sketch_min_n && !P.strict && !P.has_part;
+}
+
+// A sketch command = the sweep command just built, run over the sample; one
+// extra slot returns the number of elements visited.
+TOPT_HDN inline void sketch_command(Plan& pl) {
+  Cmd& c = pl.cmd;
+  c.sample = 0;
+  if (pl.sketch_left > 0 && !c.local && c.phase == PH_SWEEP) {
+    c.sample = sketch_shift(pl);
+    c.compact = 0;
+    c.nslots = 2 * c.ncand + 1 + pl.P.m;   // + elements visited + each row's sampled r(0) sum
+    pl.res.sweeps--;   // not a sweep of the walk (the first full sweep is still "first")
+  }
+}
+
+TOPT_NOINLINE void consume_sketch(Plan& pl, const double* t) {
+  const int m = pl.P.m;
+  Cmd& c = pl.cmd;
+  const double visited = t[2 * c.ncand];
+  const double scale = visited > 0.0 ? (double)pl.P.n_global / visited : 0.0;
+  bool refine = false;   // some row's bracket is still wider than its sampling noise
+  for (int j = 0; j < m; ++j) {
+    const int b = c.row_start[j], e = c.row_start[j + 1];
+    if (e <= b || !(scale > 0.0)) continue;
+    Walk& w = pl.w[j];
+    // nearest points on either side of the sampled root, seeded with what the
+    // walk knows exactly (r(0) from PREP)
+    bool ha = w.hasA != 0, hb = w.hasB != 0;
+    double ya = w.ya, Ra = w.Ra, yb = w.yb, Rb = w.Rb;
+    double smax = dmax_(ha ? w.Sa : 0.0, hb ? w.Sb : 0.0);
+    // r(y) ~ r(0) [exact, from PREP] + scale (sampled sum at y - sampled sum
+    // at 0): only the terms that change between 0 and y carry sampling
+    // noise (the clipped constants of the centre-of-mass rows, which cancel
+    // to a small r over the whole vector but not over a sample, drop out)
+    const double R0s = t[2 * c.ncand + 1 + j];
+    double dmax = 0.0;
+    for (int k = b; k < e; ++k) {
+      const double y = c.cand_y[k], D = scale * (t[2 * k] - R0s), R = w.r0 + D;
+      const double S = scale * t[2 * k + 1];
+      smax = dmax_(smax, S);
+      if (fabs(R) <= fabs(w.r0)) dmax = dmax_(dmax, fabs(D));   // |difference| near the root
+      if (R <= 0.0 && (!ha || y > ya)) { ha = true; ya = y; Ra = R; }
+      if (R > 0.0 && (!hb || y < yb)) { hb = true; yb = y; Rb = R; }
+    }
+    if (!(ha && hb)) continue;   // no sign change among the points: keep the earlier estimate
+    double hy;
+    if (ya < yb) {
+      hy = ya - est_div(Ra * (yb - ya), Rb - Ra);
+      if (!(hy >= ya)) hy = ya;
+      if (!(hy <= yb)) hy = yb;
+    } else {   // sampling noise crossed the two sides: the middle of the span
+      const double tmp = ya; ya = yb; yb = tmp;
+      hy = 0.5 * (ya + yb);
+    }
+    // sampling noise of the scaled difference, ~ 6 |difference| / sqrt(visited)
+    // (coefficient of variation of the changed terms taken as <= 6), in units of y
+    const double noise = smax > 0.0 ? est_div(6.0 * dmax_(dmax, fabs(w.r0)), sqrt(visited) * smax) : 0.0;
+    const double width = 0.125 * (yb - ya);
+    refine = refine || width > noise;
+    const double hs = dmax_(dmax_(width, noise), 1e-300);
+    w.hok = 1; w.hy = hy; w.hs = hs;
+  }
+  pl.sketch_left = refine ? pl.sketch_left - 1 : 0;
+  c.sample = 0;
+}
+
 // Build the next sweep over all walks that need evaluations; if none do,
 // advance the stage.  Returns true if a sweep was scheduled.
 TOPT_NOINLINE bool schedule_sweep(Plan& pl) {
@@ -731,6 +816,7 @@ TOPT_NOINLINE bool schedule_sweep(Plan& pl) {
   // the CTAs holding more than GATHER_BLK of them
   c.nslots = 2 * tot + ((c.compact && !c.local) ? 2 : 0);
   if (c.local) pl.res.local_sweeps++; else pl.res.sweeps++;
+  sketch_command(pl);
   return true;
 }
 
@@ -962,6 +1048,14 @@ TOPT_NOINLINE void consume_prep_core(Plan& pl, const double* t) {
   Problem& P = pl.P;
   const int m = P.m;
   Result& r = pl.res;
+  if (pl.cmd.pat_hint) {
+    // the pattern PREP derived rows 2, 4, 6 from rows 1, 3, 5: valid only if
+    // every element verified as the exact negation -- else the general PREP
+    // runs again (cmd.phase stays PH_PREP, d and rho_tilde are rewritten alike)
+    bool bad = false;
+    for (int j = 2; j < m; j += 2) bad = bad || t[j * PREP_SLOTS + PS_NNEG] != 0.0;
+    if (bad) { pl.cmd.pat_hint = 0; return; }
+  }
   for (int j = 0; j < m; ++j) {
     const double* s = t + j * PREP_SLOTS;
     double ghat, gerr;
@@ -996,7 +1090,9 @@ TOPT_NOINLINE void consume_prep_core(Plan& pl, const double* t) {
     walk_init(pl.w[j], P.is_eq[j], ghat, E, r0, s[PS_SLOPE0], s[PS_BPLO], s[PS_BPHI],
               s[PS_ANY], cnt, P.strict != 0);
     if (pl.hint_ok[j]) { pl.w[j].hok = 1; pl.w[j].hy = pl.hint_y[j]; pl.w[j].hs = pl.hint_sig[j]; }
+    pl.sk_T[j] = s[PS_T];
   }
+  pl.sketch_left = sketch_wanted(pl) ? SKETCH_PASSES : 0;
   // Row structure seen by PREP (every row was read once): constant rows and
   // rows that are the exact negation of their predecessor.  The later passes
   // then read each distinct row once and derive the others bit for bit
@@ -1018,6 +1114,7 @@ TOPT_NOINLINE void consume_prep_core(Plan& pl, const double* t) {
               P.alias_kind[4] == AK_NEG && P.alias_kind[5] == AK_DENSE &&
               P.alias_kind[6] == AK_NEG) ? 1 : 0;
   }
+  r.pat7 = P.pat7;
   if (P.job == JOB_BUILD || P.job == JOB_DIRECTION) { set_error(pl, ST_OK); return; }
   if (m < 1) { set_error(pl, ST_DOMAIN); return; }
   // Path dispatch, projection.cpp:440-460
@@ -1064,6 +1161,11 @@ TOPT_NOINLINE void consume_sweep(Plan& pl, const double* t) {
   const int m = pl.P.m;
   Cmd& c = pl.cmd;
   ctl_mark(0);
+  if (c.sample) {   // a sketch: steer the candidates, decide nothing
+    consume_sketch(pl, t);
+    if (!schedule_sweep(pl)) after_walks(pl);
+    return;
+  }
   const bool was_global_compact = c.compact && !c.local;
   if (was_global_compact) pl.res.active = t[2 * c.ncand];
   for (int j = 0; j < m; ++j) {
@@ -1221,6 +1323,10 @@ TOPT_HDN inline void plan_start(Plan& pl) {
   c.write_delta = c.write_x = c.write_mask = 0;
   c.compact = 0;
   c.local = 0;
+  c.sample = 0;
+  pl.sketch_left = 0;
+  c.pat_hint = (P.pat_hint && P.job == JOB_PGD_STEP && P.m == 7 && !P.strict && !P.has_part &&
+                !P.structured && P.n_global == P.n) ? 1 : 0;
   if (P.job == JOB_PGD_STEP || P.job == JOB_DIRECTION) {
     c.phase = PH_STEP_REDUCE;
     c.nslots = 6;
@@ -1634,6 +1740,7 @@ TOPT_HDN inline void schedule_finish(Plan& pl, int tot) {
   c.ncand = tot;
   c.nslots = 2 * tot + ((c.compact && !c.local) ? 2 : 0);
   if (c.local) pl.res.local_sweeps++; else pl.res.sweeps++;
+  sketch_command(pl);
 }
 
 __device__ __noinline__ bool schedule_sweep_warp(Plan& pl, WarpPath& wp) {
@@ -1783,6 +1890,18 @@ __device__ __noinline__ void consume_sweep_warp(Plan& pl, const double* t) {
   const int lane = threadIdx.x & 31;
   const int m = pl.P.m;
   Cmd& c = pl.cmd;
+  __shared__ WarpPath s_wpk;
+  if (__shfl_sync(0xffffffffu, (int)c.sample, 0)) {   // a sketch (see consume_sketch)
+    if (lane == 0) {
+      pl.res.passes++;
+      consume_sketch(pl, t);
+    }
+    __syncwarp();
+    const bool more = schedule_sweep_warp(pl, s_wpk);
+    if (lane == 0 && !more) after_walks(pl);
+    __syncwarp();
+    return;
+  }
   const bool was_global_compact = c.compact && !c.local;
   for (int j = 0; j < m; ++j) consume_sweep_row_warp(pl, t, j);
   __shared__ WarpPath s_wp;
@@ -1890,6 +2009,7 @@ __device__ __noinline__ void plan_consume_cta(Plan& pl, const double* t) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int m = pl.P.m;
   const int ph = pl.cmd.phase;
+  const bool sketch = ph == PH_SWEEP && pl.cmd.sample != 0;
   __syncthreads();   // every thread has the phase before warp 0 may rewrite it
   const bool multi = m > 1 && m <= (int)(blockDim.x >> 5) && (ph == PH_SWEEP || ph == PH_PREP);
   if (!multi) {
@@ -1902,7 +2022,13 @@ __device__ __noinline__ void plan_consume_cta(Plan& pl, const double* t) {
   __shared__ double s_cand[MAX_M * MAX_K];
   __shared__ WarpPath s_wpr[MAX_M];
   Cmd& c = pl.cmd;
-  if (ph == PH_SWEEP) {
+  if (sketch) {   // steer the candidates, decide nothing (consume_sketch)
+    if (threadIdx.x == 0) {
+      pl.res.passes++;
+      consume_sketch(pl, t);
+      s_sched = 1;
+    }
+  } else if (ph == PH_SWEEP) {
     const bool was_global_compact = c.compact && !c.local;
     if (warp < m) consume_sweep_row_warp(pl, t, warp);
     __syncthreads();

@@ -728,15 +728,146 @@ __device__ __forceinline__ void prep_group(const PassCtx& c, int j0, int64_t n, 
     block_reduce_store<PREP_SLOTS>(A[r].v, PREP_SLOTS, PH_PREP, (j0 + r) * PREP_SLOTS, c.out, c.smem);
 }
 
+// Pattern PREP (cmd.pat_hint: the previous step on these buffers found rows
+// 2k the exact negations of rows 2k - 1): one sweep computes NP base rows in
+// full and only VERIFIES their negations element by element; a verified
+// negated row's sums follow from its base row's by exact sign flips (every
+// term negated, min and max breakpoints swapped), so the slots written are
+// bit for bit those of the general PREP.  FUSE0 folds the direction pass and
+// row 0 (computed in full) into the sweep.  m = 7: rows 0 | (1, 2) and then
+// (3, 4), (5, 6) -- 14 streamed n-vectors and 4 rows of arithmetic instead of
+// 18 and 7.  A failed verification (PS_NNEG != 0) makes the controller run
+// the general PREP again.
+template <bool FUSE0, int NP>
+__device__ __noinline__ void prep_pairs(const PassCtx& c, int jb0, int64_t n, bool dot,
+                                           bool use_dp, double beta, double wa, double L,
+                                           double U_) {
+  constexpr int NB = NP + (FUSE0 ? 1 : 0);   // rows computed in full
+  const Problem& P = c.plan->P;
+  const int64_t st = c.stride, n2 = n >> 1;
+  const int lane = threadIdx.x & 31;
+  const double2* __restrict__ R2 = reinterpret_cast<const double2*>(P.rho);
+  const double2* __restrict__ D2 = reinterpret_cast<const double2*>(P.d_out);
+  const double2* __restrict__ G2 = reinterpret_cast<const double2*>(P.g);
+  const double2* __restrict__ P2 = reinterpret_cast<const double2*>(use_dp ? P.d_prev : P.g);
+  const double2* __restrict__ X2 = reinterpret_cast<const double2*>(P.x);
+  double2* __restrict__ RO = reinterpret_cast<double2*>(P.rho);
+  double2* __restrict__ DO = reinterpret_cast<double2*>(P.d_out);
+  int rowf[NB];   // the full rows' indices; negated row of full row r (r >= NB - NP): rowf[r] + 1
+#pragma unroll
+  for (int r = 0; r < NB; ++r) rowf[r] = (FUSE0 && r == 0) ? 0 : jb0 + 2 * (r - (FUSE0 ? 1 : 0));
+  const double2* __restrict__ F2[NB];
+  const double2* __restrict__ N2[NP];
+#pragma unroll
+  for (int r = 0; r < NB; ++r)
+    F2[r] = reinterpret_cast<const double2*>(P.grad + (int64_t)rowf[r] * P.ld);
+#pragma unroll
+  for (int p = 0; p < NP; ++p)
+    N2[p] = reinterpret_cast<const double2*>(P.grad + (int64_t)(jb0 + 2 * p + 1) * P.ld);
+  PrepAcc A[NB];
+  double fmin[NB], fmax[NB], aref[NB], nneg[NP];
+#pragma unroll
+  for (int r = 0; r < NB; ++r) {
+#pragma unroll
+    for (int s = 0; s < PREP_SLOTS; ++s) A[r].v[s] = 0.0;
+    fmin[r] = 0.0;
+    fmax[r] = 0.0;
+    aref[r] = n > 0 ? P.grad[(int64_t)rowf[r] * P.ld] : 0.0;
+    A[r].v[PS_NNEG] = 1.0;   // a full row is not examined as a negation
+    if (c.i0 == 0) A[r].v[PS_AREF] = aref[r];
+  }
+#pragma unroll
+  for (int p = 0; p < NP; ++p) nneg[p] = 0.0;
+  constexpr int UP = 1;   // (two pairs in flight spill: 2 x 6 loads + 25 accumulators)
+  for (int64_t qb = c.i0 - lane; qb < n2; qb += UP * st) {   // warp-uniform trip count
+    double2 f2[UP][NB], m2[UP][NP], r2[UP], d2[UP];
+    const double2 z2 = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      const int64_t q = qb + u * st + lane;
+      const bool ok = q < n2;
+#pragma unroll
+      for (int r = 0; r < NB; ++r) f2[u][r] = ok ? F2[r][q] : z2;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) m2[u][p] = ok ? N2[p][q] : z2;
+      if (FUSE0) {
+        const double2 gv = ok ? G2[q] : z2, pv = (ok && use_dp) ? P2[q] : z2;
+        const double2 xv = ok ? X2[q] : z2;
+        // d = g + beta d_prev ; rho = x - (omega alpha) d
+        d2[u].x = use_dp ? gv.x + beta * pv.x : gv.x;
+        d2[u].y = use_dp ? gv.y + beta * pv.y : gv.y;
+        r2[u].x = xv.x - wa * d2[u].x;
+        r2[u].y = xv.y - wa * d2[u].y;
+        if (ok) {
+          DO[q] = d2[u];
+          RO[q] = r2[u];
+        }
+      } else {
+        r2[u] = ok ? R2[q] : z2;
+        d2[u] = (ok && dot) ? D2[q] : z2;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      if (qb + u * st + lane < n2) {
+        const double g0 = dot ? wa * d2[u].x : 0.0, g1 = dot ? wa * d2[u].y : 0.0;
+#pragma unroll
+        for (int r = 0; r < NB; ++r) {
+          prep_elem_w(A[r], f2[u][r].x, r2[u].x, g0, dot, L, U_, fmin[r], fmax[r]);
+          prep_elem_w(A[r], f2[u][r].y, r2[u].y, g1, dot, L, U_, fmin[r], fmax[r]);
+          A[r].v[PS_NCONST] += (double)((f2[u][r].x != aref[r]) + (f2[u][r].y != aref[r]));
+        }
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const double2 b = f2[u][NB - NP + p];
+          nneg[p] += (double)((m2[u][p].x != -b.x) + (m2[u][p].y != -b.y));
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NB; ++r) warp_minmax(fmin[r], fmax[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < NB; ++r)
+    block_reduce_store<PREP_SLOTS>(A[r].v, PREP_SLOTS, PH_PREP, rowf[r] * PREP_SLOTS, c.out, c.smem);
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {   // the negated rows' slots from their base rows'
+    const PrepAcc& B = A[NB - NP + p];
+    PrepAcc Dn;
+    Dn.v[PS_DOT] = -B.v[PS_DOT];
+    Dn.v[PS_DABS] = B.v[PS_DABS];
+    Dn.v[PS_S0] = -B.v[PS_S0];
+    Dn.v[PS_SLOPE0] = B.v[PS_SLOPE0];
+    Dn.v[PS_T] = B.v[PS_T];
+    Dn.v[PS_NZOUT] = B.v[PS_NZOUT];
+    Dn.v[PS_BPLO] = -B.v[PS_BPHI];
+    Dn.v[PS_BPHI] = -B.v[PS_BPLO];
+    Dn.v[PS_ANY] = B.v[PS_ANY];
+    Dn.v[PS_NCONST] = B.v[PS_NCONST];
+    Dn.v[PS_AREF] = -B.v[PS_AREF];
+    Dn.v[PS_NNEG] = nneg[p];
+    block_reduce_store<PREP_SLOTS>(Dn.v, PREP_SLOTS, PH_PREP, (jb0 + 2 * p + 1) * PREP_SLOTS, c.out,
+                                   c.smem);
+  }
+}
+
 // Dense rows, no partition, device-resident aligned inputs: the direction
 // pass fused with the first row group, then groups of PREP_GROUP rows.
 constexpr int PREP_GROUP = 2;
+__device__ __forceinline__ bool P_detect_single_rank(const PassCtx& c) {
+  return c.plan->P.n_global == c.plan->P.n;
+}
 __device__ __noinline__ void prep_dense_grouped(const PassCtx& c, int m, int64_t n, bool dir,
                                                 bool dot, bool use_dp, double beta, double wa,
                                                 double L, double U_) {
   // row 0 with the direction pass, then pairs (1,2), (3,4), ...: the +- rows
   // of two-sided constraints (a row and its negation, adjacent) share a group,
   // where the negation is detected (same 2m + 4 streamed vectors as before)
+  if (c.cmd->pat_hint && dir && m == 7 && P_detect_single_rank(c)) {
+    prep_pairs<true, 1>(c, 1, n, dot, use_dp, beta, wa, L, U_);
+    prep_pairs<false, 2>(c, 3, n, dot, use_dp, beta, wa, L, U_);
+    return;
+  }
   int j = 0;
   if (dir) {
     prep_group<1, true>(c, 0, n, dot, use_dp, beta, wa, L, U_);
@@ -1174,10 +1305,20 @@ __device__ __forceinline__ void sweep_finish(const double* y, int cnt, double* C
     if (k < cnt) C[k] = C[k] + y[k] * S[k];
 }
 
+// cmd.sample = s > 0 (a sketch, controller.h: consume_sketch): only every
+// 2^s-th step of the loop below runs; `count_slot` >= 0 then receives the
+// number of elements visited.
 template <int KC>
-__device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int cnt) {
+__device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int cnt,
+                                            int count_slot = -1) {
   const Problem& P = c.plan->P;
   const int64_t n = P.n, st = c.stride;
+  const int shift = c.cmd->sample;
+  double visited = 0.0, r0s = 0.0;   // sketch: elements visited, their sum of a clip(0, lo, hi)
+  auto term0 = [&](bool ok, double a, double r) {
+    const double lo = P.lower - r, hi = P.upper - r;
+    return ok ? a * (0.0 < lo ? lo : (0.0 > hi ? hi : 0.0)) : 0.0;
+  };
   const double* __restrict__ rho = P.rho;
   const double* __restrict__ ar = P.grad + (int64_t)j * P.ld;
   const int8_t* __restrict__ owner = P.owner;
@@ -1204,9 +1345,10 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
     const int64_t n2 = rhi >> 1;
     const double2* __restrict__ A2 = reinterpret_cast<const double2*>(ar);
     const double2* __restrict__ R2 = reinterpret_cast<const double2*>(rho);
-    for (int64_t q0 = (rlo >> 1) + c.i0 - lane; q0 < n2; q0 += 2 * st) {
+    for (int64_t q0 = (rlo >> 1) + c.i0 - lane; q0 < n2; q0 += (2 * st) << shift) {
       const int64_t qa = q0 + lane, qb = q0 + st + lane;
       const bool oa = qa < n2, ob = qb < n2;
+      visited += (double)(2 * ((int)oa + (int)ob));
       double2 a0 = (oa && !gen && !cst) ? A2[qa] : make_double2(cv, cv);
       double2 a1 = (ob && !gen && !cst) ? A2[qb] : make_double2(cv, cv);
       const double2 r0 = oa ? R2[qa] : make_double2(0.0, 0.0), r1 = ob ? R2[qb] : make_double2(0.0, 0.0);
@@ -1223,6 +1365,9 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
           a1 = make_double2(srow_fetch(c.rtab, gcode, c0), srow_fetch(c.rtab, gcode, c1));
         }
       }
+      if (shift)
+        r0s += (term0(oa, a0.x, r0.x) + term0(oa, a0.y, r0.y)) +
+               (term0(ob, a1.x, r1.x) + term0(ob, a1.y, r1.y));
       acc.push(oa, a0.x, r0.x);
       acc.push(oa, a0.y, r0.y);
       acc.push(ob, a1.x, r1.x);
@@ -1230,15 +1375,20 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
     }
   } else {
   constexpr int UL = 4;   // elements' loads in flight per lane
-  for (int64_t i0 = c.i0 - lane; i0 < n; i0 += UL * st) {   // warp-uniform trip count
+  for (int64_t i0 = c.i0 - lane; i0 < n; i0 += (UL * st) << shift) {   // warp-uniform trip count
     double av[UL], rv[UL];
     bool ok[UL];
 #pragma unroll
     for (int u = 0; u < UL; ++u) {
       const int64_t i = i0 + u * st + lane;
       ok[u] = i < n && (owner == nullptr || owner[i] == j);
+      visited += ok[u] ? 1.0 : 0.0;
       av[u] = ok[u] ? ar[i] : 0.0;
       rv[u] = ok[u] ? rho[i] : 0.0;
+    }
+    if (shift) {
+#pragma unroll
+      for (int u = 0; u < UL; ++u) r0s += term0(ok[u], av[u], rv[u]);
     }
 #pragma unroll
     for (int u = 0; u < UL; ++u) acc.push(ok[u], av[u], rv[u]);
@@ -1251,6 +1401,14 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
 #pragma unroll
   for (int k = 0; k < KC; ++k) { v[2 * k] = acc.C[k]; v[2 * k + 1] = acc.S[k]; }
   block_reduce_store<2 * KC>(v, 2 * cnt, PH_SWEEP, 2 * b, c.out, c.smem);
+  if (shift) {   // sketch slots: [2 ncand] elements visited, [2 ncand + 1 + j] row j's sampled r(0) sum
+    const double cv1[1] = {r0s};
+    block_reduce_store<1>(cv1, 1, PH_SWEEP, 2 * c.cmd->ncand + 1 + j, c.out, c.smem);
+  }
+  if (count_slot >= 0) {
+    const double cv1[1] = {visited};
+    block_reduce_store<1>(cv1, 1, PH_SWEEP, count_slot, c.out, c.smem);
+  }
 }
 
 // Compacted sweep of row j over the warps' active lists.  An element whose
@@ -1369,21 +1527,78 @@ __device__ __noinline__ void pass_sweep_row_compact(const PassCtx& c, int j, int
 // The stage-1 sweeps of C4/C5 walk up to 4 rows at once.  pass_sweep_row
 // reads rho and the row once PER ROW; here one pass over the elements reads
 // rho and each walking row's data once (a constant row -- the volume row --
-// not at all; a negated row as its base) and serves every walking row.  Per
-// element and row the classification is SweepAcc's: both breakpoints outside
-// the row's candidate window -> one of three running sums; otherwise the
-// element is queued per (warp, row) and, 32 at a time, run through the full
-// per-candidate loop (sweep_elem), whose per-lane sums are folded into the
-// warp's shared-memory accumulators by a fixed shuffle tree.  Deterministic;
-// the sums differ from the per-row sweep only in (certified) rounding.
+// not at all; a negated row as its base) and serves every walking row.
+//
+// Per element and row the clip region of the reference's own predicate on
+// fl(y a) is taken at the two ends of the row's candidate window [y_first,
+// y_last] (two products, four compares, no reciprocal): fl(y a) is monotone
+// in y, so an element with the same region at both ends has it at every
+// candidate in between and adds its exact term -- a lo, a hi, or a^2 for the
+// slope of y a^2 -- to one of two running sums.  Only elements whose region
+// changes inside the window are queued per (warp, row) and, 32 at a time, run
+// through the per-candidate loop (sweep_elem) in ms_flush, whose per-lane
+// sums are folded into the warp's shared-memory accumulators by a fixed
+// shuffle tree.  With the root sketch (controller.h) every full sweep has a
+// narrow window, so the queue path is rare.  Deterministic; the sums differ
+// from the per-row sweep only in (certified) rounding.
 constexpr int MS_ROWS = 4;      // walking rows per fused sweep
 constexpr int MS_Q = 64;        // queue entries per (warp, row)
 __host__ __device__ constexpr size_t multi_sweep_bytes() {
   return sizeof(double) * (size_t)NWARP * MS_ROWS * (2 * MAX_K + 2 * MS_Q);
 }
 
+// lanes < cntq hold queued items qa[from + lane] (a), qa[MS_Q + from + lane] (rho)
 template <int KC>
-__device__ __noinline__ void pass_sweep_multi(const PassCtx& c, int nw, const int* wrow) {
+__device__ __noinline__ void ms_flush_k(const double* qa, double* acc, const double* y, int cn,
+                                        double L, double U, int from, int cntq) {
+  const int lane = threadIdx.x & 31;
+  double C[KC], S[KC];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) { C[k] = 0.0; S[k] = 0.0; }
+  if (lane < cntq) sweep_elem<KC>(qa[from + lane], qa[MS_Q + from + lane], y, cn, L, U, C, S);
+#pragma unroll
+  for (int k = 0; k < KC; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      C[k] += __shfl_down_sync(0xffffffffu, C[k], o);
+      S[k] += __shfl_down_sync(0xffffffffu, S[k], o);
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < KC; ++k) { acc[2 * k] += C[k]; acc[2 * k + 1] += S[k]; }
+  }
+  __syncwarp();
+}
+__device__ __noinline__ void ms_flush(int kc, const double* qa, double* acc, const double* y,
+                                      int cn, double L, double U, int from, int cntq) {
+  if (kc <= 8) ms_flush_k<8>(qa, acc, y, cn, L, U, from, cntq);
+  else if (kc <= 12) ms_flush_k<12>(qa, acc, y, cn, L, U, from, cntq);
+  else ms_flush_k<MAX_K>(qa, acc, y, cn, L, U, from, cntq);
+}
+
+// Candidates far outside the others -- in a walk's first sweep the
+// infeasibility probe at the bracket end (projection.cpp:80-94) and the first
+// midpoints of a bracket much wider than the root's neighbourhood -- would
+// stretch the window over nearly every element's breakpoints.  Up to two of
+// them at one end are kept out of the window: ms_outliers finds them (their
+// gap to the next candidate more than 4x the span of the rest), and the OUTL
+// instantiation evaluates each for every un-queued element with its own
+// region test and sums.  Returns their count; *low: at the low end.
+__device__ __forceinline__ int ms_outliers(const double* y, int cn, bool* low) {
+  *low = true;
+  if (cn < 4) return 0;
+  const double y1 = y[0], y2 = y[1], y3 = y[2], yz = y[cn - 1], yy = y[cn - 2], yx = y[cn - 3];
+  const int nlo = (y3 - y2) > 4.0 * (yz - y3) ? 2 : ((y2 - y1) > 4.0 * (yz - y2) ? 1 : 0);
+  const int nhi = (yy - yx) > 4.0 * (yx - y1) ? 2 : ((yz - yy) > 4.0 * (yy - y1) ? 1 : 0);
+  if (nlo >= nhi) return nlo;
+  *low = false;
+  return nhi;
+}
+
+template <int NW, bool OUTL>
+__device__ __noinline__ void pass_sweep_multi_t(const PassCtx& c, const int* wrow, int kmax) {
+  constexpr int nw = NW;
   const Problem& P = c.plan->P;
   const Cmd& cmd = *c.cmd;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1395,69 +1610,52 @@ __device__ __noinline__ void pass_sweep_multi(const PassCtx& c, int nw, const in
   double* qbase = reinterpret_cast<double*>(c.ms_smem) + (size_t)NWARP * MS_ROWS * 2 * MAX_K +
                   (size_t)warp * MS_ROWS * 2 * MS_Q;
   // per walking row: data source, candidate window, running sums
-  int64_t off[MS_ROWS];
-  int kind[MS_ROWS], cb[MS_ROWS], cn[MS_ROWS], qn[MS_ROWS];
-  double cst[MS_ROWS], y0[MS_ROWS], yl[MS_ROWS], Sall[MS_ROWS], Clo[MS_ROWS], Chi[MS_ROWS];
+  int64_t off[NW];
+  int qn[NW];
+  unsigned negm = 0u, cstm = 0u;   // bit w: row w is a negated / a constant row
+  double cst = 0.0;                // (constant rows of one problem share their value: one volume row)
+  double y0[NW], yl[NW], Sall[NW], Cfix[NW];
+  constexpr int NO = OUTL ? 2 * NW : 1;
+  double yo[NO], So[NO], Co[NO];   // the outlier candidates (two slots per row)
+  int no[NW];                      // their count, negated when they sit at the high end
 #pragma unroll
-  for (int w = 0; w < MS_ROWS; ++w) {
-    const int j = w < nw ? wrow[w] : 0;
+  for (int w = 0; w < NW; ++w) {
+    const int j = wrow[w];
     const int ak = P.alias_kind[j];
-    kind[w] = ak;
+    const int cb = cmd.row_start[j];
+    const int cn = cmd.row_start[j + 1] - cb;
+    if (ak == AK_NEG) negm |= 1u << w;
+    if (ak == AK_CONST) { cstm |= 1u << w; cst = P.alias_c[j]; }
     off[w] = (int64_t)(ak == AK_NEG ? j - 1 : j) * ld2;
-    cst[w] = P.alias_c[j];
-    cb[w] = cmd.row_start[j];
-    cn[w] = w < nw ? cmd.row_start[j + 1] - cmd.row_start[j] : 0;
-    y0[w] = cmd.cand_y[cb[w]];
-    yl[w] = cmd.cand_y[cb[w] + (cn[w] > 0 ? cn[w] - 1 : 0)];
-    Sall[w] = Clo[w] = Chi[w] = 0.0;
+    bool olow = true;
+    const int nout = OUTL ? ms_outliers(cmd.cand_y + cb, cn, &olow) : 0;
+    no[w] = olow ? nout : -nout;
+    y0[w] = cmd.cand_y[cb + (olow ? nout : 0)];
+    yl[w] = cmd.cand_y[cb + (cn > 0 ? cn - 1 : 0) - (olow ? 0 : nout)];
+    if (OUTL) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {   // outlier u = candidate u (low end) / cn - nout + u (high end)
+        yo[2 * w + u] = u < nout ? cmd.cand_y[cb + (olow ? u : cn - nout + u)] : y0[w];
+        So[2 * w + u] = Co[2 * w + u] = 0.0;
+      }
+    }
+    Sall[w] = Cfix[w] = 0.0;
     qn[w] = 0;
   }
   for (int k = lane; k < MS_ROWS * 2 * MAX_K; k += 32) wacc[k] = 0.0;
   __syncwarp();
-  // the per-candidate loop over one (warp, row) queue; lanes < cntq hold items
   auto flush = [&](int w, int from, int cntq) {
-    double C[KC], S[KC];
-#pragma unroll
-    for (int k = 0; k < KC; ++k) { C[k] = 0.0; S[k] = 0.0; }
-    double* qa = qbase + (size_t)w * 2 * MS_Q;
-    double* qr = qa + MS_Q;
-    if (lane < cntq)
-      sweep_elem<KC>(qa[from + lane], qr[from + lane], cmd.cand_y + cb[w], cn[w], L, U, C, S);
-#pragma unroll
-    for (int k = 0; k < KC; ++k) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        C[k] += __shfl_down_sync(0xffffffffu, C[k], o);
-        S[k] += __shfl_down_sync(0xffffffffu, S[k], o);
-      }
-    }
-    if (lane == 0) {
-      double* acc = wacc + (size_t)w * 2 * MAX_K;
-#pragma unroll
-      for (int k = 0; k < KC; ++k) { acc[2 * k] += C[k]; acc[2 * k + 1] += S[k]; }
-    }
-    __syncwarp();
+    const int j = wrow[w];
+    const int cb = cmd.row_start[j];
+    ms_flush(kmax, qbase + (size_t)w * 2 * MS_Q, wacc + (size_t)w * 2 * MAX_K, cmd.cand_y + cb,
+             cmd.row_start[j + 1] - cb, L, U, from, cntq);
   };
-  auto elem = [&](int w, bool valid, double v, double r) {
-    const double a = kind[w] == AK_CONST ? cst[w] : (kind[w] == AK_NEG ? -v : v);
-    bool need = false;
-    if (valid && a != 0.0) {
-      const double lo = L - r, hi = U - r;
-      const double ra = rcp_full(a);
-      const double b1 = lo * ra, b2 = hi * ra;
-      const bool pos = a > 0.0;
-      const double bl = pos ? b1 : b2, bh = pos ? b2 : b1;
-      const bool outl = bl <= y0[w] || bl > yl[w], outh = bh < y0[w] || bh >= yl[w];
-      if (outl && outh) {
-        const bool above = !(bl > yl[w]);   // p1 == 0
-        const bool freeall = above && bh >= yl[w];
-        if (freeall) Sall[w] += a * a;
-        else if (above) Chi[w] += a * (pos ? hi : lo);
-        else Clo[w] += a * (pos ? lo : hi);
-      } else {
-        need = true;
-      }
-    }
+  // row w's value at an element from the loaded pair value
+  auto rowval = [&](int w, double v) {
+    return ((cstm >> w) & 1u) ? cst : (((negm >> w) & 1u) ? -v : v);
+  };
+  // queue the lanes whose bit is set in their needmask for row w
+  auto enqueue = [&](int w, bool need, double a, double r) {
     const unsigned nm = __ballot_sync(0xffffffffu, need);
     if (nm) {
       double* qa = qbase + (size_t)w * 2 * MS_Q;
@@ -1474,41 +1672,118 @@ __device__ __noinline__ void pass_sweep_multi(const PassCtx& c, int nw, const in
       }
     }
   };
-  for (int64_t q0 = c.i0 - lane; q0 < n2; q0 += st) {   // warp-uniform trip count
+  // One pair per thread and step, the next step's loads issued before this
+  // step's arithmetic (the classification is branch-free: every (element,
+  // row) is independent work for the fp64 pipe while the loads are in flight).
+  const double2 z2 = make_double2(0.0, 0.0);
+  int64_t q0 = c.i0 - lane;   // warp-uniform trip count
+  double2 r2 = z2, v2[NW];
+  {
     const int64_t q = q0 + lane;
     const bool ok = q < n2;
-    const double2 r2 = ok ? R2[q] : make_double2(0.0, 0.0);
-    double2 v2[MS_ROWS];
+    r2 = ok ? R2[q] : z2;
 #pragma unroll
-    for (int w = 0; w < MS_ROWS; ++w)
-      v2[w] = (ok && w < nw && kind[w] != AK_CONST) ? A2[off[w] + q] : make_double2(0.0, 0.0);
+    for (int w = 0; w < NW; ++w) v2[w] = (ok && !((cstm >> w) & 1u)) ? A2[off[w] + q] : z2;
+  }
+  for (; q0 < n2; q0 += st) {
+    const bool ok = q0 + lane < n2;
+    const int64_t qn1 = q0 + st + lane;
+    const bool ok1 = qn1 < n2;
+    const double2 r2n = ok1 ? R2[qn1] : z2;
+    double2 v2n[NW];
 #pragma unroll
-    for (int w = 0; w < MS_ROWS; ++w) {
-      if (w < nw) {
-        elem(w, ok, v2[w].x, r2.x);
-        elem(w, ok, v2[w].y, r2.y);
+    for (int w = 0; w < NW; ++w) v2n[w] = (ok1 && !((cstm >> w) & 1u)) ? A2[off[w] + qn1] : z2;
+    const double lo0 = L - r2.x, hi0 = U - r2.x, lo1 = L - r2.y, hi1 = U - r2.y;
+    unsigned needmask = 0u;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double a = rowval(w, e ? v2[w].y : v2[w].x);
+        const double lo = e ? lo1 : lo0, hi = e ? hi1 : hi0;
+        const double t0 = y0[w] * a, tl = yl[w] * a;
+        const bool b0 = t0 < lo, a0 = t0 > hi, bl = tl < lo, al = tl > hi;
+        const bool live = ok && a != 0.0;
+        const bool same = (b0 == bl) && (a0 == al);   // one region over the whole window
+        const double term = b0 ? a * lo : (a0 ? a * hi : 0.0);
+        Cfix[w] += (live && same) ? term : 0.0;
+        Sall[w] += (live && same && !b0 && !a0) ? a * a : 0.0;
+        needmask |= (live && !same) ? (1u << (2 * w + e)) : 0u;
+        if (OUTL) {   // the outlier candidates' own regions (queued elements get them in ms_flush)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const double to = yo[2 * w + u] * a;
+            const bool bo = to < lo, ao = to > hi;
+            Co[2 * w + u] += (live && same) ? (bo ? a * lo : (ao ? a * hi : 0.0)) : 0.0;
+            So[2 * w + u] += (live && same && !bo && !ao) ? a * a : 0.0;
+          }
+        }
       }
     }
+    if (__any_sync(0xffffffffu, needmask != 0u)) {   // rare once the window is narrow
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        enqueue(w, (needmask >> (2 * w)) & 1u, rowval(w, v2[w].x), r2.x);
+        enqueue(w, (needmask >> (2 * w + 1)) & 1u, rowval(w, v2[w].y), r2.y);
+      }
+    }
+    r2 = r2n;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) v2[w] = v2n[w];
   }
 #pragma unroll
-  for (int w = 0; w < MS_ROWS; ++w)
-    if (w < nw && qn[w] > 0) flush(w, 0, qn[w]);
+  for (int w = 0; w < NW; ++w)
+    if (qn[w] > 0) flush(w, 0, qn[w]);
   __syncthreads();   // the reduction scratch is reused below
   // per row: thread sums + (lane 0) the warp's queued sums, then the CTA reduction
 #pragma unroll
-  for (int w = 0; w < MS_ROWS; ++w) {
-    if (w >= nw) continue;
+  for (int w = 0; w < NW; ++w) {
+    const int j = wrow[w];
+    const int cb = cmd.row_start[j], cn = cmd.row_start[j + 1] - cb;
     const double* acc = wacc + (size_t)w * 2 * MAX_K;
-    double v[2 * KC];
+    for (int k0 = 0; k0 < cn; k0 += 4) {   // 4 candidates (8 slots) per reduction
+      double v[8];
 #pragma unroll
-    for (int k = 0; k < KC; ++k) {
-      double Ck = Chi[w] + Clo[w], Sk = Sall[w];
-      if (lane == 0) { Ck = Ck + acc[2 * k]; Sk = Sk + acc[2 * k + 1]; }
-      const double yk = k < cn[w] ? cmd.cand_y[cb[w] + k] : 0.0;
-      v[2 * k] = Ck + yk * Sk;
-      v[2 * k + 1] = Sk;
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u;
+        double Ck = Cfix[w], Sk = Sall[w];
+        if (OUTL) {
+          const int nout = no[w] < 0 ? -no[w] : no[w];
+          const int u = no[w] >= 0 ? k : k - (cn - nout);   // outlier slot of candidate k, if any
+          if (u >= 0 && u < nout && k < cn) {
+            Ck = u == 0 ? Co[2 * w] : Co[2 * w + 1];
+            Sk = u == 0 ? So[2 * w] : So[2 * w + 1];
+          }
+        }
+        if (lane == 0 && k < cn) { Ck = Ck + acc[2 * k]; Sk = Sk + acc[2 * k + 1]; }
+        const double yk = k < cn ? cmd.cand_y[cb + k] : 0.0;
+        v[2 * u] = Ck + yk * Sk;
+        v[2 * u + 1] = Sk;
+      }
+      const int ns = 2 * (cn - k0 < 4 ? cn - k0 : 4);
+      block_reduce_store<8>(v, ns, PH_SWEEP, 2 * (cb + k0), c.out, c.smem);
     }
-    block_reduce_store<2 * KC>(v, 2 * cn[w], PH_SWEEP, 2 * cb[w], c.out, c.smem);
+  }
+}
+
+__device__ void pass_sweep_multi(const PassCtx& c, int nw, const int* wrow, int kmax) {
+  const Cmd& cmd = *c.cmd;
+  bool outl = false;
+  for (int w = 0; w < nw; ++w) {
+    const int cb = cmd.row_start[wrow[w]];
+    bool low;
+    outl = outl || ms_outliers(cmd.cand_y + cb, cmd.row_start[wrow[w] + 1] - cb, &low) > 0;
+  }
+  if (outl) {   // (the outlier sums cost registers: two rows per pass over the elements)
+    for (int w = 0; w < nw; w += 2) {
+      if (w + 1 < nw) pass_sweep_multi_t<2, true>(c, wrow + w, kmax);
+      else pass_sweep_multi_t<1, true>(c, wrow + w, kmax);
+      __syncthreads();
+    }
+  } else {
+    if (nw == 2) pass_sweep_multi_t<2, false>(c, wrow, kmax);
+    else if (nw == 3) pass_sweep_multi_t<3, false>(c, wrow, kmax);
+    else pass_sweep_multi_t<4, false>(c, wrow, kmax);
   }
 }
 
@@ -1518,22 +1793,23 @@ __device__ void pass_sweep(const PassCtx& c) {
   {   // rows with detected structure: one fused pass for all walking rows
     const Problem& P = c.plan->P;
     int wrow[MS_ROWS], nw = 0, kmax = 0;
-    bool fit = !cmd.compact && c.ms_smem && P.n_alias && !P.owner && !P.structured &&
+    bool fit = !cmd.compact && !cmd.sample && c.ms_smem && P.n_alias && !P.owner && !P.structured &&
                (P.n & 1) == 0 && (P.ld & 1) == 0 && al16(P.rho) && al16(P.grad);
+    int ncst = 0;
     for (int j = 0; j < m && fit; ++j) {
       const int cnt = cmd.row_start[j + 1] - cmd.row_start[j];
       if (cnt <= 0) continue;
       if (nw == MS_ROWS) { fit = false; break; }
+      if (P.alias_kind[j] == AK_CONST && ++ncst > 1) { fit = false; break; }   // one constant row
       wrow[nw++] = j;
       kmax = cnt > kmax ? cnt : kmax;
     }
     if (fit && nw >= 2) {
-      if (kmax <= 8) pass_sweep_multi<8>(c, nw, wrow);
-      else if (kmax <= 12) pass_sweep_multi<12>(c, nw, wrow);
-      else pass_sweep_multi<MAX_K>(c, nw, wrow);
+      pass_sweep_multi(c, nw, wrow, kmax);
       return;
     }
   }
+  bool counted = false;
   for (int j = 0; j < m; ++j) {
     const int b = cmd.row_start[j], cnt = cmd.row_start[j + 1] - b;
     if (cnt <= 0) continue;
@@ -1545,11 +1821,14 @@ __device__ void pass_sweep(const PassCtx& c) {
     }
     // (10 / 12: the multi-row stage-1 sweeps, MAX_CAND / rows candidates per
     // row -- the per-element work is one select + add per template slot)
-    if (cnt <= 4) pass_sweep_row<4>(c, j, b, cnt);
-    else if (cnt <= 8) pass_sweep_row<8>(c, j, b, cnt);
-    else if (cnt <= 10) pass_sweep_row<10>(c, j, b, cnt);
-    else if (cnt <= 12) pass_sweep_row<12>(c, j, b, cnt);
-    else pass_sweep_row<MAX_K>(c, j, b, cnt);
+    // a sketch: the first row with candidates also counts the sampled elements
+    const int cslot = (cmd.sample && !counted) ? 2 * cmd.ncand : -1;
+    counted = counted || cslot >= 0;
+    if (cnt <= 4) pass_sweep_row<4>(c, j, b, cnt, cslot);
+    else if (cnt <= 8) pass_sweep_row<8>(c, j, b, cnt, cslot);
+    else if (cnt <= 10) pass_sweep_row<10>(c, j, b, cnt, cslot);
+    else if (cnt <= 12) pass_sweep_row<12>(c, j, b, cnt, cslot);
+    else pass_sweep_row<MAX_K>(c, j, b, cnt, cslot);
   }
   if (cmd.compact && c.list) {   // active elements left in this CTA
     __shared__ int s_woff[NWARP + 1];

@@ -164,6 +164,7 @@ struct Cmd {
   // PH_SWEEP active-set compaction: every candidate of row j lies in the
   // walk interval [wlo_j, whi_j]; elements whose clip region is the same at
   // both ends are folded into per-CTA fixed sums and dropped from the list.
+  int32_t pat_hint, pad_cmd2_;   // PH_PREP: the two-sweep pattern PREP (Problem::pat_hint)
   int32_t compact, local;        // local: sweep runs on the gathered items in each CTA
   int32_t load_fused;            // the items were published by the last global sweep:
                                  // every CTA loads them before the first local sweep
@@ -267,6 +268,11 @@ struct Problem {
   // root sketch (controller.h: consume_sketch): problems with at least this
   // many elements run sampled sweeps before the first full sweep (0: never)
   int64_t sketch_min_n;
+  // the previous step on these same buffers found pat7: PREP reads the rows
+  // in two sweeps and only VERIFIES rows 2, 4, 6 against -row 1, 3, 5 (their
+  // sums follow by exact sign flips); a failed verification re-runs the
+  // general PREP
+  int32_t pat_hint, pad_ph_;
 };
 enum RowKind { RK_DENSE = 0, RK_CONST = 1, RK_CENTROID = 2 };
 // Row structure detected in the data by PREP (dense rows, single rank).
@@ -278,6 +284,7 @@ struct Result {
   int32_t status, path, newton_iters, converged, curvature_violations;
   int32_t passes, sweeps, stage1_row, near_ties, fallback;
   int32_t local_sweeps, gathered;
+  int32_t pat7, pad_res_;             // PREP found the volume + 3 paired rows layout (Problem::pat7)
   int32_t final_phase, exact_passes;  // cmd.phase when the persistent kernel returned;
                                       // chain passes (strict parity)
   double active;            // active elements after the last compacted sweep
@@ -307,6 +314,7 @@ struct Plan {
   double hint_y[MAX_M], hint_sig[MAX_M];
   int32_t hint_ok[MAX_M];
   int32_t sketch_left, pad_sk_;       // sampled sweeps still to run before the full ones
+  double sk_T[MAX_M];                 // PREP's sum |a_i| max(|lo_i|, |hi_i|) (sampling-noise scale)
   // strict parity
   int32_t ghat_ex_ok;                 // g_hat dots below are reference-order exact
   int32_t nglobal;                    // grid-synchronized passes so far (partials buffer parity)

@@ -1,0 +1,11 @@
+# r02s: control-variate sketch + two-outlier fused sweep
+set -x
+O=gpurun_out/r02s
+mkdir -p $O
+TOPT_B200_FUSED_SWEEP=1 TOPT_B200_PERSISTENT=0 TOPT_B200_DEBUG_PHASES=2 timeout 200 python tools/prof_step.py --config C4 --seed 4 --steps 1 > $O/cands_c4.txt 2>&1
+for c in C4 C5; do
+  for f in 0 1; do TOPT_B200_FUSED_SWEEP=$f timeout 300 python tools/prof_step.py --trace $c > $O/trace_${c}_f$f.txt 2>&1; done
+done
+TOPT_B200_FUSED_SWEEP=1 TOPT_B200_SKETCH_MIN_N=1 timeout 900 python -m pytest tests/ -q -m gpu --timeout 200 -k "not c5 and not strict" -x > $O/pytest_forced.txt 2>&1; echo "rc=$?" >> $O/pytest_forced.txt
+TOPT_B200_FUSED_SWEEP=1 timeout 900 python -m pytest tests/test_gpu_full.py tests/test_gpu_parity.py tests/test_gpu_api.py -q --timeout 300 -k "not c5" > $O/pytest_fused.txt 2>&1; echo "rc=$?" >> $O/pytest_fused.txt
+echo done
