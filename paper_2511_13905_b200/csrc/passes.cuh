@@ -13,6 +13,7 @@
 //   term = a_i * clip(y * a_i, lo, hi)                  (:32, :35)
 //   z_i = sum_{j: y_j != 0} y_j a_ji, ascending j, from 0.0  (:199-205)
 #pragma once
+#include <type_traits>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -1196,15 +1197,141 @@ __device__ __forceinline__ void sweep_elem(double a, double r, const double* y, 
   (void)cnt;
 }
 
-// Most elements have no candidate inside their free window [bl, bh] (p1 ==
-// p2): every candidate then sees a clipped constant -- cl below the window,
-// ch above -- which costs one compare, one select pair and one add per
-// candidate.  The others are queued per warp and run through the full loop
-// 32 at a time, so no warp step is held by a few lanes.  The sums per
-// candidate get the same terms (in a different, still fixed, order).
+// Most elements have no candidate inside their free window [bl, bh] and none
+// between their two breakpoints' positions: every candidate then sees the
+// same clipped constant, or the element is free at every candidate -- one of
+// three running sums per lane.  The others are queued per warp (a, rho) and
+// run through the per-candidate evaluation 32 at a time, TRANSPOSED: lane l
+// owns candidate l & 15 and walks half (l >> 4) of the batch, reading the
+// queued elements from shared memory (broadcast) -- two accumulators per lane
+// for any number of candidates.  (One accumulator pair per candidate and lane,
+// the earlier layout, is 2 x 16 doubles per lane: pass_sweep_row<16> spilled
+// them to local memory inside the candidate loop; C5's first sweep spent 5 of
+// its 8.5 ms there.)  The sums per candidate get the same terms, in a
+// different, still fixed, order.
 constexpr int SQ_CAP = 64;   // NWARP * 2 * SQ_CAP doubles fit the reduction scratch
+static_assert(MAX_K <= 16, "the transposed candidate evaluation maps candidates to 16 lanes");
 template <int KC>
 struct SweepAcc {
+  double Cq, Sq;     // queued elements' sums at this lane's candidate (lane & 15)
+  double Sall;       // slopes of elements free at every candidate (p1 = 0, p2 = cnt)
+  double Clo, Chi;   // constants of elements clipped alike at every candidate
+  double y0, yl;     // the row's first and last candidate
+  double yk;         // this lane's candidate
+  double* qa;        // this warp's queue (shared memory, SQ_CAP entries)
+  double* qr;
+  int qn;
+  const double* y;
+  int cnt;
+  double L, U;
+  __device__ __forceinline__ void init(double* qa_, double* qr_, const double* y_, int cnt_,
+                                       double L_, double U_) {
+    Cq = 0.0; Sq = 0.0;
+    Sall = 0.0; Clo = 0.0; Chi = 0.0;
+    qa = qa_; qr = qr_; qn = 0; y = y_; cnt = cnt_; L = L_; U = U_;
+    y0 = y_[0]; yl = y_[cnt_ - 1];
+    const int k = threadIdx.x & 15;
+    yk = y_[k < cnt_ ? k : cnt_ - 1];
+  }
+  // entries [from, from + nq) of the queue at every candidate (all 32 lanes)
+  __device__ __forceinline__ void batch(int from, int nq) {
+    const int half = (threadIdx.x & 31) >> 4;
+#pragma unroll 4
+    for (int e = 0; e < 16; ++e) {
+      const int idx = half * 16 + e;
+      if (idx < nq) {   // (uniform within each half-warp)
+        const double a = qa[from + idx], r = qr[from + idx];
+        const double lo = L - r, hi = U - r;
+        const double ra = rcp_full(a);
+        const double b1 = lo * ra, b2 = hi * ra;
+        const bool pos = a > 0.0;
+        const double bl = pos ? b1 : b2, bh = pos ? b2 : b1;
+        const double cl = a * (pos ? lo : hi), ch = a * (pos ? hi : lo), aa = a * a;
+        const bool below = yk < bl, above = !(yk <= bh);
+        Cq += below ? cl : (above ? ch : 0.0);
+        Sq += (below || above) ? 0.0 : aa;
+      }
+    }
+  }
+  // all 32 lanes call push together (valid = this lane holds an element)
+  __device__ __forceinline__ void push(bool valid, double a, double r) {
+    const int lane = threadIdx.x & 31;
+    bool need = false;
+    if (valid && a != 0.0) {
+      const double lo = L - r, hi = U - r;
+      const double ra = rcp_full(a);
+      const double b1 = lo * ra, b2 = hi * ra;
+      const bool pos = a > 0.0;
+      const double bl = pos ? b1 : b2, bh = pos ? b2 : b1;
+      // window endpoints decide most elements without a search: both
+      // breakpoints outside (y_0, y_last] means p1, p2 in {0, cnt}
+      const bool outl = bl <= y0 || bl > yl, outh = bh < y0 || bh >= yl;
+      if (outl && outh) {
+        const bool p1z = !(bl > yl), p2z = !(bh >= yl);   // p1 == 0, p2 == 0
+        if (p1z == p2z) {
+          // clipped alike at every candidate: one sum, added to every C_k at
+          // the end, instead of a select + add per candidate
+          if (p1z) Chi += a * (pos ? hi : lo);
+          else Clo += a * (pos ? lo : hi);
+        } else if (p1z) {
+          // free at every candidate (a small |a| makes the window wide): its
+          // term is y_k a^2 for all k -- one slope sum
+          Sall += a * a;
+        } else {
+          need = true;
+        }
+      } else {
+        need = true;   // a breakpoint inside the window: the per-candidate evaluation
+      }
+    }
+    const unsigned nm = __ballot_sync(0xffffffffu, need);
+    if (nm) {
+      if (need) {
+        const int slot = qn + __popc(nm & ((1u << lane) - 1u));
+        qa[slot] = a;
+        qr[slot] = r;
+      }
+      qn += __popc(nm);
+      __syncwarp();
+      if (qn >= 32) {
+        batch(qn - 32, 32);
+        qn -= 32;
+        __syncwarp();
+      }
+    }
+  }
+  // Drain the queue and leave this warp's (R_k, S_k) pairs, k < 16, in
+  // out32[2k], out32[2k + 1] (shared memory; may alias the queue).
+  __device__ __forceinline__ void finish(double* out32) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    if (qn > 0) batch(0, qn);
+    qn = 0;
+    __syncwarp();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {   // fixed xor tree: every lane gets the warp's sums
+      Sall += __shfl_xor_sync(0xffffffffu, Sall, o);
+      Clo += __shfl_xor_sync(0xffffffffu, Clo, o);
+      Chi += __shfl_xor_sync(0xffffffffu, Chi, o);
+    }
+    const double C2 = Cq + __shfl_down_sync(0xffffffffu, Cq, 16);
+    const double S2 = Sq + __shfl_down_sync(0xffffffffu, Sq, 16);
+    if (lane < 16) {
+      const double Sk = S2 + Sall, Ck = (C2 + Chi) + Clo;
+      out32[2 * lane] = Ck + yk * Sk;   // r_k = C_k + y_k S_k
+      out32[2 * lane + 1] = Sk;
+    }
+    __syncwarp();
+  }
+};
+
+// The per-lane layout (one accumulator pair per candidate and lane): fewer
+// instructions per queued element than the transposed batch, but 2 KC + 5
+// live doubles -- used for the WIDE sweeps (a walk's first full sweep and the
+// sketches, where a large share of the elements has a breakpoint inside the
+// window), one pair of loads in flight so the accumulators stay in registers.
+template <int KC>
+struct SweepAccW {
   double C[KC], S[KC];
   double Sall;   // slopes of elements free at every candidate (p1 = 0, p2 = cnt)
   double Clo, Chi;   // constants of elements clipped alike at every candidate
@@ -1308,7 +1435,7 @@ __device__ __forceinline__ void sweep_finish(const double* y, int cnt, double* C
 // cmd.sample = s > 0 (a sketch, controller.h: consume_sketch): only every
 // 2^s-th step of the loop below runs; `count_slot` >= 0 then receives the
 // number of elements visited.
-template <int KC>
+template <int KC, bool WIDE>
 __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int cnt,
                                             int count_slot = -1) {
   const Problem& P = c.plan->P;
@@ -1324,7 +1451,7 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
   const int8_t* __restrict__ owner = P.owner;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // the warps' queues live in the reduction scratch (free until the end)
-  SweepAcc<KC> acc;
+  typename std::conditional<WIDE, SweepAccW<KC>, SweepAcc<KC>>::type acc;
   acc.init(c.smem + warp * 2 * SQ_CAP, c.smem + warp * 2 * SQ_CAP + SQ_CAP, c.cmd->cand_y + b,
            cnt, P.lower, P.upper);
   StreamRows R;
@@ -1348,6 +1475,26 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
     for (int64_t q0 = (rlo >> 1) + c.i0 - lane; q0 < n2; q0 += (2 * st) << shift) {
       const int64_t qa = q0 + lane, qb = q0 + st + lane;
       const bool oa = qa < n2, ob = qb < n2;
+      if (WIDE) {   // one pair at a time (same elements, same order per lane)
+        visited += (double)(2 * ((int)oa + (int)ob));
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          const int64_t qq = h ? qb : qa;
+          const bool oo = h ? ob : oa;
+          double2 av = (oo && !gen && !cst) ? A2[qq] : make_double2(cv, cv);
+          const double2 rv = oo ? R2[qq] : make_double2(0.0, 0.0);
+          if (gen && oo) {
+            int64_t c0[3], c1[3];
+            grid_coords(G, 2 * qq + G.off, c0);
+            grid_coords(G, 2 * qq + 1 + G.off, c1);
+            av = make_double2(srow_fetch(c.rtab, gcode, c0), srow_fetch(c.rtab, gcode, c1));
+          }
+          if (shift) r0s += term0(oo, av.x, rv.x) + term0(oo, av.y, rv.y);
+          acc.push(oo, av.x, rv.x);
+          acc.push(oo, av.y, rv.y);
+        }
+        continue;
+      }
       visited += (double)(2 * ((int)oa + (int)ob));
       double2 a0 = (oa && !gen && !cst) ? A2[qa] : make_double2(cv, cv);
       double2 a1 = (ob && !gen && !cst) ? A2[qb] : make_double2(cv, cv);
@@ -1394,13 +1541,27 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
     for (int u = 0; u < UL; ++u) acc.push(ok[u], av[u], rv[u]);
   }
   }
-  acc.flush();
-  __syncthreads();   // queues (in c.smem) drained before the reduction reuses it
-  sweep_finish<KC>(acc.y, cnt, acc.C, acc.S);
-  double v[2 * KC];
+  if constexpr (WIDE) {
+    acc.flush();
+    __syncthreads();   // queues (in c.smem) drained before the reduction reuses it
+    sweep_finish<KC>(acc.y, cnt, acc.C, acc.S);
+    double v[2 * KC];
 #pragma unroll
-  for (int k = 0; k < KC; ++k) { v[2 * k] = acc.C[k]; v[2 * k + 1] = acc.S[k]; }
-  block_reduce_store<2 * KC>(v, 2 * cnt, PH_SWEEP, 2 * b, c.out, c.smem);
+    for (int k = 0; k < KC; ++k) { v[2 * k] = acc.C[k]; v[2 * k + 1] = acc.S[k]; }
+    block_reduce_store<2 * KC>(v, 2 * cnt, PH_SWEEP, 2 * b, c.out, c.smem);
+  } else {
+  // per warp (R_k, S_k) into the head of its own queue region, then the
+  // warps in order (the second stage of block_reduce_store)
+  acc.finish(c.smem + warp * 2 * SQ_CAP);
+  __syncthreads();
+  if (threadIdx.x < 2 * cnt) {
+    const int sl = threadIdx.x;
+    double r = c.smem[sl];
+    for (int w = 1; w < NWARP; ++w) r += c.smem[w * 2 * SQ_CAP + sl];
+    c.out[2 * b + sl] = r;
+  }
+  __syncthreads();
+  }
   if (shift) {   // sketch slots: [2 ncand] elements visited, [2 ncand + 1 + j] row j's sampled r(0) sum
     const double cv1[1] = {r0s};
     block_reduce_store<1>(cv1, 1, PH_SWEEP, 2 * c.cmd->ncand + 1 + j, c.out, c.smem);
@@ -1824,11 +1985,17 @@ __device__ void pass_sweep(const PassCtx& c) {
     // a sketch: the first row with candidates also counts the sampled elements
     const int cslot = (cmd.sample && !counted) ? 2 * cmd.ncand : -1;
     counted = counted || cslot >= 0;
-    if (cnt <= 4) pass_sweep_row<4>(c, j, b, cnt, cslot);
-    else if (cnt <= 8) pass_sweep_row<8>(c, j, b, cnt, cslot);
-    else if (cnt <= 10) pass_sweep_row<10>(c, j, b, cnt, cslot);
-    else if (cnt <= 12) pass_sweep_row<12>(c, j, b, cnt, cslot);
-    else pass_sweep_row<MAX_K>(c, j, b, cnt, cslot);
+    // a walk's first full sweep and the sketches have wide windows: the
+    // per-lane candidate loop; later sweeps: the lean transposed batch
+    if (cmd.sample || c.plan->res.sweeps <= 1) {
+      if (cnt <= 4) pass_sweep_row<4, true>(c, j, b, cnt, cslot);
+      else if (cnt <= 8) pass_sweep_row<8, true>(c, j, b, cnt, cslot);
+      else if (cnt <= 10) pass_sweep_row<10, true>(c, j, b, cnt, cslot);
+      else if (cnt <= 12) pass_sweep_row<12, true>(c, j, b, cnt, cslot);
+      else pass_sweep_row<MAX_K, true>(c, j, b, cnt, cslot);
+    } else {
+      pass_sweep_row<MAX_K, false>(c, j, b, cnt, cslot);
+    }
   }
   if (cmd.compact && c.list) {   // active elements left in this CTA
     __shared__ int s_woff[NWARP + 1];
