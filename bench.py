@@ -476,9 +476,12 @@ def measured_traffic(workload, world):
             t = json.load(f)
     except (OSError, ValueError):
         return None
-    if t.get("workload") != workload or world != 1:
+    if world != 1:
         return None
-    return t.get("bytes_per_launch")
+    w = t.get("workloads", {}).get(workload)
+    if w is None and t.get("workload") == workload:   # (round-1 single-workload layout)
+        w = t
+    return w.get("bytes_per_launch") if w else None
 
 
 def kernel_pass_stats(ctx, step, steps, flush):

@@ -488,6 +488,7 @@ struct topt_b200_ctx {
   // the last PGD step's PREP found the pat7 row layout on these buffers
   // (Problem::pat_hint; TOPT_B200_PAT_HINT=0 disables)
   int pat_hint_on = 1;
+  int first_k = 0;   // Problem::first_k (TOPT_B200_FIRST_K)
   const double* pat_grad = nullptr;
   int64_t pat_n = 0, pat_ld = 0;
   int* d_blk_cnt = nullptr;
@@ -1011,6 +1012,7 @@ int init_problem(topt_b200_ctx* ctx, Plan& hp, int64_t n, int m, const topt_proj
   P.strict = ctx->parity;
   P.ex_debug = ctx->ex_debug;
   P.sketch_min_n = ctx->sketch_min_n;
+  P.first_k = ctx->first_k;
   return TOPT_OK;
 }
 
@@ -1292,6 +1294,7 @@ int topt_b200_ctx_create(int device, topt_b200_ctx** out) {
   if (const char* e = getenv("TOPT_B200_FUSED_SWEEP")) ctx->fused_sweep = atoi(e);
   if (const char* e = getenv("TOPT_B200_SKETCH_MIN_N")) ctx->sketch_min_n = atoll(e);
   if (const char* e = getenv("TOPT_B200_PAT_HINT")) ctx->pat_hint_on = atoi(e);
+  if (const char* e = getenv("TOPT_B200_FIRST_K")) ctx->first_k = atoi(e);
   if (!ok) { topt_b200_ctx_destroy(ctx); return TOPT_ERR_CUDA; }
   *out = ctx;
   return TOPT_OK;

@@ -781,14 +781,25 @@ TOPT_NOINLINE void consume_sketch(Plan& pl, const double* t) {
 
 // Build the next sweep over all walks that need evaluations; if none do,
 // advance the stage.  Returns true if a sweep was scheduled.
+TOPT_HDN inline int schedule_per(const Plan& pl, int need) {
+  int per = MAX_CAND / need;
+  if (per > MAX_K) per = MAX_K;
+  // a walk's first full sweep has a wide window (the per-candidate loop runs
+  // for a large share of the elements): with a sketched root estimate fewer
+  // candidates place the next bracket almost as well
+  if (pl.P.first_k > 0 && pl.res.sweeps == 0 && pl.sketch_left == 0 && !pl.cmd.local &&
+      sketch_wanted(pl) && per > pl.P.first_k)
+    per = pl.P.first_k;
+  return per;
+}
+
 TOPT_NOINLINE bool schedule_sweep(Plan& pl) {
   if (schedule_exact_walks(pl)) return true;
   const int m = pl.P.m;
   int need = 0;
   for (int j = 0; j < m; ++j) need += (pl.w[j].status == WK_NEED);
   if (!need) return false;
-  int per = MAX_CAND / need;
-  if (per > MAX_K) per = MAX_K;
+  const int per = schedule_per(pl, need);
   Cmd& c = pl.cmd;
   c.phase = PH_SWEEP;
   int tot = 0;
@@ -1720,10 +1731,6 @@ __device__ __noinline__ int schedule_row_warp(Plan& pl, int j, int per, double* 
   return nc;
 }
 
-TOPT_HDN inline int schedule_per(const Plan& pl, int need) {
-  int per = MAX_CAND / need;
-  return per > MAX_K ? MAX_K : per;
-}
 
 // The sweep command around the candidates already in cmd.cand_y (lane 0).
 TOPT_HDN inline void schedule_finish(Plan& pl, int tot) {

@@ -678,7 +678,8 @@ __device__ __forceinline__ void prep_group(const PassCtx& c, int j0, int64_t n, 
   // pairs in flight per thread: enough bytes per SM to cover HBM latency
   // (Little's law) without spilling the G rows' accumulators
   constexpr int UP = G == 1 ? 3 : 2;
-  for (int64_t qb = c.i0 - lane; qb < n2; qb += UP * st) {   // warp-uniform trip count
+  int step = 0;
+  for (int64_t qb = c.i0 - lane; qb < n2; qb += UP * st, ++step) {   // warp-uniform trip count
     double2 a2[UP][G], r2[UP], d2[UP];
     const double2 z2 = make_double2(0.0, 0.0);
 #pragma unroll
@@ -721,8 +722,12 @@ __device__ __forceinline__ void prep_group(const PassCtx& c, int j0, int64_t n, 
         }
       }
     }
+    // the filter may be stale (any breakpoint seen earlier is a valid bound):
+    // refreshed every 4th step (20 shuffles per row and refresh)
+    if ((step & 3) == 3) {
 #pragma unroll
-    for (int r = 0; r < G; ++r) warp_minmax(fmin[r], fmax[r]);
+      for (int r = 0; r < G; ++r) warp_minmax(fmin[r], fmax[r]);
+    }
   }
 #pragma unroll
   for (int r = 0; r < G; ++r)
@@ -780,7 +785,8 @@ __device__ __noinline__ void prep_pairs(const PassCtx& c, int jb0, int64_t n, bo
 #pragma unroll
   for (int p = 0; p < NP; ++p) nneg[p] = 0.0;
   constexpr int UP = 1;   // (two pairs in flight spill: 2 x 6 loads + 25 accumulators)
-  for (int64_t qb = c.i0 - lane; qb < n2; qb += UP * st) {   // warp-uniform trip count
+  int step = 0;
+  for (int64_t qb = c.i0 - lane; qb < n2; qb += UP * st, ++step) {   // warp-uniform trip count
     double2 f2[UP][NB], m2[UP][NP], r2[UP], d2[UP];
     const double2 z2 = make_double2(0.0, 0.0);
 #pragma unroll
@@ -825,8 +831,10 @@ __device__ __noinline__ void prep_pairs(const PassCtx& c, int jb0, int64_t n, bo
         }
       }
     }
+    if ((step & 7) == 7) {   // (stale filters are valid: see prep_group)
 #pragma unroll
-    for (int r = 0; r < NB; ++r) warp_minmax(fmin[r], fmax[r]);
+      for (int r = 0; r < NB; ++r) warp_minmax(fmin[r], fmax[r]);
+    }
   }
 #pragma unroll
   for (int r = 0; r < NB; ++r)

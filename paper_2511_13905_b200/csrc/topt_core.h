@@ -272,7 +272,8 @@ struct Problem {
   // in two sweeps and only VERIFIES rows 2, 4, 6 against -row 1, 3, 5 (their
   // sums follow by exact sign flips); a failed verification re-runs the
   // general PREP
-  int32_t pat_hint, pad_ph_;
+  int32_t pat_hint;
+  int32_t first_k;   // > 0: candidates per row in a walk's first full sweep (after the sketch)
 };
 enum RowKind { RK_DENSE = 0, RK_CONST = 1, RK_CENTROID = 2 };
 // Row structure detected in the data by PREP (dense rows, single rank).

@@ -79,12 +79,27 @@ def _certified_vs_summary(name, seed):
     pr = st.projection
     assert pr.path.name == g["path"]
     assert st.alpha == pytest.approx(g["alpha"], rel=1e-13)
-    np.testing.assert_allclose(st.y, g["y"], rtol=1e-9, atol=1e-9)
-    assert hashlib.sha256(st.mask.tobytes()).hexdigest() == g["mask_sha256"]
     x = st.x_new
-    # x within 1e-12 normwise elementwise sums to within n * 1e-12 max|x|
-    assert abs(float(np.sum(x)) - g["x_sum"]) <= 1e-12 * x.size
-    assert abs(float(np.sum(x * x)) - g["x_sq"]) <= 3e-12 * x.size
+    if g["converged"]:
+        np.testing.assert_allclose(st.y, g["y"], rtol=1e-9, atol=1e-9)
+        assert hashlib.sha256(st.mask.tobytes()).hexdigest() == g["mask_sha256"]
+        # x within 1e-12 normwise elementwise sums to within n * 1e-12 max|x|
+        assert abs(float(np.sum(x)) - g["x_sum"]) <= 1e-12 * x.size
+        assert abs(float(np.sum(x * x)) - g["x_sq"]) <= 3e-12 * x.size
+    else:
+        # The reference ran to its iteration cap and stopped AWAY from the
+        # projection: its sequentially summed ||Phi|| stalls on rounding noise
+        # (C5: reported residual 8.1e-4 >> tol_n).  Its duals are then only
+        # residual-accurate, so certified mode (which converges) is compared at
+        # that accuracy; strict mode reproduces the stalled run bit for bit
+        # (tests/test_gpu_strict.py).
+        assert g["residual"] > TOL_N and g["newton_iters"] == 50
+        yr = np.asarray(g["y"])
+        assert np.max(np.abs(st.y - yr)) <= 5e-2 * np.max(np.abs(yr))
+        assert (st.y != 0.0).tolist() == (yr != 0.0).tolist()      # same active rows
+        nl, nu = int((st.mask == 1).sum()), int((st.mask == 2).sum())
+        assert abs(nl - g["n_lower"]) <= 1e-4 * x.size and abs(nu - g["n_upper"]) <= 1e-4 * x.size
+        assert abs(float(np.sum(x)) - g["x_sum"]) <= 1e-6 * x.size
     if g["path"] == "newton":
         # certified mode stops where ||Phi|| <= tol_n for accurately summed h;
         # the reference stops on its sequentially summed (noisy) ||Phi||, so
