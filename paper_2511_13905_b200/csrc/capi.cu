@@ -39,7 +39,22 @@ constexpr size_t KPASS_SMEM = PLAN_SMEM;   // + the structured-row tables
 // addition order unchanged); groups combine in order.  The order depends only
 // on (nb, ns): deterministic.
 __device__ void finish_reduce(const double* partials, int nb, int ns, int phase,
-                              double* totals, double* smem, int stride = PMAX) {
+                              double* totals, double* smem, int stride = PMAX);
+// FEAS with Newton's first evaluation appended (cmd.feas_gram0): the appended
+// slots are combined on their own, i.e. in the CTA grouping a NEWTON pass of
+// the same slot count uses, so the evaluation has the bits that pass would give.
+__device__ void finish_reduce_cmd(const double* partials, int nb, const topt_b200::Cmd& cmd,
+                                  int m, double* totals, double* smem) {
+  if (cmd.phase == topt_b200::PH_FEAS && cmd.feas_gram0) {
+    const int n1 = cmd.nfeas * m;
+    finish_reduce(partials, nb, n1, cmd.phase, totals, smem);
+    finish_reduce(partials + n1, nb, cmd.nslots - n1, cmd.phase, totals + n1, smem);
+    return;
+  }
+  finish_reduce(partials, nb, cmd.nslots, cmd.phase, totals, smem);
+}
+__device__ void finish_reduce(const double* partials, int nb, int ns, int phase,
+                              double* totals, double* smem, int stride) {
   for (int s0 = 0; s0 < ns; s0 += BLOCK) {
     const int per = min(ns - s0, BLOCK);
     // G groups of CTAs per slot: ~sqrt(nb) balances the load chain (nb / G
@@ -156,7 +171,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_pass(Plan* plan, double* partials,
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  finish_reduce(partials, gridDim.x, s_cmd.nslots, s_cmd.phase, s_tot, s_red);
+  finish_reduce_cmd(partials, gridDim.x, s_cmd, plan->P.m, s_tot, s_red);
   if (totals) {   // rank mode: publish this rank's totals, no control here
     for (int s = threadIdx.x; s < s_cmd.nslots; s += BLOCK) totals[s] = s_tot[s];
   } else {
@@ -326,7 +341,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_step(Plan* plan, double* partials,
                (long long)sp.P.ex_seg, sp.P.ex_nst, sp.cmd.wa, s_tot[0],
                sp.cmd.ex_n > 1 ? s_tot[1] : 0.0);
     } else {
-      finish_reduce(part, nb, sp.cmd.nslots, sp.cmd.phase, s_tot, s_red);
+      finish_reduce_cmd(part, nb, sp.cmd, sp.P.m, s_tot, s_red);
     }
     progress_mark(3, pass);
     if (threadIdx.x == 0) sp.nglobal++;   // (read again only after the controller's barrier)
@@ -484,11 +499,15 @@ struct topt_b200_ctx {
   // root sketch (controller.h: consume_sketch): sampled sweeps before the first
   // full sweep for problems of at least this many elements (0: never;
   // TOPT_B200_SKETCH_MIN_N)
-  int64_t sketch_min_n = (int64_t)1 << 25;
+  int64_t sketch_min_n = (int64_t)1 << 22;
   // the last PGD step's PREP found the pat7 row layout on these buffers
   // (Problem::pat_hint; TOPT_B200_PAT_HINT=0 disables)
   int pat_hint_on = 1;
-  int first_k = 0;   // Problem::first_k (TOPT_B200_FIRST_K)
+  // candidates per row in a walk's first full sweep after the sketch
+  // (Problem::first_k, TOPT_B200_FIRST_K; r02y: 8 instead of 16 takes C5's
+  // first sweep from 8.5 to 6.2 ms and C4's from 449 to 330 us; the third
+  // sweep then uses its spare candidates)
+  int first_k = 8;
   const double* pat_grad = nullptr;
   int64_t pat_n = 0, pat_ld = 0;
   int* d_blk_cnt = nullptr;

@@ -977,6 +977,12 @@ TOPT_HDN inline void schedule_feas(Plan& pl) {
   }
   c.nfeas = nf;
   c.nslots = nf * m;
+  // The FEAS pass of the detected C4/C5 row layout reads exactly what
+  // Newton's first evaluation (y = 0, projection.cpp:345-357) reads: it
+  // returns that evaluation too, and a Newton solve that follows starts from
+  // it without a pass of its own.
+  c.feas_gram0 = (pl.P.pat7 && !pl.P.strict && nf > 0) ? 1 : 0;
+  if (c.feas_gram0) c.nslots += m + m * (m + 1) / 2;
   pl.stage = SG_FEAS;
   if (nf == 0) start_newton(pl);
 }
@@ -1017,6 +1023,20 @@ TOPT_NOINLINE void consume_feas(Plan& pl, const double* t) {
       cmd_final(pl, y, 0);
       return;
     }
+  }
+  if (pl.cmd.feas_gram0 && pl.cmd.phase == PH_FEAS) {
+    // Newton's evaluation at y = 0 came with the FEAS pass: consume it as if
+    // a PH_NEWTON pass had returned it (scalar m x m solve: same pivots and
+    // arithmetic as the warp version)
+    const double* t0 = t + pl.cmd.nfeas * m;
+    Newton& nt = pl.nt;
+    Newton z = {};
+    nt = z;
+    nt.in_linesearch = 0;
+    pl.stage = SG_NEWTON;
+    pl.cmd.feas_gram0 = 0;
+    consume_newton(pl, t0);
+    return;
   }
   start_newton(pl);
 }

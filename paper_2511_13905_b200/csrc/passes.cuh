@@ -2680,7 +2680,16 @@ __device__ __noinline__ void pass_feas_pat7(const PassCtx& c) {
   const int64_t n2 = P.n >> 1, st = c.stride, ld2 = P.ld >> 1;
   const double2* __restrict__ R2 = reinterpret_cast<const double2*>(P.rho);
   const double2* __restrict__ A2 = reinterpret_cast<const double2*>(P.grad);
+  // cmd.feas_gram0: Newton's first evaluation (y = 0) rides on the first
+  // group's sweep -- h-dots of clip(0, lo, hi) and the free-set Gram of the 4
+  // distinct rows, exactly pass_newton_pat7's per-element arithmetic at y = 0
+  double h0[NB], G0[NB * (NB + 1) / 2];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) h0[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < NB * (NB + 1) / 2; ++k) G0[k] = 0.0;
   for (int f0 = 0; f0 < cmd.nfeas; f0 += FEAS_GROUP) {
+    const bool gram0 = cmd.feas_gram0 && f0 == 0;
     const int ng = cmd.nfeas - f0 < FEAS_GROUP ? cmd.nfeas - f0 : FEAS_GROUP;
     int frow[FEAS_GROUP];     // the group's candidates in registers
     double fy[FEAS_GROUP];
@@ -2714,6 +2723,19 @@ __device__ __noinline__ void pass_feas_pat7(const PassCtx& c) {
 #pragma unroll
         for (int k = 0; k < NB; ++k) acc[g][k] += b[k] * dl;
       }
+      if (gram0) {
+        const bool clipped = (0.0 < lo) || (0.0 > hi);
+        const double dl = clipd(0.0, lo, hi);
+#pragma unroll
+        for (int k = 0; k < NB; ++k) h0[k] += b[k] * dl;
+        if (!clipped) {
+          int qq = 0;
+#pragma unroll
+          for (int j = 0; j < NB; ++j)
+#pragma unroll
+            for (int k = j; k < NB; ++k) { G0[qq] = __fma_rn(b[j], b[k], G0[qq]); ++qq; }
+        }
+      }
     };
     int64_t q = c.i0;
     for (; q + st < n2; q += 2 * st) {   // two pairs in flight (see pass_newton_pat7)
@@ -2739,6 +2761,24 @@ __device__ __noinline__ void pass_feas_pat7(const PassCtx& c) {
       for (int k = 0; k < M; ++k) vv[k] = p7_neg(k) ? -acc[g][bi[k]] : acc[g][bi[k]];
       block_reduce_store<M>(vv, M, PH_FEAS, (f0 + g) * M, c.out, c.smem);
     }
+  }
+  if (cmd.feas_gram0) {   // expand to the m = 7 layout: 7 h-dots, then the packed 28-entry Gram
+    constexpr int NG = M * (M + 1) / 2;
+    const int bi[M] = {0, 1, 1, 2, 2, 3, 3};
+    double vv[M + NG];
+#pragma unroll
+    for (int k = 0; k < M; ++k) vv[k] = p7_neg(k) ? -h0[bi[k]] : h0[bi[k]];
+    int sidx = 0;
+#pragma unroll
+    for (int j = 0; j < M; ++j)
+#pragma unroll
+      for (int k = j; k < M; ++k) {
+        const int x = bi[j] < bi[k] ? bi[j] : bi[k], y = bi[j] < bi[k] ? bi[k] : bi[j];
+        const int gi = x * NB - x * (x - 1) / 2 + (y - x);
+        vv[M + sidx] = (p7_neg(j) != p7_neg(k)) ? -G0[gi] : G0[gi];
+        ++sidx;
+      }
+    block_reduce_store<M + NG>(vv, M + NG, PH_FEAS, cmd.nfeas * M, c.out, c.smem);
   }
 }
 

@@ -164,7 +164,9 @@ struct Cmd {
   // PH_SWEEP active-set compaction: every candidate of row j lies in the
   // walk interval [wlo_j, whi_j]; elements whose clip region is the same at
   // both ends are folded into per-CTA fixed sums and dropped from the list.
-  int32_t pat_hint, pad_cmd2_;   // PH_PREP: the two-sweep pattern PREP (Problem::pat_hint)
+  int32_t pat_hint;              // PH_PREP: the two-sweep pattern PREP (Problem::pat_hint)
+  int32_t feas_gram0;            // PH_FEAS: also return Newton's first evaluation (y = 0):
+                                 // m h-dots and the packed free-set Gram after the nfeas * m dots
   int32_t compact, local;        // local: sweep runs on the gathered items in each CTA
   int32_t load_fused;            // the items were published by the last global sweep:
                                  // every CTA loads them before the first local sweep
