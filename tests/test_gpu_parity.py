@@ -63,6 +63,18 @@ def test_projection_full(name, seed):
     assert res.bisect_iters[0] == orc["bisect_iters"][0]
 
 
+@pytest.mark.parametrize("kind", ["volume", "compliance"])
+def test_projection_sketched_single_row(kind):
+    """Single-row problems large enough for the root sketch (>= 2^22 elements:
+    sampled sweeps, the 8-candidate first sweep, then the compacted sweeps):
+    y and delta still bit-identical to the oracle, same bisection iterations."""
+    p = (synth.min_compliance_volume(4096, 2048, 7) if kind == "volume"
+         else synth.min_volume_compliance(2048, 4096, 8))
+    assert p.n >= 1 << 22
+    res, orc = check_projection(p)
+    assert res.bisect_iters[0] == orc["bisect_iters"][0]
+
+
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C4p"])
 def test_pgd_step_small(name):
     p = synth.SMALL[name](7)
