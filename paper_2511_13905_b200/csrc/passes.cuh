@@ -268,6 +268,10 @@ __device__ __forceinline__ void prefetch_l2(const void* base, int64_t off_bytes,
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((unsigned)bytes) : "memory");
 }
 
+__device__ __forceinline__ void prefetch_line_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // ---- Row-pair streaming -------------------------------------------------------
 // Passes that read several element-aligned rows (rho, A rows, x, g, ...) for
 // every element load them as 16-byte pairs: each thread takes element pairs
@@ -787,6 +791,24 @@ __device__ __noinline__ void prep_pairs(const PassCtx& c, int jb0, int64_t n, bo
   constexpr int UP = 1;   // (two pairs in flight spill: 2 x 6 loads + 25 accumulators)
   int step = 0;
   for (int64_t qb = c.i0 - lane; qb < n2; qb += UP * st, ++step) {   // warp-uniform trip count
+    {   // the next step's lines into L2 (one lane per 128-byte line, no registers held):
+        // one pair in flight per thread does not cover the HBM latency by itself
+      const int64_t qn = qb + 2 * UP * st + lane;   // two steps ahead
+      if ((lane & 7) == 0 && qn < n2) {
+#pragma unroll
+        for (int r = 0; r < NB; ++r) prefetch_line_l2(F2[r] + qn);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) prefetch_line_l2(N2[p] + qn);
+        if (FUSE0) {
+          prefetch_line_l2(G2 + qn);
+          if (use_dp) prefetch_line_l2(P2 + qn);
+          prefetch_line_l2(X2 + qn);
+        } else {
+          prefetch_line_l2(R2 + qn);
+          if (dot) prefetch_line_l2(D2 + qn);
+        }
+      }
+    }
     double2 f2[UP][NB], m2[UP][NP], r2[UP], d2[UP];
     const double2 z2 = make_double2(0.0, 0.0);
 #pragma unroll
@@ -1449,6 +1471,7 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
   const Problem& P = c.plan->P;
   const int64_t n = P.n, st = c.stride;
   const int shift = c.cmd->sample;
+  const bool pf_l2 = n >= ((int64_t)1 << 22);   // (an L2-resident problem gains nothing: C2 + 2 us)
   double visited = 0.0, r0s = 0.0;   // sketch: elements visited, their sum of a clip(0, lo, hi)
   auto term0 = [&](bool ok, double a, double r) {
     const double lo = P.lower - r, hi = P.upper - r;
@@ -1483,6 +1506,17 @@ __device__ __noinline__ void pass_sweep_row(const PassCtx& c, int j, int b, int 
     for (int64_t q0 = (rlo >> 1) + c.i0 - lane; q0 < n2; q0 += (2 * st) << shift) {
       const int64_t qa = q0 + lane, qb = q0 + st + lane;
       const bool oa = qa < n2, ob = qb < n2;
+      if (pf_l2 && (lane & 7) == 0) {   // the next step's lines into L2 (see prep_pairs)
+        const int64_t na = qa + ((2 * st) << shift), nb2 = na + st;
+        if (na < n2) {
+          prefetch_line_l2(R2 + na);
+          if (!gen && !cst) prefetch_line_l2(A2 + na);
+        }
+        if (nb2 < n2) {
+          prefetch_line_l2(R2 + nb2);
+          if (!gen && !cst) prefetch_line_l2(A2 + nb2);
+        }
+      }
       if (WIDE) {   // one pair at a time (same elements, same order per lane)
         visited += (double)(2 * ((int)oa + (int)ob));
 #pragma unroll 1
